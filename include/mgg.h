@@ -1,0 +1,343 @@
+/*
+ * mgg.h — C-ABI of the B200-native MGG hot path (libmgg.so).
+ *
+ * Plain C types only: pointers, sizes, status codes. No exceptions, no torch
+ * types. Every call returns an int status (0 OK, 1 INPUT, 2 PARSE, 3 CONFIG,
+ * 4 INTEGRITY, 5 CUDA — the reference's exception taxonomy,
+ * R:proj/include/pipeshard/errors.hpp:26-59, plus CUDA) and mgg_last_error()
+ * returns the thread-local message of the last failure.
+ *
+ * Two layers:
+ *
+ *  A. The thin CUDA layer ("device runtime"): contexts, symmetric
+ *     peer-mapped embedding stores, device plans, and the kernels — K1
+ *     pipelined aggregation, K2 Update GEMM, K3 cross-GPU barrier. The C++
+ *     host engine (include/mgg/engine.hpp) drives the GPU only through these.
+ *     Together they replace the reference's execution model
+ *     `simulate(plan, hw, dim, mode)` (R:proj/include/pipeshard/sim.hpp:91-93)
+ *     and the per-GPU loop of `multi_gpu_run` (R:proj/src/sim.cpp:597-624).
+ *
+ *  B. Host facade for non-C++ callers (Python/ctypes, cgo, JNI): graph
+ *     ingestion, the Alg. 1 split, the neighbor-partition builder, the cost
+ *     model, the tuner, and the GCN/GIN engine. Each entry cites the
+ *     reference interface it stands in for.
+ *
+ * Ownership: handles are library-owned (free with the matching *_destroy);
+ * host arrays are caller-owned and only read/written during the call.
+ * Threading: a context and everything created from it must be driven by one
+ * host thread at a time; distinct contexts are independent.
+ */
+#ifndef MGG_H_
+#define MGG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MGG_OK = 0,
+  MGG_E_INPUT = 1,
+  MGG_E_PARSE = 2,
+  MGG_E_CONFIG = 3,
+  MGG_E_INTEGRITY = 4,
+  MGG_E_CUDA = 5
+};
+
+const char* mgg_last_error(void);
+const char* mgg_version(void);
+/* 1 if a CUDA device is visible, 0 otherwise (never fails). */
+int mgg_cuda_available(void);
+/* Frees memory the library returned (JSON strings, CSV). */
+void mgg_free(void* p);
+
+/* ======================================================================= */
+/* A. device runtime                                                        */
+/* ======================================================================= */
+
+typedef struct mgg_ctx mgg_ctx;
+typedef struct mgg_store mgg_store;
+typedef struct mgg_dplan mgg_dplan;
+typedef struct mgg_dbuf mgg_dbuf;
+
+/* A context spans `num_parts` logical partitions (the reference's "GPUs",
+ * R:proj/src/sim.cpp:609). part_device[p] >= 0: this process drives part p on
+ * that CUDA device (several parts may share one device — the "logical
+ * partitions" configuration); -1: part p is driven by another process and its
+ * memory is imported with mgg_store_ipc_import. At most 16 parts. */
+int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out);
+int mgg_ctx_destroy(mgg_ctx* ctx);
+/* Waits for all work this process queued on every local part. */
+int mgg_ctx_synchronize(mgg_ctx* ctx);
+
+/* Symmetric embedding store — the paper's NVSHMEM "shared" NE space
+ * (R:PAPER.md:333-345) as per-part shards: part p holds global rows
+ * [part_lb[p], part_lb[p+1]) (follow_split ranges,
+ * R:proj/src/placement.cpp:96-103), `dim` fp32 columns at a pitch rounded up
+ * to 4 floats (16-B rows for 128-bit loads). Padding is zero and stays zero.
+ * Local shards are allocated here; remote shards are imported. */
+int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim,
+                     mgg_store** out);
+int mgg_store_destroy(mgg_store* s);
+int mgg_store_info(const mgg_store* s, uint32_t* dim, uint32_t* pitch);
+/* CUDA IPC handle (64 bytes) of a local shard / import a peer's shard. */
+int mgg_store_ipc_export(const mgg_store* s, uint32_t part, void* handle64);
+int mgg_store_ipc_import(mgg_store* s, uint32_t part, const void* handle64);
+/* Copies global rows [row_begin, row_begin+row_count) between host (ld floats
+ * per host row, ld >= dim) and whichever local shards hold them; rows of
+ * remote parts are skipped. Asynchronous on the parts' streams when the host
+ * memory is pinned; synchronize before reusing the host buffer. */
+int mgg_store_upload(mgg_store* s, const float* host, uint64_t row_begin,
+                     uint64_t row_count, uint32_t ld);
+int mgg_store_download(const mgg_store* s, float* host, uint64_t row_begin,
+                       uint64_t row_count, uint32_t ld);
+/* Device pointer of a shard as seen by this process (local or imported). */
+int mgg_store_shard(const mgg_store* s, uint32_t part, void** dptr);
+
+/* Small device buffers (weights, biases) on one local part's device. */
+int mgg_dbuf_create(mgg_ctx* ctx, uint32_t part, const void* host, size_t bytes,
+                    mgg_dbuf** out);
+int mgg_dbuf_destroy(mgg_dbuf* b);
+
+/* Pinned host memory for zero-staging H2D/D2H. */
+int mgg_host_alloc(size_t bytes, void** out);
+int mgg_host_free(void* p);
+
+/* Device form of one part's launch plan (FlatPlan, include/mgg/workload.hpp):
+ * per kind, (target_row, begin) int32 pairs with a sentinel and one packed
+ * column per neighbor ((owner << 28) | offset). Warps are implicit: warp w
+ * owns partitions [w*dist, (w+1)*dist) of each kind (interleaved) or the
+ * local groups then the remote groups (segregated); a CTA is wpb warps
+ * (R:proj/src/workload.cpp:103-172). */
+typedef struct {
+  uint32_t part;
+  uint32_t ps, dist, wpb;
+  uint32_t mapping;     /* 0 interleaved, 1 segregated */
+  uint32_t granularity; /* 0 partitioned, 1 whole_list */
+  uint64_t rows;        /* chunk rows (target rows of this part) */
+  uint64_t n_local, n_remote;            /* partitions per kind */
+  const int32_t* local_meta;  /* 2*(n_local+1) */
+  const uint32_t* local_cols; uint64_t local_cols_len;
+  const int32_t* remote_meta; /* 2*(n_remote+1) */
+  const uint32_t* remote_cols; uint64_t remote_cols_len;
+} mgg_plan_desc;
+
+int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* desc, mgg_dplan** out);
+int mgg_dplan_destroy(mgg_dplan* p);
+
+/* K1 — pipelined aggregation over one part's plan:
+ *   out[t] += Σ_{u in partitions of t} f(in[u])        f = ReLU if relu_in
+ * Local rows come from the part's own shard with coalesced 128-bit loads;
+ * remote rows from peer shards (NVLink/NVSwitch peer-mapped pointers) are
+ * issued before the paired local partition is reduced and consumed after it
+ * — the async discipline of R:proj/src/sim.cpp:102-125 / R:PAPER.md:406-419.
+ * Partials of one target combine in registers while consecutive partitions
+ * of a warp share it, then with fp32 vector reductions into `out` (the
+ * paper's "shuffling and atomics", R:PAPER.md:309). `out` must hold the self
+ * term already (mgg_rows_init). */
+typedef struct {
+  int relu_in;
+  int phase; /* 0 all, 1 local partitions only, 2 remote only (phase-split
+                measurement, R:proj/src/sim.cpp:127-142) */
+} mgg_agg_opts;
+int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
+                  mgg_store* out, const mgg_agg_opts* opts);
+
+/* out[r] = scale * f(in[r]) for the part's own rows (self term / copies).
+ * f: 0 identity, 1 ReLU. */
+int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
+                  mgg_store* out, float scale, int relu_in);
+
+/* Row softmax over the `dim` columns of the part's rows (in place allowed). */
+int mgg_rows_softmax(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
+                     mgg_store* out);
+
+/* K2 — Update GEMM on one part's rows:
+ *   x   = pre(in[r])          pre: 0 none, 1 ReLU, 2 ReLU(x + pre_bias)
+ *   y   = x · W (+ bias)      W: k x m row-major fp32, k = in dim, m = out dim
+ *   out = act(y)              act: 0 none, 1 ReLU, 2 row softmax
+ *   out2 (optional) = out2_scale * y   (accumulator seeding)
+ * fp32 accumulate. */
+typedef struct {
+  const mgg_dbuf* w;
+  const mgg_dbuf* bias;     /* m floats or NULL */
+  const mgg_dbuf* pre_bias; /* k floats, for pre == 2 */
+  uint32_t pre;
+  uint32_t act;
+  float out2_scale;
+} mgg_dense_desc;
+int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
+              const mgg_dense_desc* d, mgg_store* out, mgg_store* out2);
+
+/* K3 — cross-GPU layer barrier (R:PAPER.md:258 "result synchronization at
+ * the end"; barrier_cycles, R:proj/src/sim.cpp:620): device-side flags in
+ * peer-mapped memory, release/acquire at system scope, no host round trip.
+ * No-op when every part is local to this process (stream order suffices). */
+int mgg_barrier(mgg_ctx* ctx, mgg_store* flags);
+
+/* Timing with CUDA events on the part's stream around `reps` launches of
+ * K1; returns the median ns (backs the tuner's SimulateFn,
+ * R:proj/include/pipeshard/tuner.hpp:28-30). */
+int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
+                       mgg_store* out, const mgg_agg_opts* opts, uint32_t reps,
+                       uint64_t* median_ns);
+
+/* Number of kernels this library launched since the context was created. */
+uint64_t mgg_ctx_launch_count(const mgg_ctx* ctx);
+
+/* ======================================================================= */
+/* B. host facade                                                           */
+/* ======================================================================= */
+
+typedef struct mgg_graph mgg_graph;
+typedef struct mgg_flat_plan mgg_flat_plan;
+typedef struct mgg_engine mgg_engine;
+
+/* Graph ingestion — R:proj/include/pipeshard/graph.hpp:59-85. */
+int mgg_graph_from_csr(uint64_t num_nodes, uint64_t num_edges,
+                       const uint64_t* row_ptr, const uint64_t* col_idx,
+                       mgg_graph** out); /* validate_csr */
+int mgg_graph_from_edges(uint64_t num_nodes, uint64_t num_edges,
+                         const uint64_t* src, const uint64_t* dst,
+                         mgg_graph** out); /* from_edges */
+/* kind 0 uniform, 1 powerlaw (gen_synthetic, bit-identical to the
+ * reference); 2 rmat (a=0.57,b=0.19,c=0.19; `avg_degree` = edge count). */
+int mgg_graph_generate(int kind, uint64_t num_nodes, double avg_degree,
+                       uint64_t seed, mgg_graph** out);
+int mgg_graph_load_edge_list(const char* path, mgg_graph** out);
+int mgg_graph_load_csr(const char* path, mgg_graph** out);
+int mgg_graph_save_csr(const mgg_graph* g, const char* path);
+int mgg_graph_dims(const mgg_graph* g, uint64_t* num_nodes, uint64_t* num_edges);
+const uint64_t* mgg_graph_row_ptr(const mgg_graph* g);
+const uint64_t* mgg_graph_col_idx(const mgg_graph* g);
+int mgg_graph_destroy(mgg_graph* g);
+
+/* Alg. 1 — split_by_edges (R:proj/src/placement.cpp:44): num_gpus-1 points. */
+int mgg_split_by_edges(const mgg_graph* g, uint32_t num_gpus, uint64_t* split_points);
+/* plan_ne_placement (R:proj/src/placement.cpp:73); mode 0 equal_nodes,
+ * 1 follow_split; ranges = 2*num_gpus (lb, ub). */
+int mgg_plan_ne_placement(const mgg_graph* g, uint32_t num_gpus, int mode,
+                          uint64_t dim, uint64_t* ranges);
+/* translate (R:proj/src/placement.cpp:108) for `count` ids. */
+int mgg_translate(const mgg_graph* g, uint32_t num_gpus, int mode, uint64_t count,
+                  const uint64_t* ids, uint32_t* gpu, uint64_t* offset);
+/* memory_footprint (R:proj/src/placement.cpp:121): per_gpu = 2*num_gpus
+ * (ne_bytes, gp_bytes). */
+int mgg_memory_footprint(const mgg_graph* g, uint32_t num_gpus, int mode,
+                         uint64_t dim, uint64_t device_mem_bytes,
+                         uint64_t* per_gpu, int* fits);
+
+/* Neighbor-partition builder: split_local_remote + build_launch_plan
+ * (R:proj/src/workload.cpp:26-211) for one gpu, in device form.
+ * mapping 0 interleaved 1 segregated; granularity 0 partitioned 1 whole_list. */
+int mgg_flat_plan_build(const mgg_graph* g, uint32_t num_gpus, int placement_mode,
+                        uint32_t gpu, uint32_t ps, uint32_t dist, uint32_t wpb,
+                        uint64_t dim, int mapping, int granularity,
+                        mgg_flat_plan** out);
+/* info[10] = {n_local, n_remote, local_cols, remote_cols, num_warps,
+ *             num_blocks, first_target, rows, smem_bytes_per_block,
+ *             launch_smem_bytes} */
+int mgg_flat_plan_info(const mgg_flat_plan* p, uint64_t* info);
+const int32_t* mgg_flat_plan_meta(const mgg_flat_plan* p, int kind);
+const uint32_t* mgg_flat_plan_cols(const mgg_flat_plan* p, int kind);
+/* Canonical reference JSON of the expanded plan (to_json(KernelLaunchPlan),
+ * R:proj/src/workload.cpp:276-305). Free with mgg_free. */
+int mgg_flat_plan_json(const mgg_flat_plan* p, char** json);
+/* Expanded warp/task view: warp_off[num_warps+1], task_kind[], task_idx[]. */
+int mgg_flat_plan_tasks(const mgg_flat_plan* p, uint64_t* warp_off,
+                        uint8_t* task_kind, uint32_t* task_idx);
+int mgg_flat_plan_destroy(mgg_flat_plan* p);
+
+/* Cost model — R:proj/src/costmodel.cpp:27-77. */
+uint64_t mgg_wpw(uint32_t ps, uint32_t dist, uint32_t wpb, uint64_t dim);
+uint64_t mgg_smem(uint32_t ps, uint32_t dist, uint32_t wpb, uint64_t dim);
+int mgg_launch_geometry(uint64_t n_local, uint64_t n_remote, uint32_t ps,
+                        uint32_t dist, uint32_t wpb, const char* profile,
+                        uint64_t* num_warps_blocks, double* blocks_per_sm);
+/* Violations joined as "name;name;" into buf; returns their count (>= 0) or
+ * a negative status. */
+int mgg_validate(uint32_t ps, uint32_t dist, uint32_t wpb, uint64_t dim,
+                 uint32_t num_sms, uint32_t max_warps, uint64_t smem_per_sm,
+                 char* buf, size_t buflen);
+/* resolve_profile (R:proj/src/costmodel.cpp:118): JSON text, mgg_free it. */
+int mgg_profile_json(const char* name_or_path, char** json);
+
+/* Tuner — R:proj/src/tuner.cpp:129-243. The callback returns the latency of
+ * one configuration; a non-zero *err from it aborts the search with that
+ * configuration named in the error. trace: 4 u64 per entry (ps, dist, wpb,
+ * cycles), capacity `cap` entries, count in *n; best[4]. */
+typedef uint64_t (*mgg_measure_fn)(uint32_t ps, uint32_t dist, uint32_t wpb,
+                                   void* user, int* err);
+int mgg_optimize(mgg_measure_fn fn, void* user, uint32_t num_sms,
+                 uint32_t max_warps, uint64_t smem_per_sm, uint64_t dim,
+                 int retreat_value_rank, uint64_t max_evaluations,
+                 uint64_t* trace, size_t cap, size_t* n, uint64_t* best);
+int mgg_exhaustive(mgg_measure_fn fn, void* user, uint32_t num_sms,
+                   uint32_t max_warps, uint64_t smem_per_sm, uint64_t dim,
+                   uint64_t* table, size_t cap, size_t* n);
+
+/* GCN / GIN engine — the multi-GPU forward driver (the shape of
+ * multi_gpu_run, R:proj/src/sim.cpp:597-624, with the layer arithmetic of
+ * R:PAPER.md:504-517 that the reference leaves out). */
+typedef struct {
+  uint32_t kind;       /* 0 GCN (R:PAPER.md:504-508), 1 GIN (511-517) */
+  uint32_t layers;     /* GCN: 2; GIN: any >= 1 */
+  uint32_t in_dim;
+  uint32_t hidden;     /* GCN hidden width; GIN MLP hidden width */
+  uint32_t out_dim;    /* classes */
+  float eps;           /* GIN epsilon */
+  /* Weights, fp32 row-major, packed layer after layer:
+   *  GCN: w1 = [W^1 (in x hidden), W^2 (hidden x out)]; b1/w2/b2 unused.
+   *  GIN layer l (d_l -> d_{l+1}, d_0 = in, d_L = out, inner = hidden):
+   *    w1 += d_l x hidden, b1 += hidden, w2 += hidden x d_{l+1},
+   *    b2 += d_{l+1}. */
+  const float* w1;
+  const float* b1;
+  const float* w2;
+  const float* b2;
+} mgg_model_desc;
+
+/* Builds split (Alg. 1), follow_split placement, per-part plans, stores and
+ * weights for the parts this process drives (part_device as in
+ * mgg_ctx_create). */
+int mgg_engine_create(const mgg_graph* g, uint32_t num_parts,
+                      const int32_t* part_device, uint32_t ps, uint32_t dist,
+                      uint32_t wpb, const mgg_model_desc* model,
+                      mgg_engine** out);
+int mgg_engine_destroy(mgg_engine* e);
+/* IPC blob of every shard of local part `part` (stores + barrier flags). */
+int mgg_engine_ipc_export(const mgg_engine* e, uint32_t part, void* blob,
+                          size_t* len);
+int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob,
+                          size_t len);
+/* Re-plan with a new (ps, dist, wpb) (tuner hook). */
+int mgg_engine_set_config(mgg_engine* e, uint32_t ps, uint32_t dist, uint32_t wpb);
+/* x: num_nodes x in_dim host rows (only this process's rows are read). */
+int mgg_engine_set_input(mgg_engine* e, const float* x);
+/* Device-resident forward (async). */
+int mgg_engine_forward(mgg_engine* e);
+/* z: num_nodes x out_dim; only this process's rows are written. */
+int mgg_engine_get_output(mgg_engine* e, float* z);
+/* End to end: H2D x, forward, D2H z (synchronous). */
+int mgg_engine_forward_host(mgg_engine* e, const float* x, float* z);
+/* Layer-k intermediate (post-aggregation accumulator) rows, for parity. */
+int mgg_engine_get_hidden(mgg_engine* e, uint32_t which, float* rows, uint32_t* width);
+/* Standalone aggregation through the engine's plans (K1 over every local
+ * part): out = self_scale*f(x) + Σ f(x_u); x/out num_nodes x dim host rows. */
+int mgg_engine_aggregate_host(mgg_engine* e, const float* x, uint32_t dim,
+                              float self_scale, int relu_in, float* out);
+/* Median-of-reps K1 latency (ns) at aggregation width `dim` for the current
+ * config, max over local parts — the tuner's SimulateFn. */
+int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps,
+                              int phase, uint64_t* median_ns);
+/* stats[8] = {local_parts_total, remote_parts_total, local_edges,
+ * remote_edges, num_warps, num_blocks, kernel_launches, plan_build_ns} */
+int mgg_engine_stats(const mgg_engine* e, uint64_t* stats);
+mgg_ctx* mgg_engine_ctx(mgg_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGG_H_ */

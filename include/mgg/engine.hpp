@@ -1,0 +1,123 @@
+// Multi-GPU GCN/GIN forward driver — the B200 counterpart of the reference's
+// orchestration `multi_gpu_run` (R:proj/src/sim.cpp:597-624: split ->
+// place -> per-GPU local/remote split -> plan -> execute -> max + barrier),
+// now executing the layer arithmetic the reference leaves to the paper
+// (GCN R:PAPER.md:504-508, GIN R:PAPER.md:511-517) on the sm_100a kernels
+// through the C-ABI of include/mgg.h (layer A). Host-side C++ only.
+//
+// Layer programs. Every layer aggregates at the narrower of its two widths:
+// Â·H·W = Â·(H·W), and for GIN the first MLP Linear commutes with the sum,
+// ((1+eps)h_v + Σh_u)·W1 = (1+eps)(h_v·W1) + Σ(h_u·W1). A layer is then a
+// short op list over symmetric stores — Dense (K2, may seed the aggregation
+// accumulator with the self term), Init (self term), Barrier (K3: the next
+// gather reads peer shards), Aggregate (K1), Softmax — and activations of a
+// hidden layer are applied lazily by the consumer (ReLU-on-load), so no
+// extra pass ever touches HBM for them.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mgg/costmodel.hpp"
+#include "mgg/graph.hpp"
+#include "mgg/placement.hpp"
+#include "mgg/workload.hpp"
+
+struct mgg_ctx;
+struct mgg_store;
+struct mgg_dplan;
+struct mgg_dbuf;
+
+namespace mgg {
+
+struct ModelSpec {
+  enum class Kind { gcn, gin } kind = Kind::gcn;
+  std::uint32_t layers = 2;
+  std::uint32_t in_dim = 0, hidden = 0, out_dim = 0;
+  float eps = 0.f;
+  // packed weights, layout of mgg_model_desc (include/mgg.h)
+  std::vector<float> w1, b1, w2, b2;
+};
+
+class Engine {
+ public:
+  /// part_device[p] >= 0: this process drives part p on that device;
+  /// -1: another process does (import its shards with import_ipc).
+  /// `g` must outlive the engine (re-planning reads it).
+  Engine(const CsrGraph& g, std::uint32_t num_parts,
+         std::vector<std::int32_t> part_device, KernelConfig cfg, ModelSpec spec);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const WorkloadSplit& split() const { return split_; }
+  const NePlacement& placement() const { return ne_; }
+  const KernelConfig& config() const { return cfg_; }
+  mgg_ctx* ctx() const { return ctx_; }
+
+  std::vector<std::uint8_t> export_ipc(std::uint32_t part) const;
+  void import_ipc(std::uint32_t part, const std::vector<std::uint8_t>& blob);
+
+  void set_config(const KernelConfig& cfg);
+  void set_input(const float* x);            // N x in_dim host rows
+  void forward();                            // async, device resident
+  void synchronize();
+  void get_output(float* z);                 // N x out_dim host rows
+  void forward_host(const float* x, float* z);
+  /// Post-aggregation accumulator of layer `which` (N x width host rows).
+  std::uint32_t get_hidden(std::uint32_t which, float* rows);
+
+  /// Standalone K1 through the engine's plans (single-process only).
+  void aggregate_host(const float* x, std::uint32_t dim, float self_scale,
+                      bool relu_in, float* out);
+  /// Median K1 ns at width `dim`, max over local parts (tuner SimulateFn).
+  std::uint64_t time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase);
+
+  struct Stats {
+    std::uint64_t local_parts = 0, remote_parts = 0, local_edges = 0,
+                  remote_edges = 0, warps = 0, blocks = 0, launches = 0,
+                  plan_build_ns = 0;
+  };
+  Stats stats() const;
+
+ private:
+  enum class OpKind { dense, init, aggregate, barrier, softmax };
+  struct Op {
+    OpKind kind;
+    int in = -1, out = -1, out2 = -1;  // store indices
+    int w = -1, bias = -1, pre_bias = -1;  // weight slots
+    std::uint32_t pre = 0, act = 0;
+    float scale = 1.f;
+    int relu = 0;
+  };
+
+  int add_store(std::uint32_t dim);
+  int add_weight(const float* src, std::size_t n);
+  void build_program();
+  void build_plans();
+  void free_plans();
+  void run(const Op& op);
+  mgg_store* scratch(std::uint32_t dim, int slot);
+
+  const CsrGraph& g_;
+  std::uint32_t num_parts_;
+  std::vector<std::int32_t> dev_;
+  KernelConfig cfg_;
+  ModelSpec spec_;
+  WorkloadSplit split_;
+  NePlacement ne_;
+  mgg_ctx* ctx_ = nullptr;
+  std::vector<mgg_dplan*> plans_;     // per part (null if remote)
+  std::vector<mgg_store*> stores_;    // model stores (IPC-exported)
+  mgg_store* flags_ = nullptr;        // K3 flags
+  std::vector<std::vector<mgg_dbuf*>> weights_;  // [slot][part]
+  std::vector<Op> program_;
+  int input_ = -1, output_ = -1;
+  std::vector<int> hidden_;           // post-aggregation stores per layer
+  mgg_store* scratch_[2] = {nullptr, nullptr};
+  Stats stats_;
+};
+
+}  // namespace mgg

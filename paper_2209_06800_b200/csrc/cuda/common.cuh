@@ -1,0 +1,91 @@
+// Internal declarations of the device runtime (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "mgg.h"
+
+namespace mgg::dev {
+
+constexpr uint32_t kMaxParts = 16;
+
+/// Thrown inside the runtime, turned into MGG_E_* at the ABI edge.
+struct Status {
+  int code;
+  std::string msg;
+};
+
+void check(cudaError_t e, const char* what);
+/// Thread-local message behind mgg_last_error() (shared with the host facade).
+std::string& last_error();
+#define MGG_CUDA(x) ::mgg::dev::check((x), #x)
+
+}  // namespace mgg::dev
+
+struct mgg_ctx {
+  uint32_t num_parts = 0;
+  std::vector<int32_t> device;         // -1: remote process
+  std::vector<cudaStream_t> stream;    // per part (null for remote)
+  std::vector<cudaEvent_t> ev0, ev1;   // timing events per part
+  uint64_t launches = 0;
+  uint32_t epoch = 0;                  // barrier generation
+  bool all_local = true;
+  bool single_device = true;
+};
+
+struct mgg_store {
+  mgg_ctx* ctx = nullptr;
+  uint32_t dim = 0, pitch = 0;
+  std::vector<uint64_t> lb;            // num_parts + 1
+  std::vector<float*> shard;           // as seen by this process
+  std::vector<uint8_t> owned, imported;
+  // per local part: device copy of the shard table for that part's device
+  std::vector<const float**> dtable;
+  uint64_t rows(uint32_t p) const { return lb[p + 1] - lb[p]; }
+};
+
+struct mgg_dbuf {
+  mgg_ctx* ctx = nullptr;
+  uint32_t part = 0;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct mgg_dplan {
+  mgg_ctx* ctx = nullptr;
+  uint32_t part = 0;
+  uint32_t ps = 1, dist = 1, wpb = 1, mapping = 0, granularity = 0;
+  uint64_t rows = 0, n_local = 0, n_remote = 0;
+  int2* lmeta = nullptr;
+  uint32_t* lcols = nullptr;
+  int2* rmeta = nullptr;
+  uint32_t* rcols = nullptr;
+  uint64_t num_warps = 0, num_local_warps = 0;
+};
+
+namespace mgg::dev {
+
+/// Switch to the part's device; returns its stream.
+cudaStream_t enter(mgg_ctx* ctx, uint32_t part);
+void count_launch(mgg_ctx* ctx, uint64_t n = 1);
+
+// launchers (aggregate.cu / dense.cu)
+void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
+                      mgg_store* out, int relu_in, int phase, cudaStream_t st);
+void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
+                      float scale, int relu_in, cudaStream_t st);
+void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
+                  const float* w, const float* bias, const float* pre_bias,
+                  uint32_t m, uint32_t pre, uint32_t act, float* out,
+                  uint32_t out_pitch, float* out2, float out2_scale,
+                  cudaStream_t st);
+void launch_softmax(const float* in, float* out, uint64_t rows, uint32_t pitch,
+                    uint32_t m, cudaStream_t st);
+void launch_barrier(unsigned* const* flag_shards_dev, unsigned* own, uint32_t me,
+                    uint32_t num_parts, uint32_t epoch, cudaStream_t st);
+
+}  // namespace mgg::dev

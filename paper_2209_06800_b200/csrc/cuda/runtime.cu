@@ -1,0 +1,502 @@
+// Device runtime: contexts, symmetric stores, device plans, K3 barrier and
+// the C-ABI of layer A (include/mgg.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mgg::dev {
+
+thread_local std::string g_last_error;
+std::string& last_error() { return g_last_error; }
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Status{MGG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+cudaStream_t enter(mgg_ctx* ctx, uint32_t part) {
+  if (!ctx || part >= ctx->num_parts) throw Status{MGG_E_INPUT, "part out of range"};
+  if (ctx->device[part] < 0)
+    throw Status{MGG_E_INPUT, "part " + std::to_string(part) + " is not local"};
+  MGG_CUDA(cudaSetDevice(ctx->device[part]));
+  return ctx->stream[part];
+}
+
+void count_launch(mgg_ctx* ctx, uint64_t n) { ctx->launches += n; }
+
+namespace {
+
+// K3: announce `epoch` to every part, then wait until every part announced.
+__global__ void barrier_kernel(unsigned* const* shards, unsigned* own, uint32_t me,
+                               uint32_t n, uint32_t epoch) {
+  const uint32_t q = threadIdx.x;
+  if (q < n) {
+    unsigned* slot = shards[q] + me;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(own + q) : "memory");
+    } while (static_cast<int>(seen - epoch) < 0);
+  }
+  __syncwarp();
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MGG_OK;
+  } catch (const Status& s) {
+    g_last_error = s.msg;
+    return s.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return MGG_E_INPUT;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MGG_E_INPUT;
+  }
+}
+
+void refresh_tables(mgg_store* s) {
+  mgg_ctx* ctx = s->ctx;
+  for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+    if (ctx->device[p] < 0) continue;
+    MGG_CUDA(cudaSetDevice(ctx->device[p]));
+    std::vector<const float*> host(kMaxParts, nullptr);
+    for (uint32_t q = 0; q < ctx->num_parts; ++q) host[q] = s->shard[q];
+    if (!s->dtable[p]) {
+      void* d = nullptr;
+      MGG_CUDA(cudaMalloc(&d, kMaxParts * sizeof(float*)));
+      s->dtable[p] = static_cast<const float**>(d);
+    }
+    MGG_CUDA(cudaMemcpy(s->dtable[p], host.data(), kMaxParts * sizeof(float*),
+                        cudaMemcpyHostToDevice));
+  }
+}
+
+template <class T>
+T* upload_array(const T* host, size_t n) {
+  void* d = nullptr;
+  const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+  MGG_CUDA(cudaMalloc(&d, bytes));
+  if (n) MGG_CUDA(cudaMemcpy(d, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  return static_cast<T*>(d);
+}
+
+}  // namespace
+
+void launch_barrier(unsigned* const* shards, unsigned* own, uint32_t me, uint32_t n,
+                    uint32_t epoch, cudaStream_t st) {
+  barrier_kernel<<<1, 32, 0, st>>>(shards, own, me, n, epoch);
+  MGG_CUDA(cudaGetLastError());
+}
+
+}  // namespace mgg::dev
+
+using namespace mgg::dev;
+
+extern "C" {
+
+const char* mgg_last_error(void) { return g_last_error.c_str(); }
+
+int mgg_cuda_available(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n > 0 ? 1 : 0;
+}
+
+int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out) {
+  return guard([&] {
+    if (!out || !part_device) throw Status{MGG_E_INPUT, "ctx_create: null argument"};
+    if (num_parts < 1 || num_parts > kMaxParts)
+      throw Status{MGG_E_CONFIG, "ctx_create: num_parts must be in [1,16]"};
+    int ndev = 0;
+    MGG_CUDA(cudaGetDeviceCount(&ndev));
+    auto* c = new mgg_ctx();
+    try {
+      c->num_parts = num_parts;
+      c->device.assign(part_device, part_device + num_parts);
+      c->stream.assign(num_parts, nullptr);
+      c->ev0.assign(num_parts, nullptr);
+      c->ev1.assign(num_parts, nullptr);
+      int first = -1;
+      for (uint32_t p = 0; p < num_parts; ++p) {
+        const int d = c->device[p];
+        if (d < 0) {
+          c->all_local = false;
+          continue;
+        }
+        if (d >= ndev) throw Status{MGG_E_INPUT, "ctx_create: no CUDA device " + std::to_string(d)};
+        if (first < 0) first = d;
+        if (d != first) c->single_device = false;
+        MGG_CUDA(cudaSetDevice(d));
+        // parts on one device share one stream: launches then order phases
+        // across logical partitions without a barrier
+        for (uint32_t q = 0; q < p; ++q)
+          if (c->device[q] == d) c->stream[p] = c->stream[q];
+        if (!c->stream[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->stream[p], cudaStreamNonBlocking));
+        MGG_CUDA(cudaEventCreate(&c->ev0[p]));
+        MGG_CUDA(cudaEventCreate(&c->ev1[p]));
+      }
+      // peer access between every pair of local devices (single-process
+      // multi-GPU); imported IPC shards enable it lazily
+      for (uint32_t p = 0; p < num_parts; ++p)
+        for (uint32_t q = 0; q < num_parts; ++q) {
+          const int a = c->device[p], b = c->device[q];
+          if (a < 0 || b < 0 || a == b) continue;
+          int ok = 0;
+          MGG_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
+          if (!ok) throw Status{MGG_E_CUDA, "ctx_create: no peer access between devices"};
+          MGG_CUDA(cudaSetDevice(a));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled)
+            cudaGetLastError();
+          else
+            MGG_CUDA(e);
+        }
+    } catch (...) {
+      mgg_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int mgg_ctx_destroy(mgg_ctx* c) {
+  if (!c) return MGG_OK;
+  for (uint32_t p = 0; p < c->num_parts; ++p) {
+    if (c->device[p] < 0) continue;
+    cudaSetDevice(c->device[p]);
+    bool shared = false;
+    for (uint32_t q = 0; q < p; ++q) shared |= c->stream[q] == c->stream[p];
+    if (c->stream[p] && !shared) cudaStreamDestroy(c->stream[p]);
+    if (c->ev0[p]) cudaEventDestroy(c->ev0[p]);
+    if (c->ev1[p]) cudaEventDestroy(c->ev1[p]);
+  }
+  delete c;
+  return MGG_OK;
+}
+
+int mgg_ctx_synchronize(mgg_ctx* c) {
+  return guard([&] {
+    for (uint32_t p = 0; p < c->num_parts; ++p) {
+      if (c->device[p] < 0) continue;
+      MGG_CUDA(cudaSetDevice(c->device[p]));
+      MGG_CUDA(cudaStreamSynchronize(c->stream[p]));
+    }
+  });
+}
+
+uint64_t mgg_ctx_launch_count(const mgg_ctx* c) { return c ? c->launches : 0; }
+
+int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_store** out) {
+  return guard([&] {
+    if (!ctx || !part_lb || !out) throw Status{MGG_E_INPUT, "store_create: null argument"};
+    if (dim == 0) throw Status{MGG_E_INPUT, "store_create: dim must be >= 1"};
+    auto* s = new mgg_store();
+    try {
+      s->ctx = ctx;
+      s->dim = dim;
+      s->pitch = (dim + 3) / 4 * 4;
+      s->lb.assign(part_lb, part_lb + ctx->num_parts + 1);
+      for (uint32_t p = 0; p < ctx->num_parts; ++p)
+        if (s->lb[p + 1] < s->lb[p]) throw Status{MGG_E_INPUT, "store_create: ranges must be ascending"};
+      s->shard.assign(ctx->num_parts, nullptr);
+      s->owned.assign(ctx->num_parts, 0);
+      s->imported.assign(ctx->num_parts, 0);
+      s->dtable.assign(ctx->num_parts, nullptr);
+      for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+        if (ctx->device[p] < 0) continue;
+        MGG_CUDA(cudaSetDevice(ctx->device[p]));
+        const size_t bytes = std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256);
+        void* d = nullptr;
+        MGG_CUDA(cudaMalloc(&d, bytes));
+        MGG_CUDA(cudaMemset(d, 0, bytes));
+        s->shard[p] = static_cast<float*>(d);
+        s->owned[p] = 1;
+      }
+      refresh_tables(s);
+    } catch (...) {
+      mgg_store_destroy(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int mgg_store_destroy(mgg_store* s) {
+  if (!s) return MGG_OK;
+  mgg_ctx* ctx = s->ctx;
+  for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+    if (s->owned[p] && s->shard[p]) {
+      cudaSetDevice(ctx->device[p]);
+      cudaFree(s->shard[p]);
+    }
+    if (s->imported[p] && s->shard[p]) cudaIpcCloseMemHandle(s->shard[p]);
+    if (s->dtable[p]) {
+      cudaSetDevice(ctx->device[p]);
+      cudaFree(s->dtable[p]);
+    }
+  }
+  delete s;
+  return MGG_OK;
+}
+
+int mgg_store_info(const mgg_store* s, uint32_t* dim, uint32_t* pitch) {
+  if (!s) return MGG_E_INPUT;
+  if (dim) *dim = s->dim;
+  if (pitch) *pitch = s->pitch;
+  return MGG_OK;
+}
+
+int mgg_store_ipc_export(const mgg_store* s, uint32_t part, void* handle64) {
+  return guard([&] {
+    if (!s || part >= s->ctx->num_parts || !s->owned[part])
+      throw Status{MGG_E_INPUT, "ipc_export: part is not a local shard"};
+    MGG_CUDA(cudaSetDevice(s->ctx->device[part]));
+    cudaIpcMemHandle_t h;
+    MGG_CUDA(cudaIpcGetMemHandle(&h, s->shard[part]));
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int mgg_store_ipc_import(mgg_store* s, uint32_t part, const void* handle64) {
+  return guard([&] {
+    mgg_ctx* ctx = s->ctx;
+    if (part >= ctx->num_parts || ctx->device[part] >= 0)
+      throw Status{MGG_E_INPUT, "ipc_import: part is local"};
+    int dev = -1;
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      if (ctx->device[p] >= 0) dev = ctx->device[p];
+    if (dev < 0) throw Status{MGG_E_INPUT, "ipc_import: context has no local part"};
+    MGG_CUDA(cudaSetDevice(dev));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    void* d = nullptr;
+    MGG_CUDA(cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess));
+    if (s->imported[part] && s->shard[part]) cudaIpcCloseMemHandle(s->shard[part]);
+    s->shard[part] = static_cast<float*>(d);
+    s->imported[part] = 1;
+    refresh_tables(s);
+  });
+}
+
+static int copy_rows(const mgg_store* s, float* host_rw, const float* host_ro,
+                     uint64_t row_begin, uint64_t row_count, uint32_t ld, bool up) {
+  return guard([&] {
+    if (!s) throw Status{MGG_E_INPUT, "store copy: null store"};
+    if (ld < s->dim) throw Status{MGG_E_INPUT, "store copy: ld < dim"};
+    mgg_ctx* ctx = s->ctx;
+    const uint64_t end = row_begin + row_count;
+    for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+      if (ctx->device[p] < 0) continue;
+      const uint64_t a = std::max(row_begin, s->lb[p]), b = std::min(end, s->lb[p + 1]);
+      if (a >= b) continue;
+      cudaStream_t st = enter(ctx, p);
+      float* dev = s->shard[p] + (a - s->lb[p]) * s->pitch;
+      const size_t hoff = (a - row_begin) * (size_t)ld;
+      if (up)
+        MGG_CUDA(cudaMemcpy2DAsync(dev, s->pitch * 4, host_ro + hoff, ld * 4, s->dim * 4,
+                                   b - a, cudaMemcpyHostToDevice, st));
+      else
+        MGG_CUDA(cudaMemcpy2DAsync(host_rw + hoff, ld * 4, dev, s->pitch * 4, s->dim * 4,
+                                   b - a, cudaMemcpyDeviceToHost, st));
+    }
+  });
+}
+
+int mgg_store_upload(mgg_store* s, const float* host, uint64_t row_begin,
+                     uint64_t row_count, uint32_t ld) {
+  return copy_rows(s, nullptr, host, row_begin, row_count, ld, true);
+}
+
+int mgg_store_download(const mgg_store* s, float* host, uint64_t row_begin,
+                       uint64_t row_count, uint32_t ld) {
+  return copy_rows(s, host, nullptr, row_begin, row_count, ld, false);
+}
+
+int mgg_store_shard(const mgg_store* s, uint32_t part, void** dptr) {
+  if (!s || part >= s->ctx->num_parts || !dptr) return MGG_E_INPUT;
+  *dptr = s->shard[part];
+  return MGG_OK;
+}
+
+int mgg_dbuf_create(mgg_ctx* ctx, uint32_t part, const void* host, size_t bytes,
+                    mgg_dbuf** out) {
+  return guard([&] {
+    enter(ctx, part);
+    auto* b = new mgg_dbuf();
+    b->ctx = ctx;
+    b->part = part;
+    b->bytes = bytes;
+    const cudaError_t e = cudaMalloc(&b->ptr, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) {
+      delete b;
+      check(e, "cudaMalloc");
+    }
+    if (bytes && host) MGG_CUDA(cudaMemcpy(b->ptr, host, bytes, cudaMemcpyHostToDevice));
+    *out = b;
+  });
+}
+
+int mgg_dbuf_destroy(mgg_dbuf* b) {
+  if (!b) return MGG_OK;
+  cudaSetDevice(b->ctx->device[b->part]);
+  cudaFree(b->ptr);
+  delete b;
+  return MGG_OK;
+}
+
+int mgg_host_alloc(size_t bytes, void** out) {
+  return guard([&] { MGG_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 16), cudaHostAllocPortable)); });
+}
+
+int mgg_host_free(void* p) {
+  return guard([&] { MGG_CUDA(cudaFreeHost(p)); });
+}
+
+int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* d, mgg_dplan** out) {
+  return guard([&] {
+    if (!d || !out) throw Status{MGG_E_INPUT, "dplan_upload: null argument"};
+    enter(ctx, d->part);
+    if (d->ps < 1 || d->dist < 1 || d->wpb < 1 || d->wpb > 16)
+      throw Status{MGG_E_CONFIG, "dplan_upload: bad ps/dist/wpb"};
+    if (d->n_local > 0x7fffffffull || d->n_remote > 0x7fffffffull)
+      throw Status{MGG_E_CONFIG, "dplan_upload: too many partitions"};
+    auto* p = new mgg_dplan();
+    try {
+      p->ctx = ctx;
+      p->part = d->part;
+      p->ps = d->ps;
+      p->dist = d->dist;
+      p->wpb = d->wpb;
+      p->mapping = d->mapping;
+      p->granularity = d->granularity;
+      p->rows = d->rows;
+      p->n_local = d->n_local;
+      p->n_remote = d->n_remote;
+      p->lmeta = reinterpret_cast<int2*>(upload_array(d->local_meta, 2 * (d->n_local + 1)));
+      p->rmeta = reinterpret_cast<int2*>(upload_array(d->remote_meta, 2 * (d->n_remote + 1)));
+      p->lcols = upload_array(d->local_cols, d->local_cols_len);
+      p->rcols = upload_array(d->remote_cols, d->remote_cols_len);
+      p->num_local_warps = (d->n_local + d->dist - 1) / d->dist;
+      const uint64_t nr_w = (d->n_remote + d->dist - 1) / d->dist;
+      p->num_warps = d->mapping == 0 ? std::max(p->num_local_warps, nr_w)
+                                     : p->num_local_warps + nr_w;
+    } catch (...) {
+      mgg_dplan_destroy(p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int mgg_dplan_destroy(mgg_dplan* p) {
+  if (!p) return MGG_OK;
+  cudaSetDevice(p->ctx->device[p->part]);
+  cudaFree(p->lmeta);
+  cudaFree(p->rmeta);
+  cudaFree(p->lcols);
+  cudaFree(p->rcols);
+  delete p;
+  return MGG_OK;
+}
+
+int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
+                  mgg_store* out, const mgg_agg_opts* opts) {
+  return guard([&] {
+    if (!plan || !in || !out) throw Status{MGG_E_INPUT, "aggregate: null argument"};
+    if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "aggregate: in/out width differ"};
+    cudaStream_t st = enter(ctx, plan->part);
+    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, st);
+  });
+}
+
+int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
+                  float scale, int relu_in) {
+  return guard([&] {
+    if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "rows_init: in/out width differ"};
+    cudaStream_t st = enter(ctx, part);
+    launch_rows_init(in->shard[part], out->shard[part], in->rows(part), in->pitch, scale,
+                     relu_in, st);
+    count_launch(ctx);
+  });
+}
+
+int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in, const mgg_dense_desc* d,
+              mgg_store* out, mgg_store* out2) {
+  return guard([&] {
+    if (!in || !d || !out || !d->w) throw Status{MGG_E_INPUT, "dense: null argument"};
+    if (out2 && out2->pitch != out->pitch) throw Status{MGG_E_INPUT, "dense: out2 width differs"};
+    cudaStream_t st = enter(ctx, part);
+    launch_dense(in->shard[part], in->pitch, in->dim, in->rows(part),
+                 static_cast<const float*>(d->w->ptr),
+                 d->bias ? static_cast<const float*>(d->bias->ptr) : nullptr,
+                 d->pre_bias ? static_cast<const float*>(d->pre_bias->ptr) : nullptr,
+                 out->dim, d->pre, d->act, out->shard[part], out->pitch,
+                 out2 ? out2->shard[part] : nullptr, d->out2_scale, st);
+    count_launch(ctx, (out->dim + 63) / 64);
+  });
+}
+
+int mgg_rows_softmax(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out) {
+  return guard([&] {
+    if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "rows_softmax: in/out width differ"};
+    cudaStream_t st = enter(ctx, part);
+    launch_softmax(in->shard[part], out->shard[part], in->rows(part), in->pitch, in->dim, st);
+    count_launch(ctx);
+  });
+}
+
+int mgg_barrier(mgg_ctx* ctx, mgg_store* flags) {
+  return guard([&] {
+    if (ctx->all_local && ctx->single_device) return;  // stream order suffices
+    if (!flags) throw Status{MGG_E_INPUT, "barrier: flags store required"};
+    ++ctx->epoch;
+    if (ctx->all_local) {  // one process, several devices: host-side join
+      for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+        MGG_CUDA(cudaSetDevice(ctx->device[p]));
+        MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
+      }
+      return;
+    }
+    for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+      if (ctx->device[p] < 0) continue;
+      cudaStream_t st = enter(ctx, p);
+      launch_barrier(reinterpret_cast<unsigned* const*>(const_cast<float**>(flags->dtable[p])),
+                     reinterpret_cast<unsigned*>(flags->shard[p]), p, ctx->num_parts,
+                     ctx->epoch, st);
+      count_launch(ctx);
+    }
+  });
+}
+
+int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
+                       mgg_store* out, const mgg_agg_opts* opts, uint32_t reps,
+                       uint64_t* median_ns) {
+  return guard([&] {
+    cudaStream_t st = enter(ctx, plan->part);
+    reps = std::max(reps, 1u);
+    std::vector<float> ms(reps);
+    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, st);
+    for (uint32_t r = 0; r < reps; ++r) {
+      MGG_CUDA(cudaEventRecord(ctx->ev0[plan->part], st));
+      launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, st);
+      MGG_CUDA(cudaEventRecord(ctx->ev1[plan->part], st));
+      MGG_CUDA(cudaEventSynchronize(ctx->ev1[plan->part]));
+      MGG_CUDA(cudaEventElapsedTime(&ms[r], ctx->ev0[plan->part], ctx->ev1[plan->part]));
+    }
+    std::sort(ms.begin(), ms.end());
+    *median_ns = static_cast<uint64_t>(ms[reps / 2] * 1e6);
+  });
+}
+
+}  // extern "C"

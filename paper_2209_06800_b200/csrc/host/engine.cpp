@@ -1,0 +1,383 @@
+// GCN/GIN multi-GPU forward driver (see include/mgg/engine.hpp). Talks to the
+// GPU exclusively through the C-ABI of include/mgg.h.
+#include "mgg/engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "mgg.h"
+#include "mgg/errors.hpp"
+
+namespace mgg {
+
+namespace {
+
+// C-ABI status -> the host API's exception taxonomy.
+void ok(int st) {
+  if (st == MGG_OK) return;
+  const std::string msg = mgg_last_error();
+  switch (st) {
+    case MGG_E_PARSE: throw ParseError(msg, 0);
+    case MGG_E_CONFIG: throw ConfigError(msg);
+    case MGG_E_INTEGRITY: throw IntegrityError(msg);
+    case MGG_E_CUDA: throw CudaError(msg);
+    default: throw InputError(msg);
+  }
+}
+
+}  // namespace
+
+Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
+               std::vector<std::int32_t> part_device, KernelConfig cfg, ModelSpec spec)
+    : g_(g), num_parts_(num_parts), dev_(std::move(part_device)), cfg_(cfg),
+      spec_(std::move(spec)) {
+  if (dev_.size() != num_parts_) throw InputError("engine: part_device size != num_parts");
+  if (spec_.in_dim == 0 || spec_.hidden == 0 || spec_.out_dim == 0)
+    throw InputError("engine: model widths must be >= 1");
+  if (spec_.kind == ModelSpec::Kind::gcn && spec_.layers != 2)
+    throw ConfigError("engine: GCN is the 2-layer model of R:PAPER.md:504-508");
+  if (spec_.layers < 1) throw ConfigError("engine: layers must be >= 1");
+  split_ = split_by_edges(g_, num_parts_);
+  ne_ = plan_ne_placement(g_, num_parts_, PlacementMode::follow_split, spec_.in_dim, &split_);
+  try {
+    ok(mgg_ctx_create(num_parts_, dev_.data(), &ctx_));
+    std::vector<std::uint64_t> flag_lb(num_parts_ + 1);
+    for (std::uint32_t p = 0; p <= num_parts_; ++p) flag_lb[p] = p;
+    ok(mgg_store_create(ctx_, flag_lb.data(), kMaxOwners, &flags_));
+    build_program();
+    build_plans();
+  } catch (...) {
+    free_plans();
+    for (auto* s : stores_) mgg_store_destroy(s);
+    for (auto& slot : weights_)
+      for (auto* b : slot) mgg_dbuf_destroy(b);
+    mgg_store_destroy(flags_);
+    mgg_ctx_destroy(ctx_);
+    throw;
+  }
+}
+
+Engine::~Engine() {
+  if (ctx_) mgg_ctx_synchronize(ctx_);
+  free_plans();
+  for (auto* s : stores_) mgg_store_destroy(s);
+  for (auto* s : scratch_) mgg_store_destroy(s);
+  for (auto& slot : weights_)
+    for (auto* b : slot) mgg_dbuf_destroy(b);
+  mgg_store_destroy(flags_);
+  mgg_ctx_destroy(ctx_);
+}
+
+int Engine::add_store(std::uint32_t dim) {
+  std::vector<std::uint64_t> lb(num_parts_ + 1);
+  for (std::uint32_t p = 0; p < num_parts_; ++p) lb[p] = ne_.ranges[p].lb;
+  lb[num_parts_] = g_.num_nodes;
+  mgg_store* s = nullptr;
+  ok(mgg_store_create(ctx_, lb.data(), dim, &s));
+  stores_.push_back(s);
+  return static_cast<int>(stores_.size()) - 1;
+}
+
+int Engine::add_weight(const float* src, std::size_t n) {
+  std::vector<mgg_dbuf*> per(num_parts_, nullptr);
+  weights_.push_back(per);
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0) ok(mgg_dbuf_create(ctx_, p, src, n * sizeof(float), &weights_.back()[p]));
+  return static_cast<int>(weights_.size()) - 1;
+}
+
+void Engine::build_program() {
+  const auto& s = spec_;
+  input_ = add_store(s.in_dim);
+  int cur = input_;          // store holding the layer input
+  std::uint32_t cur_w = s.in_dim;
+  int fin = 0;               // pending ReLU on `cur`
+  const bool gcn = s.kind == ModelSpec::Kind::gcn;
+  std::size_t o1 = 0, ob1 = 0, o2 = 0, ob2 = 0;
+  auto need = [](const std::vector<float>& v, std::size_t n, const char* what) {
+    if (v.size() < n) throw InputError(std::string("engine: weight array too short: ") + what);
+  };
+
+  for (std::uint32_t l = 0; l < s.layers; ++l) {
+    const bool last = l + 1 == s.layers;
+    if (gcn) {
+      // GCN layer l: width a -> b, W_l packed in w1 (R:PAPER.md:504-508)
+      const std::uint32_t a = cur_w, b = last ? s.out_dim : s.hidden;
+      need(s.w1, o1 + std::size_t(a) * b, "gcn W");
+      const int W = add_weight(s.w1.data() + o1, std::size_t(a) * b);
+      o1 += std::size_t(a) * b;
+      if (b < a) {  // update first: T = f(H)·W, A = T + Σ T_u
+        const int T = add_store(b), A = add_store(b);
+        program_.push_back({OpKind::dense, cur, T, A, W, -1, -1, std::uint32_t(fin), 0, 1.f, 0});
+        program_.push_back({OpKind::barrier});
+        program_.push_back({OpKind::aggregate, T, A});
+        hidden_.push_back(A);
+        if (last) {
+          const int Z = add_store(b);
+          program_.push_back({OpKind::softmax, A, Z});
+          output_ = Z;
+        }
+        cur = A;
+      } else {  // aggregate first: A = f(H) + Σ f(H_u), then A·W
+        const int A = add_store(a), Y = add_store(b);
+        program_.push_back({OpKind::init, cur, A, -1, -1, -1, -1, 0, 0, 1.f, fin});
+        program_.push_back({OpKind::barrier});
+        program_.push_back({OpKind::aggregate, cur, A, -1, -1, -1, -1, 0, 0, 1.f, fin});
+        hidden_.push_back(A);
+        program_.push_back({OpKind::dense, A, Y, -1, W, -1, -1, 0, last ? 2u : 0u, 1.f, 0});
+        if (last) output_ = Y;
+        cur = Y;
+      }
+      cur_w = b;
+      fin = 1;
+    } else {
+      // GIN layer l: MLP((1+eps) h_v + Σ h_u), MLP = Lin(a,h)-ReLU-Lin(h,b)
+      const std::uint32_t a = cur_w, h = s.hidden;
+      const std::uint32_t b = last ? s.out_dim : s.hidden;
+      need(s.w1, o1 + std::size_t(a) * h, "gin W1");
+      need(s.b1, ob1 + h, "gin b1");
+      need(s.w2, o2 + std::size_t(h) * b, "gin W2");
+      need(s.b2, ob2 + b, "gin b2");
+      const int W1 = add_weight(s.w1.data() + o1, std::size_t(a) * h);
+      const int B1 = add_weight(s.b1.data() + ob1, h);
+      const int W2 = add_weight(s.w2.data() + o2, std::size_t(h) * b);
+      const int B2 = add_weight(s.b2.data() + ob2, b);
+      o1 += std::size_t(a) * h;
+      ob1 += h;
+      o2 += std::size_t(h) * b;
+      ob2 += b;
+      const float self = 1.f + s.eps;
+      const int O = add_store(b);
+      if (h < a) {  // T = f(H)·W1; A = (1+eps)T + Σ T_u; O = ReLU(A+b1)·W2 + b2
+        const int T = add_store(h), A = add_store(h);
+        program_.push_back({OpKind::dense, cur, T, A, W1, -1, -1, std::uint32_t(fin), 0, self, 0});
+        program_.push_back({OpKind::barrier});
+        program_.push_back({OpKind::aggregate, T, A});
+        hidden_.push_back(A);
+        program_.push_back({OpKind::dense, A, O, -1, W2, B2, B1, 2, last ? 2u : 0u, 1.f, 0});
+      } else {  // A = (1+eps) f(H) + Σ f(H_u); M = ReLU(A·W1+b1); O = M·W2+b2
+        const int A = add_store(a), M = add_store(h);
+        program_.push_back({OpKind::init, cur, A, -1, -1, -1, -1, 0, 0, self, fin});
+        program_.push_back({OpKind::barrier});
+        program_.push_back({OpKind::aggregate, cur, A, -1, -1, -1, -1, 0, 0, 1.f, fin});
+        hidden_.push_back(A);
+        program_.push_back({OpKind::dense, A, M, -1, W1, B1, -1, 0, 1, 1.f, 0});
+        program_.push_back({OpKind::dense, M, O, -1, W2, B2, -1, 0, last ? 2u : 0u, 1.f, 0});
+      }
+      if (last) output_ = O;
+      cur = O;
+      cur_w = b;
+      fin = 1;
+    }
+    // the next layer's aggregation reads this layer's output from peers
+  }
+}
+
+void Engine::free_plans() {
+  for (auto*& p : plans_) {
+    mgg_dplan_destroy(p);
+    p = nullptr;
+  }
+}
+
+void Engine::build_plans() {
+  free_plans();
+  plans_.assign(num_parts_, nullptr);
+  stats_ = {};
+  const auto t0 = std::chrono::steady_clock::now();
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    if (dev_[p] < 0) continue;
+    const FlatPlan fp = build_flat_plan(g_, split_, ne_, p, cfg_, spec_.in_dim);
+    mgg_plan_desc d{};
+    d.part = p;
+    d.ps = cfg_.ps;
+    d.dist = cfg_.dist;
+    d.wpb = cfg_.wpb;
+    d.mapping = 0;
+    d.granularity = 0;
+    d.rows = fp.rows;
+    d.n_local = fp.local.num_parts();
+    d.n_remote = fp.remote.num_parts();
+    d.local_meta = fp.local.meta.data();
+    d.local_cols = fp.local.cols.data();
+    d.local_cols_len = fp.local.cols.size();
+    d.remote_meta = fp.remote.meta.data();
+    d.remote_cols = fp.remote.cols.data();
+    d.remote_cols_len = fp.remote.cols.size();
+    ok(mgg_dplan_upload(ctx_, &d, &plans_[p]));
+    stats_.local_parts += d.n_local;
+    stats_.remote_parts += d.n_remote;
+    stats_.local_edges += d.local_cols_len;
+    stats_.remote_edges += d.remote_cols_len;
+    stats_.warps += fp.num_warps();
+    stats_.blocks += fp.num_blocks();
+  }
+  stats_.plan_build_ns = static_cast<std::uint64_t>(
+      std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count());
+}
+
+void Engine::set_config(const KernelConfig& cfg) {
+  const auto v = validate(cfg, builtin_profile("b200"), spec_.in_dim);
+  if (!v.empty()) throw ConfigError("engine: config violates " + v.front().constraint);
+  ok(mgg_ctx_synchronize(ctx_));
+  cfg_ = cfg;
+  build_plans();
+}
+
+std::vector<std::uint8_t> Engine::export_ipc(std::uint32_t part) const {
+  std::vector<std::uint8_t> blob;
+  auto put = [&](const mgg_store* s) {
+    std::uint8_t h[64];
+    ok(mgg_store_ipc_export(s, part, h));
+    blob.insert(blob.end(), h, h + 64);
+  };
+  put(flags_);
+  for (auto* s : stores_) put(s);
+  return blob;
+}
+
+void Engine::import_ipc(std::uint32_t part, const std::vector<std::uint8_t>& blob) {
+  if (blob.size() != 64 * (stores_.size() + 1))
+    throw InputError("engine: IPC blob does not match this engine's stores");
+  ok(mgg_store_ipc_import(flags_, part, blob.data()));
+  for (std::size_t i = 0; i < stores_.size(); ++i)
+    ok(mgg_store_ipc_import(stores_[i], part, blob.data() + 64 * (i + 1)));
+}
+
+void Engine::run(const Op& op) {
+  if (op.kind == OpKind::barrier) {
+    ok(mgg_barrier(ctx_, flags_));
+    return;
+  }
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    if (dev_[p] < 0) continue;
+    switch (op.kind) {
+      case OpKind::dense: {
+        mgg_dense_desc d{};
+        d.w = weights_[op.w][p];
+        d.bias = op.bias >= 0 ? weights_[op.bias][p] : nullptr;
+        d.pre_bias = op.pre_bias >= 0 ? weights_[op.pre_bias][p] : nullptr;
+        d.pre = op.pre;
+        d.act = op.act;
+        d.out2_scale = op.scale;
+        ok(mgg_dense(ctx_, p, stores_[op.in], &d, stores_[op.out],
+                     op.out2 >= 0 ? stores_[op.out2] : nullptr));
+        break;
+      }
+      case OpKind::init:
+        ok(mgg_rows_init(ctx_, p, stores_[op.in], stores_[op.out], op.scale, op.relu));
+        break;
+      case OpKind::aggregate: {
+        mgg_agg_opts o{op.relu, 0};
+        ok(mgg_aggregate(ctx_, plans_[p], stores_[op.in], stores_[op.out], &o));
+        break;
+      }
+      case OpKind::softmax:
+        ok(mgg_rows_softmax(ctx_, p, stores_[op.in], stores_[op.out]));
+        break;
+      case OpKind::barrier:
+        break;
+    }
+  }
+}
+
+void Engine::set_input(const float* x) {
+  ok(mgg_store_upload(stores_[input_], x, 0, g_.num_nodes, spec_.in_dim));
+}
+
+void Engine::forward() {
+  // inputs of every part must be resident before the first peer gather
+  ok(mgg_barrier(ctx_, flags_));
+  for (const Op& op : program_) run(op);
+}
+
+void Engine::synchronize() { ok(mgg_ctx_synchronize(ctx_)); }
+
+void Engine::get_output(float* z) {
+  ok(mgg_store_download(stores_[output_], z, 0, g_.num_nodes, spec_.out_dim));
+  synchronize();
+}
+
+void Engine::forward_host(const float* x, float* z) {
+  set_input(x);
+  forward();
+  get_output(z);
+}
+
+std::uint32_t Engine::get_hidden(std::uint32_t which, float* rows) {
+  if (which >= hidden_.size()) throw InputError("engine: no such hidden layer");
+  std::uint32_t dim = 0;
+  ok(mgg_store_info(stores_[hidden_[which]], &dim, nullptr));
+  if (rows) {
+    ok(mgg_store_download(stores_[hidden_[which]], rows, 0, g_.num_nodes, dim));
+    synchronize();
+  }
+  return dim;
+}
+
+mgg_store* Engine::scratch(std::uint32_t dim, int slot) {
+  std::uint32_t have = 0;
+  if (scratch_[slot]) ok(mgg_store_info(scratch_[slot], &have, nullptr));
+  if (!scratch_[slot] || have != dim) {
+    mgg_store_destroy(scratch_[slot]);
+    scratch_[slot] = nullptr;
+    std::vector<std::uint64_t> lb(num_parts_ + 1);
+    for (std::uint32_t p = 0; p < num_parts_; ++p) lb[p] = ne_.ranges[p].lb;
+    lb[num_parts_] = g_.num_nodes;
+    ok(mgg_store_create(ctx_, lb.data(), dim, &scratch_[slot]));
+  }
+  return scratch_[slot];
+}
+
+void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
+                            bool relu_in, float* out) {
+  for (auto d : dev_)
+    if (d < 0) throw InputError("engine: aggregate_host needs every part in this process");
+  mgg_store* in = scratch(dim, 0);
+  mgg_store* acc = scratch(dim, 1);
+  ok(mgg_store_upload(in, x, 0, g_.num_nodes, dim));
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    ok(mgg_rows_init(ctx_, p, in, acc, self_scale, relu_in ? 1 : 0));
+  ok(mgg_barrier(ctx_, flags_));
+  mgg_agg_opts o{relu_in ? 1 : 0, 0};
+  for (std::uint32_t p = 0; p < num_parts_; ++p) ok(mgg_aggregate(ctx_, plans_[p], in, acc, &o));
+  ok(mgg_store_download(acc, out, 0, g_.num_nodes, dim));
+  synchronize();
+}
+
+std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase) {
+  // Prefer a model store pair of that width (valid across processes).
+  mgg_store *in = nullptr, *out = nullptr;
+  for (const Op& op : program_)
+    if (op.kind == OpKind::aggregate) {
+      std::uint32_t w = 0;
+      ok(mgg_store_info(stores_[op.in], &w, nullptr));
+      if (w == dim) {
+        in = stores_[op.in];
+        out = stores_[op.out];
+        break;
+      }
+    }
+  if (!in) {
+    in = scratch(dim, 0);
+    out = scratch(dim, 1);
+  }
+  std::uint64_t worst = 0;
+  mgg_agg_opts o{0, phase};
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    if (dev_[p] < 0) continue;
+    std::uint64_t ns = 0;
+    ok(mgg_time_aggregate(ctx_, plans_[p], in, out, &o, reps, &ns));
+    worst = std::max(worst, ns);
+  }
+  return worst;
+}
+
+Engine::Stats Engine::stats() const {
+  Stats s = stats_;
+  s.launches = mgg_ctx_launch_count(ctx_);
+  return s;
+}
+
+}  // namespace mgg

@@ -1,0 +1,144 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the CPU oracle.
+
+Tolerance (north_star): layer outputs within 1e-4 relative with fp32
+accumulate. "Relative" is per output row: |gpu - ref| <= 1e-4 * max|ref_row|
+(an fp32 sum of hundreds of signed terms cannot be elementwise-relative near
+cancellation; the row scale is the magnitude the terms carry). Softmax rows
+are compared absolutely (they are already normalised).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def assert_rows_close(got, ref, tol=TOL, what=""):
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    scale = np.abs(ref).max(axis=1, keepdims=True)
+    scale = np.maximum(scale, 1e-6)
+    err = (np.abs(got.astype(np.float64) - ref) / scale).max() if got.size else 0.0
+    assert err <= tol, f"{what}: max row-relative error {err:.3e} > {tol}"
+    return err
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu(mgg):
+    assert mgg.cuda_available(), "gpu-marked test but no CUDA device is visible"
+
+
+def _graphs(mgg):
+    yield "rmat", mgg.gen_rmat(3000, 40000, seed=5)
+    yield "powerlaw", mgg.gen_synthetic(mgg.POWERLAW, 2000, 12, 3)
+    yield "uniform", mgg.gen_synthetic(mgg.UNIFORM, 1500, 9.5, 4)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 4])
+@pytest.mark.parametrize("dim", [1, 3, 16, 41, 64, 100, 128, 200])
+def test_aggregate_matches_oracle(mgg, oracle_mod, parts, dim):
+    g = mgg.gen_rmat(2048, 30000, seed=dim)
+    x = mgg.random_features(g.num_nodes, dim, seed=dim + 1)
+    model = mgg.make_gcn(dim, 8, 4)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=8, dist=2, wpb=4)
+    before = eng.stats()["launches"]
+    out = eng.aggregate(x, 1.0)
+    assert eng.stats()["launches"] > before, "no kernel launched"
+    ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x)
+    assert_rows_close(out, ref, what=f"agg parts={parts} dim={dim}")
+    eng.close()
+
+
+@pytest.mark.parametrize("cfg", [(1, 1, 1), (2, 1, 2), (16, 1, 4), (32, 4, 8), (4, 16, 16),
+                                 (32, 16, 1), (8, 2, 3)])
+def test_aggregate_every_config(mgg, oracle_mod, cfg):
+    ps, dist, wpb = cfg
+    for name, g in _graphs(mgg):
+        x = mgg.random_features(g.num_nodes, 16, seed=7)
+        eng = mgg.Engine(g, 2, [0, 0], mgg.make_gcn(16, 8, 4), ps=ps, dist=dist, wpb=wpb)
+        out = eng.aggregate(x, 1.0, relu_in=True)
+        ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
+        assert_rows_close(out, ref, what=f"{name} cfg={cfg}")
+        eng.close()
+
+
+def test_aggregate_edge_cases(mgg, oracle_mod):
+    # isolated nodes, an empty trailing chunk, self loops, duplicates, a hub
+    rows = [[0, 0, 1], [], [3] * 70, list(range(8)) * 9, [], [5], [2, 2]]
+    edges = [(v, u) for v, r in enumerate(rows) for u in r]
+    g = mgg.from_edges(8, edges)
+    x = mgg.random_features(8, 20, seed=9)
+    for parts in (1, 2, 5, 8):
+        eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(20, 4, 2), ps=4, dist=2, wpb=2)
+        out = eng.aggregate(x, 0.5)
+        ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x, self_scale=0.5)
+        assert_rows_close(out, ref, what=f"edge parts={parts}")
+        eng.close()
+
+
+def test_single_node_graph(mgg, oracle_mod):
+    g = mgg.from_edges(1, [(0, 0)])
+    x = mgg.random_features(1, 4, seed=1)
+    eng = mgg.Engine(g, 1, [0], mgg.make_gcn(4, 4, 2))
+    assert_rows_close(eng.aggregate(x), oracle_mod.aggregate(g.row_ptr, g.col_idx, x))
+    eng.close()
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3])
+def test_gcn2_forward(mgg, oracle_mod, parts):
+    g = mgg.gen_rmat(4000, 60000, seed=11)
+    model = mgg.make_gcn(96, 16, 41, seed=3)
+    x = mgg.random_features(g.num_nodes, 96, seed=4)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=16, dist=1, wpb=4)
+    z = np.zeros((g.num_nodes, 41), np.float32)
+    eng.forward_host(x, z)
+    h1, logits, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+    # layer-1 accumulator = Â X W1 (pre-ReLU)
+    a1 = eng.get_hidden(0)
+    y1 = oracle_mod.dense(x, model.w1[: 96 * 16].reshape(96, 16))
+    assert_rows_close(a1, oracle_mod.aggregate(g.row_ptr, g.col_idx, y1), what="A1")
+    assert_rows_close(np.maximum(a1, 0), h1, what="H1")
+    a2 = eng.get_hidden(1)
+    assert_rows_close(a2, oracle_mod.aggregate(g.row_ptr, g.col_idx, h1), what="A2")
+    assert np.abs(z - zr).max() <= TOL, np.abs(z - zr).max()
+    eng.close()
+
+
+def test_gcn2_update_first_second_layer(mgg, oracle_mod):
+    # classes < hidden: layer 2 runs dense-first then aggregation + softmax
+    g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 10, 2)
+    model = mgg.make_gcn(32, 64, 8, seed=5)
+    x = mgg.random_features(g.num_nodes, 32, seed=6)
+    eng = mgg.Engine(g, 2, [0, 0], model, ps=8, dist=2, wpb=4)
+    z = np.zeros((g.num_nodes, 8), np.float32)
+    eng.forward_host(x, z)
+    _, logits, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+    assert_rows_close(eng.get_hidden(1), logits, what="logits")
+    assert np.abs(z - zr).max() <= TOL
+    eng.close()
+
+
+@pytest.mark.parametrize("parts", [1, 2])
+def test_gin5_forward(mgg, oracle_mod, parts):
+    g = mgg.gen_rmat(3000, 30000, seed=21)
+    model = mgg.make_gin(100, 64, 47, layers=5, seed=8, eps=0.25)
+    x = mgg.random_features(g.num_nodes, 100, seed=9)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=16, dist=2, wpb=4)
+    z = np.zeros((g.num_nodes, 47), np.float32)
+    eng.forward_host(x, z)
+    logits, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
+    assert np.abs(z - zr).max() <= TOL, np.abs(z - zr).max()
+    eng.close()
+
+
+def test_config_change_keeps_results(mgg, oracle_mod):
+    g = mgg.gen_rmat(3000, 40000, seed=2)
+    model = mgg.make_gcn(16, 16, 16)
+    x = mgg.random_features(g.num_nodes, 16, seed=3)
+    eng = mgg.Engine(g, 2, [0, 0], model, ps=1, dist=1, wpb=1)
+    ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x)
+    for cfg in [(1, 1, 1), (32, 1, 16), (4, 8, 2)]:
+        eng.set_config(*cfg)
+        assert_rows_close(eng.aggregate(x), ref, what=str(cfg))
+        assert eng.time_aggregate(16, reps=3) > 0
+    eng.close()
