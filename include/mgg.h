@@ -187,6 +187,12 @@ int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
 /* Number of kernels this library launched since the context was created. */
 uint64_t mgg_ctx_launch_count(const mgg_ctx* ctx);
 
+/* CUDA events on a part's stream, addressed by slot (created on first use):
+ * the only clock the benchmark and tuner trust (device time, never host). */
+int mgg_event_record(mgg_ctx* ctx, uint32_t part, uint32_t slot);
+/* Waits for slot b, then *ms = elapsed(a -> b). */
+int mgg_event_elapsed(mgg_ctx* ctx, uint32_t part, uint32_t a, uint32_t b, float* ms);
+
 /* ======================================================================= */
 /* B. host facade                                                           */
 /* ======================================================================= */
@@ -336,6 +342,15 @@ int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps,
  * remote_edges, num_warps, num_blocks, kernel_launches, plan_build_ns} */
 int mgg_engine_stats(const mgg_engine* e, uint64_t* stats);
 mgg_ctx* mgg_engine_ctx(mgg_engine* e);
+/* Per-op device timing of subsequent forwards (events around every op of the
+ * layer program on the first local part's stream; no host sync added). */
+int mgg_engine_set_profiling(mgg_engine* e, int on);
+/* Program size / per-op accumulated ms, op kind (0 dense, 1 init,
+ * 2 aggregate, 3 barrier, 4 softmax), op width (output columns) and the
+ * number of profiled forwards. Arrays hold `cap` entries. */
+int mgg_engine_profile(mgg_engine* e, double* op_ms, uint32_t* op_kind,
+                       uint32_t* op_width, size_t cap, size_t* n_ops,
+                       uint64_t* forwards);
 
 #ifdef __cplusplus
 }

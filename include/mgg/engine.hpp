@@ -75,6 +75,15 @@ class Engine {
   /// Median K1 ns at width `dim`, max over local parts (tuner SimulateFn).
   std::uint64_t time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase);
 
+  /// Per-op device timing (CUDA events on the first local part's stream).
+  void set_profiling(bool on);
+  struct OpProfile {
+    double ms = 0;           // accumulated over profiled forwards
+    std::uint32_t kind = 0;  // 0 dense 1 init 2 aggregate 3 barrier 4 softmax
+    std::uint32_t width = 0; // output columns
+  };
+  std::vector<OpProfile> profile(std::uint64_t* forwards);
+
   struct Stats {
     std::uint64_t local_parts = 0, remote_parts = 0, local_edges = 0,
                   remote_edges = 0, warps = 0, blocks = 0, launches = 0,
@@ -117,6 +126,9 @@ class Engine {
   int input_ = -1, output_ = -1;
   std::vector<int> hidden_;           // post-aggregation stores per layer
   mgg_store* scratch_[2] = {nullptr, nullptr};
+  bool profiling_ = false;
+  std::uint32_t prof_part_ = 0, next_slot_ = 0;
+  std::vector<std::uint32_t> prof_starts_;  // first slot of each profiled forward
   Stats stats_;
 };
 

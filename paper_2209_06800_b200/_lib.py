@@ -140,6 +140,10 @@ _sig("mgg_engine_aggregate_host", I, vp, f32p, U32, C.c_float, I, f32p)
 _sig("mgg_engine_time_aggregate", I, vp, U32, U32, I, u64p)
 _sig("mgg_engine_stats", I, vp, u64p)
 _sig("mgg_engine_ctx", vp, vp)
+_sig("mgg_engine_set_profiling", I, vp, I)
+_sig("mgg_engine_profile", I, vp, C.POINTER(C.c_double), u32p, u32p, SZ, C.POINTER(SZ), u64p)
+_sig("mgg_event_record", I, vp, U32, U32)
+_sig("mgg_event_elapsed", I, vp, U32, U32, U32, f32p)
 
 # every exported symbol the header declares (checked by the CPU test suite)
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "mgg.h")

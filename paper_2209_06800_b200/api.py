@@ -455,6 +455,28 @@ class Engine:
         check(lib.mgg_engine_time_aggregate(self._h, dim, reps, phase, C.byref(ns)))
         return ns.value
 
+    def set_profiling(self, on: bool) -> None:
+        check(lib.mgg_engine_set_profiling(self._h, int(on)))
+
+    OP_KINDS = ("dense", "init", "aggregate", "barrier", "softmax")
+
+    def profile(self):
+        """[(kind, width, accumulated ms)] per program op, and #forwards."""
+        cap = 256
+        ms = np.zeros(cap, np.float64)
+        kind = np.zeros(cap, np.uint32)
+        width = np.zeros(cap, np.uint32)
+        n = C.c_size_t()
+        fw = C.c_uint64()
+        check(lib.mgg_engine_profile(self._h, _p(ms, C.c_double), _p(kind, C.c_uint32),
+                                     _p(width, C.c_uint32), cap, C.byref(n), C.byref(fw)))
+        ops = [(self.OP_KINDS[int(kind[i])], int(width[i]), float(ms[i]))
+               for i in range(n.value)]
+        return ops, fw.value
+
+    def ctx(self):
+        return lib.mgg_engine_ctx(self._h)
+
     def stats(self) -> dict:
         s = np.zeros(8, np.uint64)
         check(lib.mgg_engine_stats(self._h, _p(s, C.c_uint64)))

@@ -31,6 +31,7 @@ struct mgg_ctx {
   std::vector<int32_t> device;         // -1: remote process
   std::vector<cudaStream_t> stream;    // per part (null for remote)
   std::vector<cudaEvent_t> ev0, ev1;   // timing events per part
+  std::vector<std::vector<cudaEvent_t>> evpool;  // mgg_event_record slots
   uint64_t launches = 0;
   uint32_t epoch = 0;                  // barrier generation
   bool all_local = true;

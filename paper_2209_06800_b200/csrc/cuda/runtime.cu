@@ -127,6 +127,7 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
       c->stream.assign(num_parts, nullptr);
       c->ev0.assign(num_parts, nullptr);
       c->ev1.assign(num_parts, nullptr);
+      c->evpool.assign(num_parts, {});
       int first = -1;
       for (uint32_t p = 0; p < num_parts; ++p) {
         const int d = c->device[p];
@@ -180,6 +181,8 @@ int mgg_ctx_destroy(mgg_ctx* c) {
     if (c->stream[p] && !shared) cudaStreamDestroy(c->stream[p]);
     if (c->ev0[p]) cudaEventDestroy(c->ev0[p]);
     if (c->ev1[p]) cudaEventDestroy(c->ev1[p]);
+    for (cudaEvent_t e : c->evpool[p])
+      if (e) cudaEventDestroy(e);
   }
   delete c;
   return MGG_OK;
@@ -196,6 +199,27 @@ int mgg_ctx_synchronize(mgg_ctx* c) {
 }
 
 uint64_t mgg_ctx_launch_count(const mgg_ctx* c) { return c ? c->launches : 0; }
+
+int mgg_event_record(mgg_ctx* ctx, uint32_t part, uint32_t slot) {
+  return guard([&] {
+    cudaStream_t st = enter(ctx, part);
+    auto& pool = ctx->evpool[part];
+    if (slot >= pool.size()) pool.resize(slot + 1, nullptr);
+    if (!pool[slot]) MGG_CUDA(cudaEventCreate(&pool[slot]));
+    MGG_CUDA(cudaEventRecord(pool[slot], st));
+  });
+}
+
+int mgg_event_elapsed(mgg_ctx* ctx, uint32_t part, uint32_t a, uint32_t b, float* ms) {
+  return guard([&] {
+    enter(ctx, part);
+    const auto& pool = ctx->evpool[part];
+    if (a >= pool.size() || b >= pool.size() || !pool[a] || !pool[b])
+      throw Status{MGG_E_INPUT, "event_elapsed: slot never recorded"};
+    MGG_CUDA(cudaEventSynchronize(pool[b]));
+    MGG_CUDA(cudaEventElapsedTime(ms, pool[a], pool[b]));
+  });
+}
 
 int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_store** out) {
   return guard([&] {

@@ -482,4 +482,21 @@ int mgg_engine_stats(const mgg_engine* e, uint64_t* s) {
 }
 mgg_ctx* mgg_engine_ctx(mgg_engine* e) { return e ? e->e->ctx() : nullptr; }
 
+int mgg_engine_set_profiling(mgg_engine* e, int on) {
+  return guard([&] { e->e->set_profiling(on != 0); });
+}
+
+int mgg_engine_profile(mgg_engine* e, double* op_ms, uint32_t* op_kind, uint32_t* op_width,
+                       size_t cap, size_t* n_ops, uint64_t* forwards) {
+  return guard([&] {
+    const auto prof = e->e->profile(forwards);
+    *n_ops = prof.size();
+    for (std::size_t i = 0; i < prof.size() && i < cap; ++i) {
+      op_ms[i] = prof[i].ms;
+      op_kind[i] = prof[i].kind;
+      op_width[i] = prof[i].width;
+    }
+  });
+}
+
 }  // extern "C"

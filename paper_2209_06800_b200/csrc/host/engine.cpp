@@ -289,7 +289,44 @@ void Engine::set_input(const float* x) {
 void Engine::forward() {
   // inputs of every part must be resident before the first peer gather
   ok(mgg_barrier(ctx_, flags_));
-  for (const Op& op : program_) run(op);
+  if (!profiling_) {
+    for (const Op& op : program_) run(op);
+    return;
+  }
+  prof_starts_.push_back(next_slot_);
+  ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
+  for (const Op& op : program_) {
+    run(op);
+    ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
+  }
+}
+
+void Engine::set_profiling(bool on) {
+  profiling_ = on;
+  next_slot_ = 0;
+  prof_starts_.clear();
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0) {
+      prof_part_ = p;
+      break;
+    }
+}
+
+std::vector<Engine::OpProfile> Engine::profile(std::uint64_t* forwards) {
+  std::vector<OpProfile> out(program_.size());
+  for (std::size_t i = 0; i < program_.size(); ++i) {
+    out[i].kind = static_cast<std::uint32_t>(program_[i].kind);
+    if (program_[i].out >= 0) ok(mgg_store_info(stores_[program_[i].out], &out[i].width, nullptr));
+  }
+  for (std::uint32_t s0 : prof_starts_)
+    for (std::size_t i = 0; i < program_.size(); ++i) {
+      float ms = 0;
+      ok(mgg_event_elapsed(ctx_, prof_part_, s0 + static_cast<std::uint32_t>(i),
+                           s0 + static_cast<std::uint32_t>(i) + 1, &ms));
+      out[i].ms += ms;
+    }
+  if (forwards) *forwards = prof_starts_.size();
+  return out;
 }
 
 void Engine::synchronize() { ok(mgg_ctx_synchronize(ctx_)); }
