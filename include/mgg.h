@@ -100,6 +100,8 @@ int mgg_store_shard(const mgg_store* s, uint32_t part, void** dptr);
 int mgg_dbuf_create(mgg_ctx* ctx, uint32_t part, const void* host, size_t bytes,
                     mgg_dbuf** out);
 int mgg_dbuf_destroy(mgg_dbuf* b);
+/* Device address of a buffer (for the probes below). */
+void* mgg_dbuf_ptr(const mgg_dbuf* b);
 
 /* Pinned host memory for zero-staging H2D/D2H. */
 int mgg_host_alloc(size_t bytes, void** out);
@@ -183,6 +185,15 @@ int mgg_barrier(mgg_ctx* ctx, mgg_store* flags);
 int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
                        mgg_store* out, const mgg_agg_opts* opts, uint32_t reps,
                        uint64_t* median_ns);
+
+/* K5 — hardware probes (re-fit the b200 cost-model profile, roofline
+ * denominators): sustained gather GB/s of rows table[idx[i]] (device
+ * pointers; pitch floats per row) and dependent-load latency (ns) of a
+ * random cycle `next` (device pointer) — local HBM, L2 or a peer GPU. */
+int mgg_probe_gather(mgg_ctx* ctx, uint32_t part, const float* table, uint32_t pitch,
+                     const uint32_t* idx, uint64_t n, uint32_t reps, double* gbps);
+int mgg_probe_chase(mgg_ctx* ctx, uint32_t part, const uint32_t* next, uint32_t steps,
+                    double* ns_per_load);
 
 /* Number of kernels this library launched since the context was created. */
 uint64_t mgg_ctx_launch_count(const mgg_ctx* ctx);

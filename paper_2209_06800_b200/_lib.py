@@ -85,6 +85,9 @@ _sig("mgg_store_download", I, vp, f32p, U64, U64, U32)
 _sig("mgg_store_shard", I, vp, U32, PP)
 _sig("mgg_dbuf_create", I, vp, U32, vp, SZ, PP)
 _sig("mgg_dbuf_destroy", I, vp)
+_sig("mgg_dbuf_ptr", vp, vp)
+_sig("mgg_probe_gather", I, vp, U32, vp, U32, vp, U64, U32, C.POINTER(C.c_double))
+_sig("mgg_probe_chase", I, vp, U32, vp, U32, C.POINTER(C.c_double))
 _sig("mgg_host_alloc", I, SZ, PP)
 _sig("mgg_host_free", I, vp)
 _sig("mgg_dplan_upload", I, vp, C.POINTER(PlanDesc), PP)

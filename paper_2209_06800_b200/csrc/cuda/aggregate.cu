@@ -1,29 +1,37 @@
 // K1 — MGG pipelined neighbor aggregation for sm_100a.
 //
-// One kernel per part consumes that part's FlatPlan as-is: CTA = wpb warps,
+// Work geometry is the plan's, unchanged: logical CTA = wpb warps, logical
 // warp w owns partitions [w·dist, (w+1)·dist) of the local list and of the
 // remote list (interleaved mapping, R:proj/src/workload.cpp:103-124), or the
-// local groups then the remote groups (segregated, 126-146). Inside a warp
-// the pair loop follows the async discipline of the reference's per-warp
-// program (R:proj/src/sim.cpp:102-125, paper Fig. 6b):
+// local groups then the remote groups (segregated, 126-146); partitions hold
+// <= ps neighbors. The kernel is persistent: a resident CTA of wpb warps
+// walks a contiguous chunk of logical CTAs (grid = SMs x occupancy), so the
+// millions of logical CTAs cost no launch/scheduling overhead and a physical
+// warp can keep one target's partial sum in registers across consecutive
+// logical warps.
 //
-//   for pair i:  issue remote-row loads of R_i         (peer shard, NVLink)
-//                reduce local partition L_i            (own shard, HBM/L2)
-//                consume R_i                            (registers)
+// Per logical warp the pair loop follows the reference's async discipline
+// (R:proj/src/sim.cpp:102-125, paper Fig. 6b):
+//   pair i:  issue the remote-row loads of R_i   (peer shard over NVLink)
+//            reduce local partition L_i          (own shard, HBM/L2)
+//            consume R_i                          (registers)
+// so R_i's NVLink latency hides under L_i's local work inside one kernel,
+// with no host round trip and no NCCL call.
 //
-// so the NVLink latency of R_i is covered by L_i's local work, tile by tile,
-// inside one kernel and without any host round trip or NCCL call.
-//
-// Lane layout: a row of `vec` float4 is covered by VEC (>= vec, power of 2)
-// lanes; a warp step gathers RPW = 32/VEC rows with one 128-bit load per
-// lane (coalesced per row). Partials for one target stay in registers while
-// consecutive partitions of the warp share that target (owner combine), then
-// fold across the RPW row groups with shuffles and land in `out` with one
-// 128-bit vector reduction per lane (REDG.ADD.F32x4).
-//
-// Rows wider than 128 floats (VEC > 32) use the wide variant: each lane owns
-// float4 columns lane, lane+32, ... and walks the partition row by row.
+// Memory access: a warp loads the (target, begin) records of its dist
+// partitions with one coalesced 64-bit load, then each partition's <= 32
+// column ids with one coalesced 32-bit load, and distributes both by
+// shuffles. Rows are gathered with 128-bit loads, VEC (power of two >= row
+// float4s) lanes per row, RPW = 32/VEC rows per step, up to 4 steps in
+// flight per lane. A target's partials fold across the RPW row groups with
+// xor-shuffles and land in `out` with one 128-bit vector reduction
+// (REDG.ADD.F32x4) per lane, only when the warp's target changes.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -41,45 +49,42 @@ struct AggArgs {
   uint32_t nL, nR;
   uint32_t pitch;             // floats per row (multiple of 4)
   uint32_t vec;               // float4 per row = pitch / 4
-  uint32_t dist;
+  uint32_t dist, wpb;
   uint32_t mapping;           // 0 interleaved, 1 segregated
   uint32_t local_warps;       // segregated: warps holding local groups
+  uint32_t num_warps;         // logical warps
+  uint32_t num_lblocks;       // logical CTAs = ceil(num_warps / wpb)
   uint32_t num_owners;
   int phase;                  // 0 all, 1 local only, 2 remote only
 };
 
 constexpr uint32_t kShift = 28;
 constexpr uint32_t kMask = (1u << kShift) - 1;
+constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
+__device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ float4 f4relu(float4 a) {
-  return make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f),
-                     fmaxf(a.w, 0.f));
+  return make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
 }
 __device__ __forceinline__ float4 ld_row4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
 __device__ __forceinline__ void red_add4(float* p, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w)
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
                : "memory");
 }
-
-struct Part {
-  int target, begin, end;
-};
-__device__ __forceinline__ Part load_part(const int2* meta, uint32_t i) {
-  const int2 a = __ldg(meta + i);
-  const int2 b = __ldg(meta + i + 1);
-  return {a.x, a.y, b.y};
+__device__ __forceinline__ const float* shfl_ptr(const float* p, int src) {
+  const unsigned long long v = reinterpret_cast<unsigned long long>(p);
+  return reinterpret_cast<const float*>(__shfl_sync(kFull, v, src));
 }
 
 // Warp-uniform ranges [l0,l1) of local and [r0,r1) of remote partitions.
-__device__ __forceinline__ void warp_groups(const AggArgs& a, uint32_t w,
-                                            uint32_t& l0, uint32_t& l1,
-                                            uint32_t& r0, uint32_t& r1) {
+__device__ __forceinline__ void warp_groups(const AggArgs& a, uint32_t w, uint32_t& l0,
+                                            uint32_t& l1, uint32_t& r0, uint32_t& r1) {
   if (a.mapping == 0) {
     l0 = r0 = w * a.dist;
     l1 = min(l0 + a.dist, a.nL);
@@ -99,199 +104,299 @@ __device__ __forceinline__ void warp_groups(const AggArgs& a, uint32_t w,
   if (a.phase == 1) r1 = r0;
 }
 
-// ---------------------------------------------------------------------------
-// Narrow rows: VEC lanes per row, RPW rows per warp step.
+// Contiguous chunk of logical CTAs owned by this resident CTA.
+__device__ __forceinline__ void cta_chunk(uint32_t total, uint32_t& b0, uint32_t& b1) {
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  b0 = min(blockIdx.x * per, total);
+  b1 = min(b0 + per, total);
+}
 
 template <int VEC, bool RELU>
-struct Narrow {
-  static constexpr int RPW = 32 / VEC;
-  static constexpr int PF = 4;  // remote steps staged ahead (registers)
-
+struct Lanes {
+  static constexpr int RPW = 32 / VEC;  // rows per warp step
+  static constexpr int PF = 4;          // remote steps staged ahead
   int lane, sub, v;
-  bool vlane;  // lane covers a real float4 of the row
+  bool vlane;
 
-  __device__ __forceinline__ Narrow(uint32_t vec) {
+  __device__ __forceinline__ explicit Lanes(uint32_t vec) {
     lane = threadIdx.x & 31;
     sub = lane / VEC;
     v = lane % VEC;
-    vlane = v < (int)vec;
+    vlane = v < static_cast<int>(vec);
   }
 
-  __device__ __forceinline__ float4 fetch(const AggArgs& a,
-                                          const uint32_t* __restrict__ cols,
-                                          const Part& p, int step, bool remote,
-                                          const float* const* tab) const {
-    const int k = p.begin + step * RPW + sub;
-    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (vlane && k < p.end) {
-      const uint32_t c = __ldg(cols + k);
-      const float* base = remote ? tab[c >> kShift] : a.own;
-      r = ld_row4(base + (size_t)(c & kMask) * a.pitch + 4 * v);
-      if (RELU) r = f4relu(r);
+  // Row `r` (< n) of the current column window; base from the lane table for
+  // remote rows (peer shards), own shard otherwise.
+  template <bool REMOTE>
+  __device__ __forceinline__ float4 row(const AggArgs& a, uint32_t colwin, int r, int n,
+                                        const float* tab_lane) const {
+    const uint32_t c = __shfl_sync(kFull, colwin, r & 31);
+    const float* base = a.own;
+    if (REMOTE) base = shfl_ptr(tab_lane, static_cast<int>(c >> kShift));
+    float4 x = f4zero();
+    if (vlane && r < n) {
+      x = ld_row4(base + static_cast<size_t>(c & kMask) * a.pitch + 4 * v);
+      if (RELU) x = f4relu(x);
     }
-    return r;
+    return x;
   }
 
-  __device__ __forceinline__ void flush(const AggArgs& a, float4 acc,
-                                        int target) const {
-#pragma unroll
-    for (int off = 16; off >= VEC; off >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
-      acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
-    }
-    if (sub == 0 && vlane) red_add4(a.out + (size_t)target * a.pitch + 4 * v, acc);
-  }
-
-  // Reduce partition p (all steps) into acc.
-  __device__ __forceinline__ float4 reduce(const AggArgs& a,
-                                           const uint32_t* __restrict__ cols,
-                                           const Part& p, bool remote,
-                                           const float* const* tab,
-                                           float4 acc, int first_step) const {
-    const int steps = (p.end - p.begin + RPW - 1) / RPW;
-    for (int s = first_step; s < steps; s += 4) {
+  // Sum rows [s0*RPW, n) of the window into acc, 4 steps of loads in flight.
+  template <bool REMOTE>
+  __device__ __forceinline__ float4 window(const AggArgs& a, uint32_t colwin, int n, int s0,
+                                           float4 acc, const float* tab_lane) const {
+    const int steps = (n + RPW - 1) / RPW;
+    for (int s = s0; s < steps; s += 4) {
       float4 t[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        t[u] = (s + u < steps) ? fetch(a, cols, p, s + u, remote, tab)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        t[u] = row<REMOTE>(a, colwin, (s + u) * RPW + sub, (s + u) < steps ? n : 0, tab_lane);
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc = f4add(acc, t[u]);
     }
     return acc;
   }
+
+  __device__ __forceinline__ void flush(const AggArgs& a, float4 acc, int target) const {
+#pragma unroll
+    for (int off = 16; off >= VEC; off >>= 1) {
+      acc.x += __shfl_xor_sync(kFull, acc.x, off);
+      acc.y += __shfl_xor_sync(kFull, acc.y, off);
+      acc.z += __shfl_xor_sync(kFull, acc.z, off);
+      acc.w += __shfl_xor_sync(kFull, acc.w, off);
+    }
+    if (sub == 0 && vlane) red_add4(a.out + static_cast<size_t>(target) * a.pitch + 4 * v, acc);
+  }
 };
 
-template <int VEC, bool RELU>
-__global__ void __launch_bounds__(512) agg_narrow(AggArgs a) {
-  __shared__ const float* tab[kMaxParts];
-  if (threadIdx.x < a.num_owners) tab[threadIdx.x] = a.table[threadIdx.x];
-  __syncthreads();
-
-  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  uint32_t l0, l1, r0, r1;
-  warp_groups(a, w, l0, l1, r0, r1);
-  const uint32_t nl = l1 - l0, nr = r1 - r0;
-  if (nl == 0 && nr == 0) return;
-
-  using N = Narrow<VEC, RELU>;
-  const N n(a.vec);
-  float4 accL = make_float4(0.f, 0.f, 0.f, 0.f), accR = accL;
-  int curL = -1, curR = -1;
-  const uint32_t pairs = max(nl, nr);
-
-  for (uint32_t i = 0; i < pairs; ++i) {
-    // (1) issue remote-row loads for R_i (first PF steps stay in flight)
-    Part rp{};
-    float4 pre[N::PF];
-    const bool has_r = i < nr;
-    if (has_r) {
-      rp = load_part(a.rmeta, r0 + i);
-#pragma unroll
-      for (int s = 0; s < N::PF; ++s)
-        pre[s] = n.fetch(a, a.rcols, rp, s, true, tab);
-    }
-    // (2) reduce the paired local partition L_i while R_i is in flight
-    if (i < nl) {
-      const Part lp = load_part(a.lmeta, l0 + i);
-      if (lp.target != curL) {
-        if (curL >= 0) n.flush(a, accL, curL);
-        accL = make_float4(0.f, 0.f, 0.f, 0.f);
-        curL = lp.target;
-      }
-      accL = n.reduce(a, a.lcols, lp, false, tab, accL, 0);
-    }
-    // (3) consume R_i
-    if (has_r) {
-      if (rp.target != curR) {
-        if (curR >= 0) n.flush(a, accR, curR);
-        accR = make_float4(0.f, 0.f, 0.f, 0.f);
-        curR = rp.target;
-      }
-#pragma unroll
-      for (int s = 0; s < N::PF; ++s) accR = f4add(accR, pre[s]);
-      accR = n.reduce(a, a.rcols, rp, true, tab, accR, N::PF);
-    }
-  }
-  if (curL >= 0) n.flush(a, accL, curL);
-  if (curR >= 0) n.flush(a, accR, curR);
+__device__ __forceinline__ uint32_t load_colwin(const uint32_t* cols, int beg, int n) {
+  const int lane = threadIdx.x & 31;
+  return lane < n ? __ldg(cols + beg + lane) : 0u;
 }
 
-// ---------------------------------------------------------------------------
-// Wide rows (vec > 32 float4): lanes own columns, rows walked one by one.
+// Partition records of logical warp w (dist+1 <= 17 entries, one coalesced
+// 64-bit load per kind).
+struct WarpMeta {
+  int2 ml, mr;
+  int nl, nr;
+};
 
-template <bool RELU>
-__global__ void __launch_bounds__(512) agg_wide(AggArgs a) {
-  __shared__ const float* tab[kMaxParts];
-  if (threadIdx.x < a.num_owners) tab[threadIdx.x] = a.table[threadIdx.x];
-  __syncthreads();
-
-  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__device__ __forceinline__ WarpMeta load_warp_meta(const AggArgs& a, uint32_t w, bool remote) {
+  WarpMeta m{make_int2(0, 0), make_int2(0, 0), 0, 0};
+  if (w >= a.num_warps) return m;
+  const int lane = threadIdx.x & 31;
   uint32_t l0, l1, r0, r1;
   warp_groups(a, w, l0, l1, r0, r1);
-  const uint32_t nl = l1 - l0, nr = r1 - r0;
-  if (nl == 0 && nr == 0) return;
-  const int lane = threadIdx.x & 31;
-  constexpr int CH = 4;  // float4 columns per lane per pass
+  m.nl = static_cast<int>(l1 - l0);
+  m.nr = static_cast<int>(r1 - r0);
+  if (lane <= m.nl && m.nl > 0) m.ml = __ldg(a.lmeta + l0 + lane);
+  if (remote && lane <= m.nr && m.nr > 0) m.mr = __ldg(a.rmeta + r0 + lane);
+  return m;
+}
 
-  for (uint32_t c0 = 0; c0 < a.vec; c0 += 32 * CH) {
-    for (int kind = 0; kind < 2; ++kind) {
-      const bool remote = kind == 1;
-      const uint32_t b = remote ? r0 : l0, cnt = remote ? nr : nl;
-      const int2* meta = remote ? a.rmeta : a.lmeta;
-      const uint32_t* cols = remote ? a.rcols : a.lcols;
-      float4 acc[CH];
-      int cur = -1;
-      for (uint32_t i = 0; i < cnt; ++i) {
-        const Part p = load_part(meta, b + i);
-        if (p.target != cur) {
-          if (cur >= 0)
+template <int VEC, bool RELU, bool REMOTE, int MINB>
+__global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
+  using L = Lanes<VEC, RELU>;
+  const L ln(a.vec);
+  const int lane = ln.lane;
+  const float* tab_lane = nullptr;
+  if (REMOTE && lane < static_cast<int>(a.num_owners)) tab_lane = a.table[lane];
+
+  float4 accL = f4zero(), accR = f4zero();
+  int curL = -1, curR = -1;
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+  // software pipeline: records of the next logical warp and the column
+  // window of the next local partition are always one step ahead
+  WarpMeta next = load_warp_meta(a, b0 * a.wpb + wib, REMOTE);
+
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    const WarpMeta cur = next;
+    next = load_warp_meta(a, (lb + 1 < b1) ? w + a.wpb : a.num_warps, REMOTE);
+    const int nl = cur.nl, nr = cur.nr;
+    const int2 ml = cur.ml, mr = cur.mr;
+    const int pairs = max(nl, nr);
+    uint32_t lwin = 0;
+    if (nl > 0) {
+      const int b = __shfl_sync(kFull, ml.y, 0);
+      lwin = load_colwin(a.lcols, b, min(__shfl_sync(kFull, ml.y, 1) - b, 32));
+    }
+
+    for (int i = 0; i < pairs; ++i) {
+      // (1) issue R_i: column window + first PF steps of peer rows
+      int rt = -1, rbeg = 0, rend = 0, rn = 0;
+      uint32_t rwin = 0;
+      float4 pre[L::PF];
+      if (REMOTE && i < nr) {
+        rt = __shfl_sync(kFull, mr.x, i);
+        rbeg = __shfl_sync(kFull, mr.y, i);
+        rend = __shfl_sync(kFull, mr.y, i + 1);
+        rn = min(rend - rbeg, 32);
+        rwin = load_colwin(a.rcols, rbeg, rn);
+#pragma unroll
+        for (int s = 0; s < L::PF; ++s)
+          pre[s] = ln.template row<true>(a, rwin, s * L::RPW + ln.sub, rn, tab_lane);
+      }
+      // (2) reduce L_i while R_i's rows are in flight
+      if (i < nl) {
+        const int lt = __shfl_sync(kFull, ml.x, i);
+        const int beg = __shfl_sync(kFull, ml.y, i);
+        const int end = __shfl_sync(kFull, ml.y, i + 1);
+        // prefetch the next partition's column window before gathering
+        uint32_t lnext = 0;
+        if (i + 1 < nl) {
+          const int e2 = __shfl_sync(kFull, ml.y, i + 2);
+          lnext = load_colwin(a.lcols, end, min(e2 - end, 32));
+        }
+        if (lt != curL) {
+          if (curL >= 0) ln.flush(a, accL, curL);
+          accL = f4zero();
+          curL = lt;
+        }
+        accL = ln.template window<false>(a, lwin, min(end - beg, 32), 0, accL, nullptr);
+        for (int b = beg + 32; b < end; b += 32) {  // whole-list tails
+          const int n = min(end - b, 32);
+          accL = ln.template window<false>(a, load_colwin(a.lcols, b, n), n, 0, accL, nullptr);
+        }
+        lwin = lnext;
+      }
+      // (3) consume R_i
+      if (REMOTE && i < nr) {
+        if (rt != curR) {
+          if (curR >= 0) ln.flush(a, accR, curR);
+          accR = f4zero();
+          curR = rt;
+        }
+#pragma unroll
+        for (int s = 0; s < L::PF; ++s) accR = f4add(accR, pre[s]);
+        accR = ln.template window<true>(a, rwin, rn, L::PF, accR, tab_lane);
+        for (int beg = rbeg + 32; beg < rend; beg += 32) {  // whole-list tails
+          const int n = min(rend - beg, 32);
+          accR = ln.template window<true>(a, load_colwin(a.rcols, beg, n), n, 0, accR, tab_lane);
+        }
+      }
+    }
+  }
+  if (curL >= 0) ln.flush(a, accL, curL);
+  if (REMOTE && curR >= 0) ln.flush(a, accR, curR);
+}
+
+// Rows wider than 128 floats (vec > 32 float4): lanes own float4 columns
+// lane, lane+32, ...; a partition's rows are walked one by one.
+template <bool RELU>
+__global__ void __launch_bounds__(512) agg_wide(AggArgs a) {
+  const int lane = threadIdx.x & 31;
+  constexpr int CH = 4;
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    uint32_t l0, l1, r0, r1;
+    warp_groups(a, w, l0, l1, r0, r1);
+    for (uint32_t c0 = 0; c0 < a.vec; c0 += 32 * CH) {
+      for (int kind = 0; kind < 2; ++kind) {
+        const bool remote = kind == 1;
+        const uint32_t b = remote ? r0 : l0, cnt = remote ? r1 - r0 : l1 - l0;
+        const int2* meta = remote ? a.rmeta : a.lmeta;
+        const uint32_t* cols = remote ? a.rcols : a.lcols;
+        float4 acc[CH];
+        int cur = -1;
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const int2 m0 = __ldg(meta + b + i);
+          const int end = __ldg(meta + b + i + 1).y;
+          if (m0.x != cur) {
+            if (cur >= 0)
+#pragma unroll
+              for (int j = 0; j < CH; ++j) {
+                const uint32_t col = c0 + lane + 32 * j;
+                if (col < a.vec) red_add4(a.out + (size_t)cur * a.pitch + 4 * col, acc[j]);
+              }
+#pragma unroll
+            for (int j = 0; j < CH; ++j) acc[j] = f4zero();
+            cur = m0.x;
+          }
+          for (int k = m0.y; k < end; ++k) {
+            const uint32_t c = __ldg(cols + k);
+            const float* row =
+                (remote ? a.table[c >> kShift] : a.own) + (size_t)(c & kMask) * a.pitch;
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
               const uint32_t col = c0 + lane + 32 * j;
-              if (col < a.vec) red_add4(a.out + (size_t)cur * a.pitch + 4 * col, acc[j]);
-            }
-#pragma unroll
-          for (int j = 0; j < CH; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          cur = p.target;
-        }
-        for (int k = p.begin; k < p.end; ++k) {
-          const uint32_t c = __ldg(cols + k);
-          const float* row =
-              (remote ? tab[c >> kShift] : a.own) + (size_t)(c & kMask) * a.pitch;
-#pragma unroll
-          for (int j = 0; j < CH; ++j) {
-            const uint32_t col = c0 + lane + 32 * j;
-            if (col < a.vec) {
-              float4 x = ld_row4(row + 4 * col);
-              if (RELU) x = f4relu(x);
-              acc[j] = f4add(acc[j], x);
+              if (col < a.vec) {
+                float4 x = ld_row4(row + 4 * col);
+                if (RELU) x = f4relu(x);
+                acc[j] = f4add(acc[j], x);
+              }
             }
           }
         }
-      }
-      if (cur >= 0)
+        if (cur >= 0)
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const uint32_t col = c0 + lane + 32 * j;
-          if (col < a.vec) red_add4(a.out + (size_t)cur * a.pitch + 4 * col, acc[j]);
-        }
+          for (int j = 0; j < CH; ++j) {
+            const uint32_t col = c0 + lane + 32 * j;
+            if (col < a.vec) red_add4(a.out + (size_t)cur * a.pitch + 4 * col, acc[j]);
+          }
+      }
     }
   }
 }
 
-template <bool RELU>
-void dispatch(const AggArgs& a, dim3 grid, dim3 block, cudaStream_t st) {
-  const uint32_t v = a.vec;
-  if (v <= 1) agg_narrow<1, RELU><<<grid, block, 0, st>>>(a);
-  else if (v <= 2) agg_narrow<2, RELU><<<grid, block, 0, st>>>(a);
-  else if (v <= 4) agg_narrow<4, RELU><<<grid, block, 0, st>>>(a);
-  else if (v <= 8) agg_narrow<8, RELU><<<grid, block, 0, st>>>(a);
-  else if (v <= 16) agg_narrow<16, RELU><<<grid, block, 0, st>>>(a);
-  else if (v <= 32) agg_narrow<32, RELU><<<grid, block, 0, st>>>(a);
-  else agg_wide<RELU><<<grid, block, 0, st>>>(a);
+using KernelFn = void (*)(AggArgs);
+
+// MINB = CTAs of 512 threads that must fit per SM (register cap 128/MINB).
+template <bool RELU, bool REMOTE, int MINB>
+KernelFn pick_minb(uint32_t v) {
+  if (v <= 1) return agg_kernel<1, RELU, REMOTE, MINB>;
+  if (v <= 2) return agg_kernel<2, RELU, REMOTE, MINB>;
+  if (v <= 4) return agg_kernel<4, RELU, REMOTE, MINB>;
+  if (v <= 8) return agg_kernel<8, RELU, REMOTE, MINB>;
+  if (v <= 16) return agg_kernel<16, RELU, REMOTE, MINB>;
+  if (v <= 32) return agg_kernel<32, RELU, REMOTE, MINB>;
+  return agg_wide<RELU>;
+}
+
+int reg_cap_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_MINB");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
+template <bool RELU, bool REMOTE>
+KernelFn pick(uint32_t v) {
+  // measured on B200 (profiles/): local-only is best at a 64-register cap
+  // (no spills, 36 warps/SM); the remote variant's staging buffer wants the
+  // uncapped allocation
+  switch (reg_cap_mode()) {
+    case 1: return pick_minb<RELU, REMOTE, 1>(v);
+    case 2: return pick_minb<RELU, REMOTE, 2>(v);
+    case 3: return pick_minb<RELU, REMOTE, 3>(v);
+    default: return REMOTE ? pick_minb<RELU, REMOTE, 1>(v) : pick_minb<RELU, REMOTE, 2>(v);
+  }
+}
+
+// Resident CTAs per SM for (kernel, CTA size), cached per device.
+unsigned resident_grid(KernelFn k, int threads) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, unsigned> cache;
+  int dev = 0;
+  MGG_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_pair(reinterpret_cast<const void*>(k), threads * 64 + dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0, sms = 0;
+  MGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0));
+  MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned g = static_cast<unsigned>(std::max(1, per_sm) * sms);
+  cache[key] = g;
+  return g;
 }
 
 // out[r] = scale * f(in[r]) over rows*pitch floats
@@ -323,18 +428,21 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   a.pitch = in->pitch;
   a.vec = in->pitch / 4;
   a.dist = p->dist;
+  a.wpb = p->wpb;
   a.mapping = p->mapping;
   a.local_warps = static_cast<uint32_t>(p->num_local_warps);
   a.num_owners = ctx->num_parts;
   a.phase = phase;
   if (p->num_warps == 0) return;
-  const uint64_t blocks = (p->num_warps + p->wpb - 1) / p->wpb;
-  if (blocks > 0x7fffffffull) throw Status{MGG_E_CONFIG, "aggregate: grid too large"};
-  const dim3 grid(static_cast<unsigned>(blocks)), block(32 * p->wpb);
-  if (relu_in)
-    dispatch<true>(a, grid, block, st);
-  else
-    dispatch<false>(a, grid, block, st);
+  if (p->num_warps > 0xffffffffull) throw Status{MGG_E_CONFIG, "aggregate: too many warps"};
+  a.num_warps = static_cast<uint32_t>(p->num_warps);
+  a.num_lblocks = (a.num_warps + a.wpb - 1) / a.wpb;
+  const bool remote = a.nR > 0 && phase != 1;
+  KernelFn k = relu_in ? (remote ? pick<true, true>(a.vec) : pick<true, false>(a.vec))
+                       : (remote ? pick<false, true>(a.vec) : pick<false, false>(a.vec));
+  const int threads = 32 * static_cast<int>(p->wpb);
+  const unsigned grid = std::min<unsigned>(resident_grid(k, threads), a.num_lblocks);
+  k<<<grid, threads, 0, st>>>(a);
   MGG_CUDA(cudaGetLastError());
   count_launch(ctx);
 }

@@ -379,6 +379,8 @@ int mgg_dbuf_destroy(mgg_dbuf* b) {
   return MGG_OK;
 }
 
+void* mgg_dbuf_ptr(const mgg_dbuf* b) { return b ? b->ptr : nullptr; }
+
 int mgg_host_alloc(size_t bytes, void** out) {
   return guard([&] { MGG_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 16), cudaHostAllocPortable)); });
 }

@@ -1,0 +1,65 @@
+"""K5 hardware probes (include/mgg.h mgg_probe_*): the measured ceilings the
+aggregation kernel is judged against and the b200 cost-model profile is
+re-fitted from."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import check, lib
+
+
+class _Ctx:
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        dev = np.array([device], np.int32)
+        check(lib.mgg_ctx_create(1, dev.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(self.h)))
+        self.bufs = []
+
+    def buf(self, arr: np.ndarray):
+        b = C.c_void_p()
+        arr = np.ascontiguousarray(arr)
+        check(lib.mgg_dbuf_create(self.h, 0, arr.ctypes.data, arr.nbytes, C.byref(b)))
+        self.bufs.append(b)
+        return lib.mgg_dbuf_ptr(b)
+
+    def close(self):
+        for b in self.bufs:
+            lib.mgg_dbuf_destroy(b)
+        lib.mgg_ctx_destroy(self.h)
+
+
+def gather_gbps(rows: int, dim: int, n_idx: int, device: int = 0, reps: int = 5,
+                seed: int = 0) -> float:
+    """Sustained GB/s of gathering n_idx uniformly random rows (dim fp32,
+    pitch rounded to 4) from a rows x dim table — the K1 gather ceiling."""
+    pitch = (dim + 3) // 4 * 4
+    rng = np.random.default_rng(seed)
+    ctx = _Ctx(device)
+    try:
+        table = ctx.buf(rng.uniform(-1, 1, (rows, pitch)).astype(np.float32))
+        idx = ctx.buf(rng.integers(0, rows, n_idx, dtype=np.uint32))
+        g = C.c_double()
+        check(lib.mgg_probe_gather(ctx.h, 0, table, pitch, idx, n_idx, reps, C.byref(g)))
+        return g.value
+    finally:
+        ctx.close()
+
+
+def chase_ns(nbytes: int, device: int = 0, steps: int = 20000, seed: int = 0) -> float:
+    """Dependent-load latency (ns) over a random cycle spanning nbytes."""
+    n = max(nbytes // 128, 2)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n).astype(np.uint64)
+    nxt = np.zeros(n * 32, np.uint32)  # one pointer per 128-B line
+    order = perm * 32
+    nxt[order] = np.roll(order, -1)
+    ctx = _Ctx(device)
+    try:
+        p = ctx.buf(nxt)
+        ns = C.c_double()
+        check(lib.mgg_probe_chase(ctx.h, 0, p, steps, C.byref(ns)))
+        return ns.value
+    finally:
+        ctx.close()
