@@ -46,6 +46,7 @@ struct mgg_store {
   std::vector<uint8_t> owned, imported;
   // per local part: device copy of the shard table for that part's device
   std::vector<const float**> dtable;
+  std::vector<float*> stage;           // per local part: dense H2D/D2H slab
   uint64_t rows(uint32_t p) const { return lb[p + 1] - lb[p]; }
 };
 
@@ -54,6 +55,8 @@ struct mgg_dbuf {
   uint32_t part = 0;
   void* ptr = nullptr;
   size_t bytes = 0;
+  void* tc_cache = nullptr;  // W^T hi/lo split for the tcgen05 GEMM
+  uint32_t tc_k = 0, tc_m = 0;
 };
 
 struct mgg_dplan {
@@ -86,6 +89,12 @@ void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                   cudaStream_t st);
 void launch_softmax(const float* in, float* out, uint64_t rows, uint32_t pitch,
                     uint32_t m, cudaStream_t st);
+bool gemm_tc_supported(uint32_t k, uint32_t m);
+const float* gemm_tc_prepare(mgg_dbuf* w, uint32_t k, uint32_t m, cudaStream_t st);
+void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
+                     const float* wt, const float* bias, const float* pre_bias, uint32_t m,
+                     uint32_t pre, uint32_t act, float* out, uint32_t out_pitch, float* out2,
+                     float out2_scale, cudaStream_t st);
 void launch_barrier(unsigned* const* flag_shards_dev, unsigned* own, uint32_t me,
                     uint32_t num_parts, uint32_t epoch, cudaStream_t st);
 

@@ -1,0 +1,442 @@
+// K2 — Update GEMM on the 5th-gen tensor cores: out = act(pre(X) · W + b).
+//
+// tcgen05.mma kind::tf32 with a 3xTF32 split so the product keeps fp32
+// accuracy (the 1e-4 parity bar): X = Xh + Xl, W = Wh + Wl with Xh, Wh
+// exact TF32 values (low 13 mantissa bits cleared) and
+//   X·W ≈ Xh·Wh + Xh·Wl + Xl·Wh        (dropped Xl·Wl term ~ 2^-22 |X||W|).
+// The GEMM is HBM-bound at these widths (N <= 64, ~2N flop per X byte), so
+// the 3x tensor work is free; what matters is streaming X at HBM rate.
+//
+// Persistent CTA per SM, warp-specialised:
+//   warp 0  : TMA producer — X tiles (128 rows x 32 fp32 = one 128-B swizzle
+//             row per tile row) into a 4-deep smem ring; W^T hi/lo resident.
+//   warp 1  : MMA issuer — one elected thread, 3 x 4 tcgen05.mma (M=128,
+//             N=NP, K=8) per 32-wide k-block into a TMEM accumulator
+//             (double-buffered across row tiles).
+//   warp 2  : TMEM allocator.
+//   warps 4-7: split (pre-transform, Xh in place, Xl to a twin tile; the
+//             async-proxy fence hands the tile to the tensor core) and the
+//             epilogue (tcgen05.ld 32x32b -> bias / ReLU / row softmax /
+//             scaled accumulator seed -> global).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace mgg::dev {
+namespace {
+
+constexpr int BM = 128;            // rows per tile (UMMA M)
+constexpr int BK = 32;             // fp32 per 128-B swizzle row
+constexpr int kTileBytes = BM * BK * 4;  // 16 KB
+constexpr int kThreads = 256;
+
+struct TcArgs {
+  uint64_t rows;
+  uint32_t k, n_kb, m, out_pitch;
+  uint32_t pre, act, stages;
+  const float* bias;
+  const float* pre_bias;
+  float* out;
+  float* out2;
+  float out2_scale;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                       int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+// UMMA shared-memory descriptor, K-major, 128-B swizzle: rows of 128 B,
+// 8-row core groups 1024 B apart (SBO), LBO unused (1), version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                   const __grid_constant__ CUtensorMap map_w, TcArgs a) {
+  constexpr uint32_t kAccCols = NP;  // fp32 columns per accumulator
+  constexpr uint32_t kTmemCols = (2 * NP <= 32) ? 32 : (2 * NP <= 64) ? 64 : (2 * NP <= 128) ? 128
+                                 : (2 * NP <= 256) ? 256 : 512;
+  constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                              (static_cast<uint32_t>(NP >> 3) << 17) | ((BM >> 4) << 24);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t wbytes = a.n_kb * 2 * NP * 128;
+  uint8_t* w_s = smem;                          // [kb][hi|lo][NP][128 B]
+  uint8_t* x_s = smem + wbytes;                 // [stage][hi|lo][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(x_s + a.stages * 2 * kTileBytes);
+  uint64_t* full = bars;
+  uint64_t* split = bars + a.stages;
+  uint64_t* empty = bars + 2 * a.stages;
+  uint64_t* tfull = bars + 3 * a.stages;      // [2]
+  uint64_t* tempty = tfull + 2;               // [2]
+  uint64_t* wfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n_tiles = static_cast<uint32_t>((a.rows + BM - 1) / BM);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    mbar_init(wfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+      mbar_expect_tx(wfull, wbytes);
+      for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+        tma_2d(w_s + kb * 2 * NP * 128, &map_w, wfull, kb * BK, 0);
+        tma_2d(w_s + kb * 2 * NP * 128 + NP * 128, &map_w, wfull, kb * BK, NP);
+      }
+      uint32_t s = 0, ph = 0;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], kTileBytes);
+          tma_2d(x_s + s * 2 * kTileBytes, &map_x, &full[s], kb * BK, t * BM);
+          if (++s == a.stages) s = 0, ph ^= 1;
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      mbar_wait(wfull, 0);
+      uint32_t s = 0, ph = 0, it = 0;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * kAccCols;
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(&split[s], ph);
+          tc_fence_after();
+          const uint64_t xh = umma_desc(su32(x_s + s * 2 * kTileBytes));
+          const uint64_t xl = umma_desc(su32(x_s + s * 2 * kTileBytes + kTileBytes));
+          const uint64_t wh = umma_desc(su32(w_s + kb * 2 * NP * 128));
+          const uint64_t wl = umma_desc(su32(w_s + kb * 2 * NP * 128 + NP * 128));
+#pragma unroll
+          for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B
+            const uint64_t o = 2 * k;
+            mma_tf32(d, xh + o, wh + o, kIdesc, (kb | k) != 0);
+            mma_tf32(d, xh + o, wl + o, kIdesc, 1);
+            mma_tf32(d, xl + o, wh + o, kIdesc, 1);
+          }
+          mma_commit(&empty[s]);  // smem stage free once these MMAs retire
+          if (++s == a.stages) s = 0, ph ^= 1;
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- split + epilogue warpgroup
+    const int tid = threadIdx.x - 128;  // 0..127
+    const int g = warp - 4;             // TMEM lane quarter
+    uint32_t s = 0, ph = 0, it = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+        mbar_wait(&full[s], ph);
+        float4* hi = reinterpret_cast<float4*>(x_s + s * 2 * kTileBytes);
+        float4* lo = reinterpret_cast<float4*>(x_s + s * 2 * kTileBytes + kTileBytes);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = tid + 128 * j;  // float4 slot in the 16 KB tile
+          float4 v = hi[i];
+          if (a.pre) {
+            const int row = i >> 3;
+            const int chunk = (i & 7) ^ (row & 7);  // undo the 128-B swizzle
+            const uint32_t k0 = kb * BK + chunk * 4;
+            float* e = &v.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float x = e[q];
+              if (a.pre == 2 && k0 + q < a.k) x += __ldg(a.pre_bias + k0 + q);
+              e[q] = fmaxf(x, 0.f);
+            }
+          }
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          hi[i] = h;
+          lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&split[s]);
+        if (++s == a.stages) s = 0, ph ^= 1;
+      }
+      // epilogue for tile t
+      const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      float y[NP];
+#pragma unroll
+      for (int c = 0; c < NP; c += 16)
+        tmem_ld16(tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16) + c, y + c);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      const uint64_t row = static_cast<uint64_t>(t) * BM + 32 * g + lane;
+      if (row < a.rows) {
+#pragma unroll
+        for (int c = 0; c < NP; ++c)
+          if (a.bias && c < static_cast<int>(a.m)) y[c] += __ldg(a.bias + c);
+        if (a.out2) {
+          float* o2 = a.out2 + row * a.out_pitch;
+#pragma unroll
+          for (int c = 0; c < NP; c += 4)
+            if (c < static_cast<int>(a.out_pitch))
+              *reinterpret_cast<float4*>(o2 + c) =
+                  make_float4(c + 0 < (int)a.m ? y[c + 0] * a.out2_scale : 0.f,
+                              c + 1 < (int)a.m ? y[c + 1] * a.out2_scale : 0.f,
+                              c + 2 < (int)a.m ? y[c + 2] * a.out2_scale : 0.f,
+                              c + 3 < (int)a.m ? y[c + 3] * a.out2_scale : 0.f);
+        }
+        if (a.act == 1) {
+#pragma unroll
+          for (int c = 0; c < NP; ++c) y[c] = fmaxf(y[c], 0.f);
+        } else if (a.act == 2) {
+          float mx = -FLT_MAX;
+#pragma unroll
+          for (int c = 0; c < NP; ++c)
+            if (c < static_cast<int>(a.m)) mx = fmaxf(mx, y[c]);
+          float sum = 0.f;
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            y[c] = c < static_cast<int>(a.m) ? __expf(y[c] - mx) : 0.f;
+            sum += y[c];
+          }
+          const float inv = 1.f / sum;
+#pragma unroll
+          for (int c = 0; c < NP; ++c) y[c] *= inv;
+        }
+        float* o = a.out + row * a.out_pitch;
+#pragma unroll
+        for (int c = 0; c < NP; c += 4)
+          if (c < static_cast<int>(a.out_pitch))
+            *reinterpret_cast<float4*>(o + c) =
+                make_float4(c + 0 < (int)a.m ? y[c + 0] : 0.f, c + 1 < (int)a.m ? y[c + 1] : 0.f,
+                            c + 2 < (int)a.m ? y[c + 2] : 0.f, c + 3 < (int)a.m ? y[c + 3] : 0.f);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+// W (k x m row-major) -> W^T split [hi rows 0..NP) | lo rows NP..2NP), K padded.
+__global__ void prep_w_kernel(const float* __restrict__ w, uint32_t k, uint32_t m, uint32_t np,
+                              uint32_t kpad, float* __restrict__ out) {
+  const uint32_t total = np * kpad;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t n = i / kpad, kk = i % kpad;
+    const float x = (n < m && kk < k) ? w[static_cast<size_t>(kk) * m + n] : 0.f;
+    const float h = tf32_hi(x);
+    out[static_cast<size_t>(n) * kpad + kk] = h;
+    out[static_cast<size_t>(np + n) * kpad + kk] = x - h;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled encode_fn() {
+  static PFN_cuTensorMapEncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  });
+  if (!fn) throw Status{MGG_E_CUDA, "cuTensorMapEncodeTiled unavailable"};
+  return fn;
+}
+
+CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+                     uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {pitch_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                 const_cast<float*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Status{MGG_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+  return m;
+}
+
+template <int NP>
+void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
+            const TcArgs& a, cudaStream_t st) {
+  const size_t wbytes = static_cast<size_t>(a.n_kb) * 2 * NP * 128;
+  TcArgs b = a;
+  b.stages = 4;
+  auto smem_for = [&](uint32_t stages) {
+    return 1024 + wbytes + stages * 2 * kTileBytes + (3 * stages + 5) * 8 + 16;
+  };
+  while (b.stages > 2 && smem_for(b.stages) > 227 * 1024) --b.stages;
+  const size_t smem = smem_for(b.stages);
+  if (smem > 227 * 1024) throw Status{MGG_E_CONFIG, "gemm_tc: W too large for smem"};
+  const CUtensorMap mx = make_map(in, a.k, a.rows, size_t(in_pitch) * 4, BK, BM);
+  const CUtensorMap mw = make_map(wt, kpad, 2 * NP, size_t(kpad) * 4, BK, NP);
+  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  int dev = 0, sms = 0;
+  MGG_CUDA(cudaGetDevice(&dev));
+  MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const uint64_t tiles = (a.rows + BM - 1) / BM;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, sms));
+  gemm_tc_kernel<NP><<<grid, kThreads, smem, st>>>(mx, mw, b);
+  MGG_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+bool gemm_tc_supported(uint32_t k, uint32_t m) {
+  if (m == 0 || m > 64 || k < 64) return false;  // narrow K: the SIMT kernel wins
+  const uint32_t np = (m + 15) / 16 * 16;
+  const size_t wbytes = size_t((k + BK - 1) / BK) * 2 * np * 128;
+  return 1024 + wbytes + 2 * 2 * kTileBytes + 128 <= 227 * 1024;
+}
+
+// Returns the cached device W^T hi/lo block for `w`, building it on first use.
+const float* gemm_tc_prepare(mgg_dbuf* w, uint32_t k, uint32_t m, cudaStream_t st) {
+  const uint32_t np = (m + 15) / 16 * 16, kpad = (k + BK - 1) / BK * BK;
+  if (!w->tc_cache || w->tc_k != k || w->tc_m != m) {
+    if (w->tc_cache) MGG_CUDA(cudaFree(w->tc_cache));
+    w->tc_cache = nullptr;
+    MGG_CUDA(cudaMalloc(&w->tc_cache, size_t(2) * np * kpad * sizeof(float)));
+    prep_w_kernel<<<64, 256, 0, st>>>(static_cast<const float*>(w->ptr), k, m, np, kpad,
+                                      static_cast<float*>(w->tc_cache));
+    MGG_CUDA(cudaGetLastError());
+    w->tc_k = k;
+    w->tc_m = m;
+  }
+  return static_cast<const float*>(w->tc_cache);
+}
+
+void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
+                     const float* wt, const float* bias, const float* pre_bias, uint32_t m,
+                     uint32_t pre, uint32_t act, float* out, uint32_t out_pitch, float* out2,
+                     float out2_scale, cudaStream_t st) {
+  if (rows == 0) return;
+  TcArgs a{};
+  a.rows = rows;
+  a.k = k;
+  a.n_kb = (k + BK - 1) / BK;
+  a.m = m;
+  a.out_pitch = out_pitch;
+  a.pre = pre;
+  a.act = act;
+  a.bias = bias;
+  a.pre_bias = pre_bias;
+  a.out = out;
+  a.out2 = out2;
+  a.out2_scale = out2_scale;
+  const uint32_t kpad = a.n_kb * BK;
+  const uint32_t np = (m + 15) / 16 * 16;
+  switch (np) {
+    case 16: run_tc<16>(in, in_pitch, wt, kpad, a, st); break;
+    case 32: run_tc<32>(in, in_pitch, wt, kpad, a, st); break;
+    case 48: run_tc<48>(in, in_pitch, wt, kpad, a, st); break;
+    case 64: run_tc<64>(in, in_pitch, wt, kpad, a, st); break;
+    default: throw Status{MGG_E_CONFIG, "gemm_tc: unsupported width"};
+  }
+}
+
+}  // namespace mgg::dev

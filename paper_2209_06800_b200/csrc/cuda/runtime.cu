@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -237,6 +239,7 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
       s->owned.assign(ctx->num_parts, 0);
       s->imported.assign(ctx->num_parts, 0);
       s->dtable.assign(ctx->num_parts, nullptr);
+      s->stage.assign(ctx->num_parts, nullptr);
       for (uint32_t p = 0; p < ctx->num_parts; ++p) {
         if (ctx->device[p] < 0) continue;
         MGG_CUDA(cudaSetDevice(ctx->device[p]));
@@ -268,6 +271,10 @@ int mgg_store_destroy(mgg_store* s) {
     if (s->dtable[p]) {
       cudaSetDevice(ctx->device[p]);
       cudaFree(s->dtable[p]);
+    }
+    if (s->stage[p]) {
+      cudaSetDevice(ctx->device[p]);
+      cudaFree(s->stage[p]);
     }
   }
   delete s;
@@ -313,11 +320,44 @@ int mgg_store_ipc_import(mgg_store* s, uint32_t part, const void* handle64) {
   });
 }
 
-static int copy_rows(const mgg_store* s, float* host_rw, const float* host_ro,
+}  // extern "C"
+
+namespace mgg::dev {
+
+// Dense <-> pitched row copies on the device (the H2D/D2H legs stay 1D:
+// PCIe DMA of 2D copies with 2.4 KB rows runs at a third of the 1D rate).
+__global__ void repitch_kernel(const float* __restrict__ src, uint32_t src_ld,
+                               float* __restrict__ dst, uint32_t dst_ld, uint64_t rows,
+                               uint32_t cols) {
+  const uint64_t total = rows * cols;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / cols, c = i % cols;
+    dst[r * dst_ld + c] = src[r * src_ld + c];
+  }
+}
+
+void repitch(const float* src, uint32_t src_ld, float* dst, uint32_t dst_ld, uint64_t rows,
+             uint32_t cols, cudaStream_t st) {
+  const uint64_t total = rows * cols;
+  if (!total) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148 * 16));
+  repitch_kernel<<<blocks, 256, 0, st>>>(src, src_ld, dst, dst_ld, rows, cols);
+  MGG_CUDA(cudaGetLastError());
+}
+
+constexpr size_t kStageBytes = 32u << 20;
+
+}  // namespace mgg::dev
+
+extern "C" {
+
+static int copy_rows(const mgg_store* cs, float* host_rw, const float* host_ro,
                      uint64_t row_begin, uint64_t row_count, uint32_t ld, bool up) {
   return guard([&] {
-    if (!s) throw Status{MGG_E_INPUT, "store copy: null store"};
-    if (ld < s->dim) throw Status{MGG_E_INPUT, "store copy: ld < dim"};
+    if (!cs) throw Status{MGG_E_INPUT, "store copy: null store"};
+    if (ld < cs->dim) throw Status{MGG_E_INPUT, "store copy: ld < dim"};
+    auto* s = const_cast<mgg_store*>(cs);
     mgg_ctx* ctx = s->ctx;
     const uint64_t end = row_begin + row_count;
     for (uint32_t p = 0; p < ctx->num_parts; ++p) {
@@ -327,12 +367,38 @@ static int copy_rows(const mgg_store* s, float* host_rw, const float* host_ro,
       cudaStream_t st = enter(ctx, p);
       float* dev = s->shard[p] + (a - s->lb[p]) * s->pitch;
       const size_t hoff = (a - row_begin) * (size_t)ld;
-      if (up)
-        MGG_CUDA(cudaMemcpy2DAsync(dev, s->pitch * 4, host_ro + hoff, ld * 4, s->dim * 4,
-                                   b - a, cudaMemcpyHostToDevice, st));
-      else
-        MGG_CUDA(cudaMemcpy2DAsync(host_rw + hoff, ld * 4, dev, s->pitch * 4, s->dim * 4,
-                                   b - a, cudaMemcpyDeviceToHost, st));
+      const size_t row_bytes = size_t(s->dim) * 4;
+      if (ld == s->pitch) {  // identical layout: one 1D copy
+        if (up)
+          MGG_CUDA(cudaMemcpyAsync(dev, host_ro + hoff, (b - a) * row_bytes, cudaMemcpyHostToDevice, st));
+        else
+          MGG_CUDA(cudaMemcpyAsync(host_rw + hoff, dev, (b - a) * row_bytes, cudaMemcpyDeviceToHost, st));
+        continue;
+      }
+      if (ld != s->dim) {  // strided host rows: the DMA engine's 2D path
+        if (up)
+          MGG_CUDA(cudaMemcpy2DAsync(dev, s->pitch * 4, host_ro + hoff, ld * 4, row_bytes, b - a,
+                                     cudaMemcpyHostToDevice, st));
+        else
+          MGG_CUDA(cudaMemcpy2DAsync(host_rw + hoff, ld * 4, dev, s->pitch * 4, row_bytes, b - a,
+                                     cudaMemcpyDeviceToHost, st));
+        continue;
+      }
+      // dense host rows, padded device rows: 1D DMA through a staging slab
+      if (!s->stage[p]) MGG_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->stage[p]), kStageBytes));
+      const uint64_t chunk = std::max<uint64_t>(1, kStageBytes / row_bytes);
+      for (uint64_t r = a; r < b; r += chunk) {
+        const uint64_t n = std::min(chunk, b - r);
+        float* d = s->shard[p] + (r - s->lb[p]) * s->pitch;
+        const size_t h = (r - row_begin) * (size_t)ld;
+        if (up) {
+          MGG_CUDA(cudaMemcpyAsync(s->stage[p], host_ro + h, n * row_bytes, cudaMemcpyHostToDevice, st));
+          repitch(s->stage[p], s->dim, d, s->pitch, n, s->dim, st);
+        } else {
+          repitch(d, s->pitch, s->stage[p], s->dim, n, s->dim, st);
+          MGG_CUDA(cudaMemcpyAsync(host_rw + h, s->stage[p], n * row_bytes, cudaMemcpyDeviceToHost, st));
+        }
+      }
     }
   });
 }
@@ -375,6 +441,7 @@ int mgg_dbuf_destroy(mgg_dbuf* b) {
   if (!b) return MGG_OK;
   cudaSetDevice(b->ctx->device[b->part]);
   cudaFree(b->ptr);
+  if (b->tc_cache) cudaFree(b->tc_cache);
   delete b;
   return MGG_OK;
 }
@@ -463,12 +530,24 @@ int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in, const mgg_dense_
     if (!in || !d || !out || !d->w) throw Status{MGG_E_INPUT, "dense: null argument"};
     if (out2 && out2->pitch != out->pitch) throw Status{MGG_E_INPUT, "dense: out2 width differs"};
     cudaStream_t st = enter(ctx, part);
+    const float* bias = d->bias ? static_cast<const float*>(d->bias->ptr) : nullptr;
+    const float* pre_bias = d->pre_bias ? static_cast<const float*>(d->pre_bias->ptr) : nullptr;
+    static const bool force_simt = [] {
+      const char* e = std::getenv("MGG_GEMM");
+      return e && std::string(e) == "simt";
+    }();
+    if (!force_simt && gemm_tc_supported(in->dim, out->dim)) {
+      const float* wt = gemm_tc_prepare(const_cast<mgg_dbuf*>(d->w), in->dim, out->dim, st);
+      launch_dense_tc(in->shard[part], in->pitch, in->dim, in->rows(part), wt, bias, pre_bias,
+                      out->dim, d->pre, d->act, out->shard[part], out->pitch,
+                      out2 ? out2->shard[part] : nullptr, d->out2_scale, st);
+      count_launch(ctx);
+      return;
+    }
     launch_dense(in->shard[part], in->pitch, in->dim, in->rows(part),
-                 static_cast<const float*>(d->w->ptr),
-                 d->bias ? static_cast<const float*>(d->bias->ptr) : nullptr,
-                 d->pre_bias ? static_cast<const float*>(d->pre_bias->ptr) : nullptr,
-                 out->dim, d->pre, d->act, out->shard[part], out->pitch,
-                 out2 ? out2->shard[part] : nullptr, d->out2_scale, st);
+                 static_cast<const float*>(d->w->ptr), bias, pre_bias, out->dim, d->pre, d->act,
+                 out->shard[part], out->pitch, out2 ? out2->shard[part] : nullptr,
+                 d->out2_scale, st);
     count_launch(ctx, (out->dim + 63) / 64);
   });
 }

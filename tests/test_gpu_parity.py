@@ -142,3 +142,72 @@ def test_config_change_keeps_results(mgg, oracle_mod):
         assert_rows_close(eng.aggregate(x), ref, what=str(cfg))
         assert eng.time_aggregate(16, reps=3) > 0
     eng.close()
+
+
+def _dense_via_abi(mgg, x, w, b=None, pre=0, pre_bias=None, act=0, out2_scale=None):
+    """One K2 launch through the raw C-ABI (single part on device 0)."""
+    import ctypes as C
+    from paper_2209_06800_b200._lib import DenseDesc, check, lib
+    n, k = x.shape
+    m = w.shape[1]
+    ctx = C.c_void_p()
+    check(lib.mgg_ctx_create(1, (C.c_int32 * 1)(0), C.byref(ctx)))
+    lb = (C.c_uint64 * 2)(0, n)
+    sin, sout, sout2 = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    check(lib.mgg_store_create(ctx, lb, k, C.byref(sin)))
+    check(lib.mgg_store_create(ctx, lb, m, C.byref(sout)))
+    check(lib.mgg_store_create(ctx, lb, m, C.byref(sout2)))
+    fp = C.POINTER(C.c_float)
+    x = np.ascontiguousarray(x, np.float32)
+    check(lib.mgg_store_upload(sin, x.ctypes.data_as(fp), 0, n, k))
+    bufs = []
+
+    def dbuf(a):
+        if a is None:
+            return None
+        a = np.ascontiguousarray(a, np.float32)
+        h = C.c_void_p()
+        check(lib.mgg_dbuf_create(ctx, 0, a.ctypes.data, a.nbytes, C.byref(h)))
+        bufs.append(h)
+        return h
+    d = DenseDesc(dbuf(w), dbuf(b), dbuf(pre_bias), pre, act,
+                  1.0 if out2_scale is None else out2_scale)
+    check(lib.mgg_dense(ctx, 0, sin, C.byref(d), sout, sout2 if out2_scale else None))
+    y = np.zeros((n, m), np.float32)
+    y2 = np.zeros((n, m), np.float32)
+    check(lib.mgg_store_download(sout, y.ctypes.data_as(fp), 0, n, m))
+    check(lib.mgg_store_download(sout2, y2.ctypes.data_as(fp), 0, n, m))
+    check(lib.mgg_ctx_synchronize(ctx))
+    for h in bufs:
+        lib.mgg_dbuf_destroy(h)
+    for s in (sin, sout, sout2):
+        lib.mgg_store_destroy(s)
+    lib.mgg_ctx_destroy(ctx)
+    return y, y2
+
+
+@pytest.mark.parametrize("shape", [(1000, 602, 16), (5000, 100, 64), (333, 64, 47),
+                                   (4097, 16, 41), (129, 37, 5), (7, 200, 64), (2000, 8, 16)])
+@pytest.mark.parametrize("mode", ["plain", "relu_pre", "bias_relu_pre", "softmax", "seed"])
+def test_dense_matches_oracle(mgg, oracle_mod, shape, mode):
+    n, k, m = shape
+    rng = np.random.default_rng(n + k + m)
+    x = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (k, m)) / np.sqrt(k)).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, m).astype(np.float32)
+    pb = rng.uniform(-0.5, 0.5, k).astype(np.float32)
+    kw = dict(plain={}, relu_pre=dict(pre=1), bias_relu_pre=dict(pre=2, pre_bias=pb),
+              softmax=dict(act=2, b=b), seed=dict(out2_scale=1.5, b=b))[mode]
+    y, y2 = _dense_via_abi(mgg, x, w, **kw)
+    xr = x
+    if kw.get("pre") == 1:
+        xr = np.maximum(x, 0)
+    if kw.get("pre") == 2:
+        xr = np.maximum(x + pb, 0)
+    ref = oracle_mod.dense(xr, w, kw.get("b"), act=kw.get("act", 0))
+    if mode == "softmax":
+        assert np.abs(y - ref).max() <= TOL
+    else:
+        assert_rows_close(y, ref, what=f"dense {shape} {mode}")
+    if mode == "seed":
+        assert_rows_close(y2, 1.5 * oracle_mod.dense(xr, w, b), what="out2")
