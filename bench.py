@@ -138,6 +138,18 @@ def agg_bytes(edges: int, parts: int, rows: int, dim: int) -> int:
     return edges * (4 * pitch + 4) + 8 * parts + 2 * rows * 4 * pitch
 
 
+def _traffic(args):
+    """DRAM bytes per K1 launch from the committed ncu capture of this config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            t = json.load(f)
+        if t.get("config") == [args.ps, args.dist, args.wpb]:
+            return t["dram_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
 def cpu_forward_time(g, x, model, threads=0):
     import oracle
     rp, cl = g.row_ptr, g.col_idx
@@ -216,20 +228,20 @@ def main():
     x[:] = mgg.random_features(N_NODES, IN_DIM, seed=1)
     z = mgg.host_alloc((N_NODES, CLASSES))
 
+    from paper_2209_06800_b200 import dist as mdist
     if world > 1:
-        part_device = [-1] * n
-        part_device[rank] = local_rank
+        part_device = mdist.part_devices(world, rank, local_rank)
     else:
         part_device = [0] * n  # N logical partitions on one GPU if --gpus > 1
+    gather_peak = None
+    if rank == 0:  # K5 probe: the gather ceiling of this table shape, live
+        from paper_2209_06800_b200 import probes
+        gather_peak = probes.gather_gbps(N_NODES, HIDDEN, E, device=local_rank)
     t0 = time.perf_counter()
     eng = mgg.Engine(g, n, part_device, model, ps=args.ps, dist=args.dist, wpb=args.wpb)
     setup_s = time.perf_counter() - t0
     if world > 1:
-        blobs = [None] * world
-        dist.all_gather_object(blobs, eng.ipc_export(rank))
-        for p in range(world):
-            if p != rank:
-                eng.ipc_import(p, blobs[p])
+        mdist.exchange_ipc(eng, rank, world)
         dist.barrier()
     eng.set_input(x)
     eng.synchronize()
@@ -265,10 +277,7 @@ def main():
     ops, nfw = eng.profile()
     eng.set_profiling(False)
     if world > 1:
-        import torch
-        t = torch.tensor([total_ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = mdist.max_over_ranks(total_ms)
     ms_step = total_ms / args.steps
     value = 2 * E / (ms_step * 1e-3) / 1e9
 
@@ -296,10 +305,7 @@ def main():
             eng.forward_host(x, z)
         e2e_s = (time.perf_counter() - t0) / k2
         if world > 1:
-            import torch
-            t = torch.tensor([e2e_s], dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s = mdist.max_over_ranks(e2e_s)
         e2e = {"value": round(2 * E / e2e_s / 1e9, 4), "unit": "GEdges/s",
                "ms_per_step": round(e2e_s * 1e3, 3),
                "h2d_bytes_per_step": int(N_NODES * IN_DIM * 4 // (world if world > 1 else 1)),
@@ -332,14 +338,21 @@ def main():
                        "classes": CLASSES, "ps": args.ps, "dist": args.dist, "wpb": args.wpb,
                        "parts": n, "l2": "inputs larger than L2 (X 561 MB + CSR), no flush",
                        "layer_forward_ms": round(ms_step, 4)},
-            "roofline": {"bound": "hbm", "kernel": "K1 aggregation (agg_narrow VEC=4)",
+            "roofline": {"bound": "hbm", "kernel": "K1 aggregation (agg_kernel<4>)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": _traffic(args),
                          "algorithmic_bytes_per_launch": algo,
                          "avg_launch_ms": round(agg_ms_per_launch, 4),
                          "share_of_step": round(share, 4), "peak_source": peak_kind,
-                         "note": "gathered rows (16-wide, 15 MB table) are L2-resident; "
-                                 "algorithmic bytes count every gathered row as in SURVEY §8d"},
+                         "l2_gather": None if not gather_peak else {
+                             "peak": round(gather_peak, 1), "unit": "GB/s",
+                             "frac": round(achieved / gather_peak, 4),
+                             "source": "K5 probe (paper_2209_06800_b200/probes.py), this run"},
+                         "note": "the gathered rows (16-wide, 15 MB table) are L2-resident, so "
+                                 "the binding ceiling is the L2->SM gather rate (l2_gather); "
+                                 "algorithmic bytes count every gathered row as in SURVEY 8d; "
+                                 "traffic = ncu DRAM bytes per launch (profiles/)"},
             "ops": [{"kind": k, "width": w, "ms": round(t / nfw, 4)} for k, w, t in ops],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

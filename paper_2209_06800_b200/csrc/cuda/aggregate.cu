@@ -69,6 +69,9 @@ __device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0
 __device__ __forceinline__ float4 f4relu(float4 a) {
   return make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
 }
+// Read-only path. (An explicit ld.global.nc.L1::no_allocate asm was 45%
+// slower: the volatile asm pins the loads in program order and the compiler
+// can no longer batch the 4 steps' loads ahead of their shuffles.)
 __device__ __forceinline__ float4 ld_row4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
