@@ -1,36 +1,38 @@
 #!/usr/bin/env python
 """Benchmark of the MGG hot path on B200 (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], fits one GPU): 2-layer GCN (hidden 16,
-41 classes) on a synthetic Reddit-shaped graph — 232,965 nodes, reference
-`powerlaw` generator (SplitMix64 seed 0, avg degree 492 -> ~113.6M edges),
-input dim 602, X ~ U[-1,1) (seed 1), Glorot weights (seed 2).
+Default workload (BASELINE.json configs[1], fits one GPU): 2-layer GCN
+(hidden 16, 41 classes) on a synthetic Reddit-shaped graph — 232,965 nodes,
+the reference's `powerlaw` generator (SplitMix64 seed 0, avg degree 492 ->
+114.2M edges), input dim 602, X ~ U[-1,1) (seed 1), Glorot weights (seed 2).
+Other configs (--workload): config1 (RMAT 100K/1.6M, dim 16, 2 logical
+partitions), products-gcn (north_star target shape), products-gin
+(configs[2]), orkut-gcn (configs[3]).
 
-A step = one full GCN forward (both layers: Update GEMM X·W1, K1 layer-1
-aggregation, ReLU-on-load K1 layer-2 aggregation, GEMM·W2 + softmax) over
-the whole graph. metric = aggregation GEdges/s = layers x E / step time
-(and ms_per_step = forward ms). Inputs (X 561 MB + CSR 455 MB) are larger
-than the 126 MB L2, so no flush between steps.
+A step = one full forward (every layer: Update GEMM(s), K1 aggregation(s),
+head) over the whole graph. metric = aggregation GEdges/s = layers x E / step
+time; ms_per_step = forward ms. Inputs (X + CSR, >= 1 GB) exceed the 126 MB
+L2, so no flush between steps.
 
   value   : device-resident X, CUDA events on the engine's stream bracketing
             exactly K steps (barrier + synchronize both sides), max over ranks.
   e2e     : the same metric through the C-ABI `mgg_engine_forward_host`
             with pinned HOST X in / Z out (H2D + D2H inside the timed region).
-  roofline: dominant kernel (K1 aggregation), algorithmic bytes per launch
-            (E·(4D + 4) + 8·P + 8·rows·D) / its average event-timed
-            duration inside the timed region vs MEASURED_PEAKS hbm_gbs.
+  roofline: dominant kernel (K1 aggregation): algorithmic bytes per launch
+            (E·(4·pitch + 4) + 8·P + 8·rows·pitch) / its average
+            event-timed duration inside the timed region, vs MEASURED_PEAKS
+            hbm_gbs; plus the live K5 gather-probe ceiling (l2_gather).
   cpu_baseline: the oracle port (oracle/oracle.c, fp32 accumulate, all host
-            threads) of the same forward on the same graph, rank 0 only.
+            threads) of the same forward on the same graph, rank 0, N=1.
 
 --impl reference: the reference's CPU implementation of the path. The
 reference (pipeshard) has no layer arithmetic, so this arm times the oracle
-port of the forward (same graph/config) on all host cores, and reports the
+port of the forward (same workload) on all host cores, and reports the
 reference library's own metadata-build time beside it when oracle/_ref exists.
 
-Multi-GPU: launched by torchrun, one process per GPU; part r = rank r's
-edge-balanced node range (Alg. 1), remote rows read over NVLink from peer
-shards imported through CUDA IPC; no NCCL on the data path ("scaling":
-"strong" — the graph is fixed as N grows).
+Multi-GPU: torchrun, one process per GPU; part r = rank r's edge-balanced
+node range (Alg. 1); remote rows read in-kernel over NVLink from peer shards
+imported through CUDA IPC; no NCCL on the data path ("scaling": "strong").
 """
 from __future__ import annotations
 
@@ -48,11 +50,20 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_NODES = 232_965
-AVG_DEG = 492
-IN_DIM, HIDDEN, CLASSES = 602, 16, 41
-PS, DIST, WPB = 16, 1, 4
-WORKLOAD = "GCN-2L Reddit-shaped (BASELINE configs[1])"
+# name: (label, graph (kind, nodes, avg_degree | edges), model (kind, in, hidden, out, layers),
+#        tuned (ps, dist, wpb) — profiles/r01_tune_*.json)
+WORKLOADS = {
+    "reddit-gcn": ("GCN-2L Reddit-shaped (BASELINE configs[1])",
+                   ("powerlaw", 232_965, 492), ("gcn", 602, 16, 41, 2), (32, 16, 2)),
+    "config1": ("GCN-2L RMAT 100K/1.6M dim 16, 2 logical partitions (BASELINE configs[0])",
+                ("rmat", 100_000, 1_600_000), ("gcn", 16, 16, 16, 2), (32, 16, 2)),
+    "products-gcn": ("GCN-2L ogbn-products-shaped (north_star target shape)",
+                     ("powerlaw", 2_449_029, 25.259), ("gcn", 100, 16, 47, 2), (32, 16, 2)),
+    "products-gin": ("GIN-5L hidden 64 ogbn-products-shaped (BASELINE configs[2])",
+                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (32, 16, 2)),
+    "orkut-gcn": ("GCN-2L com-Orkut-shaped (BASELINE configs[3])",
+                  ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 2)),
+}
 
 
 def _args():
@@ -61,12 +72,20 @@ def _args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mgg", choices=["mgg", "reference"])
-    ap.add_argument("--ps", type=int, default=PS)
-    ap.add_argument("--dist", type=int, default=DIST)
-    ap.add_argument("--wpb", type=int, default=WPB)
+    ap.add_argument("--workload", default="reddit-gcn", choices=sorted(WORKLOADS))
+    ap.add_argument("--ps", type=int, default=None)
+    ap.add_argument("--dist", type=int, default=None)
+    ap.add_argument("--wpb", type=int, default=None)
+    ap.add_argument("--parts", type=int, default=None,
+                    help="logical partitions on one GPU (single process)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    tuned = WORKLOADS[a.workload][3]
+    a.ps = a.ps or tuned[0]
+    a.dist = a.dist or tuned[1]
+    a.wpb = a.wpb or tuned[2]
+    return a
 
 
 def _peaks():
@@ -125,10 +144,27 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def build_graph(mgg):
+def build(mgg, name):
+    label, gspec, mspec, _ = WORKLOADS[name]
     t0 = time.perf_counter()
-    g = mgg.gen_synthetic(mgg.POWERLAW, N_NODES, AVG_DEG, 0)
-    return g, time.perf_counter() - t0
+    kind, n, avg = gspec
+    if kind == "rmat":
+        g = mgg.gen_rmat(n, int(avg), 0)
+    else:
+        g = mgg.gen_synthetic(mgg.POWERLAW, n, avg, 0)
+    gen_s = time.perf_counter() - t0
+    mk, din, hid, out, layers = mspec
+    model = (mgg.make_gcn(din, hid, out, seed=2) if mk == "gcn"
+             else mgg.make_gin(din, hid, out, layers=layers, seed=2))
+    return label, g, model, gen_s
+
+
+def agg_widths(model):
+    """Aggregation width of each layer (aggregate at min(in, out) width)."""
+    if model.kind == 0:
+        return [min(model.in_dim, model.hidden), min(model.hidden, model.out_dim)]
+    dims = model.gin_dims()
+    return [min(dims[l], model.hidden) for l in range(model.layers)]
 
 
 def agg_bytes(edges: int, parts: int, rows: int, dim: int) -> int:
@@ -143,7 +179,8 @@ def _traffic(args):
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
             t = json.load(f)
-        if t.get("config") == [args.ps, args.dist, args.wpb]:
+        if t.get("workload") == args.workload and t.get("config") == [args.ps, args.dist,
+                                                                        args.wpb]:
             return t["dram_bytes_per_launch"]
     except Exception:  # noqa: BLE001
         pass
@@ -152,47 +189,49 @@ def _traffic(args):
 
 def cpu_forward_time(g, x, model, threads=0):
     import oracle
-    rp, cl = g.row_ptr, g.col_idx
     t0 = time.perf_counter()
-    oracle.gcn2_forward(rp, cl, x, model, acc64=False, threads=threads)
+    if model.kind == 0:
+        oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False, threads=threads)
+    else:
+        oracle.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False, threads=threads)
     return time.perf_counter() - t0
 
 
 def run_reference(args):
     """--impl reference: CPU implementation of the path on the host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     import oracle
     import paper_2209_06800_b200 as mgg
-    g, _ = build_graph(mgg)
+    label, g, model, _ = build(mgg, args.workload)
     e = g.num_edges
-    model = mgg.make_gcn(IN_DIM, HIDDEN, CLASSES, seed=2)
-    x = mgg.random_features(N_NODES, IN_DIM, seed=1)
+    layers = model.layers
+    x = mgg.random_features(g.num_nodes, model.in_dim, seed=1)
     cores = os.cpu_count() or 1
     for _ in range(max(args.warmup, 0)):
         cpu_forward_time(g, x, model)
     times = [cpu_forward_time(g, x, model) for _ in range(max(args.steps, 1))]
     t = sum(times) / len(times)
-    value = 2 * e / t / 1e9
+    value = layers * e / t / 1e9
     meta = None
     if oracle.ref_available():
         r = oracle.RefGraph.from_csr(g.row_ptr, g.col_idx)
-        secs, nparts = r.time_metadata(args.gpus, args.ps, args.dist, args.wpb, IN_DIM)
+        secs, nparts = r.time_metadata(args.gpus, args.ps, args.dist, args.wpb, model.in_dim)
         meta = {"ref_metadata_build_s": round(secs, 4), "partitions": nparts}
     line = {
-        "impl": "reference", "metric": "aggregation GEdges/s (GCN-2L forward)",
+        "impl": "reference", "metric": f"aggregation GEdges/s ({label.split()[0]} forward)",
         "value": round(value, 4), "unit": "GEdges/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "nodes": N_NODES, "edges": e, "dim": IN_DIM,
-                   "hidden": HIDDEN, "classes": CLASSES, "graph": "powerlaw seed 0"},
+        "config": {"workload": label, "nodes": g.num_nodes, "edges": e,
+                   "dim": model.in_dim, "hidden": model.hidden, "classes": model.out_dim,
+                   "layers": layers},
         "cpu_baseline": {"value": round(value, 4), "unit": "GEdges/s", "cores": cores,
                          "kind": "port",
-                         "sample": "full GCN-2L forward of the workload per step "
-                                   "(oracle.c fp32, OpenMP all host threads); the reference "
-                                   "library has no layer arithmetic",
+                         "sample": "full forward of the workload per step (oracle.c fp32, "
+                                   "OpenMP all host threads); the reference library has no "
+                                   "layer arithmetic",
                          "reference_metadata": meta},
         "e2e": {"value": round(value, 4), "unit": "GEdges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -206,12 +245,13 @@ def main():
         run_reference(args)
         return
 
-    import paper_2209_06800_b200 as mgg
+    import ctypes
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    n = max(args.gpus, world)
+    import paper_2209_06800_b200 as mgg
+    from paper_2209_06800_b200 import dist as mdist
+    from paper_2209_06800_b200._lib import lib
+
+    world, rank, local_rank = mdist.env_world()
     dist = None
     if world > 1:
         import torch
@@ -221,22 +261,25 @@ def main():
     if not mgg.cuda_available():
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU path)")
 
-    g, gen_s = build_graph(mgg)
-    E = g.num_edges
-    model = mgg.make_gcn(IN_DIM, HIDDEN, CLASSES, seed=2)
-    x = mgg.host_alloc((N_NODES, IN_DIM))
-    x[:] = mgg.random_features(N_NODES, IN_DIM, seed=1)
-    z = mgg.host_alloc((N_NODES, CLASSES))
+    label, g, model, gen_s = build(mgg, args.workload)
+    N, E = g.num_nodes, g.num_edges
+    layers = model.layers
+    x = mgg.host_alloc((N, model.in_dim))
+    x[:] = mgg.random_features(N, model.in_dim, seed=1)
+    z = mgg.host_alloc((N, model.out_dim))
 
-    from paper_2209_06800_b200 import dist as mdist
     if world > 1:
+        n = world
         part_device = mdist.part_devices(world, rank, local_rank)
     else:
-        part_device = [0] * n  # N logical partitions on one GPU if --gpus > 1
+        n = args.parts or (2 if args.workload == "config1" else max(args.gpus, 1))
+        part_device = [0] * n  # logical partitions on one GPU
+    widths = agg_widths(model)
+    w0 = widths[0]
     gather_peak = None
-    if rank == 0:  # K5 probe: the gather ceiling of this table shape, live
+    if rank == 0:  # K5 probe: the gather ceiling for this table shape, live
         from paper_2209_06800_b200 import probes
-        gather_peak = probes.gather_gbps(N_NODES, HIDDEN, E, device=local_rank)
+        gather_peak = probes.gather_gbps(N, w0, min(E, 200_000_000), device=local_rank)
     t0 = time.perf_counter()
     eng = mgg.Engine(g, n, part_device, model, ps=args.ps, dist=args.dist, wpb=args.wpb)
     setup_s = time.perf_counter() - t0
@@ -245,8 +288,6 @@ def main():
         dist.barrier()
     eng.set_input(x)
     eng.synchronize()
-
-    from paper_2209_06800_b200._lib import lib
     ctx = eng.ctx()
     my_part = rank if world > 1 else 0
 
@@ -262,16 +303,15 @@ def main():
         eng.synchronize()
         if world > 1:
             dist.barrier()
-        lib.mgg_event_record(ctx, my_part, 1000)
+        lib.mgg_event_record(ctx, my_part, 100000)
         for _ in range(args.steps):
             eng.forward()
-        lib.mgg_event_record(ctx, my_part, 1001)
+        lib.mgg_event_record(ctx, my_part, 100001)
         eng.synchronize()
         if world > 1:
             dist.barrier()
-    import ctypes
     ms = ctypes.c_float()
-    lib.mgg_event_elapsed(ctx, my_part, 1000, 1001, ctypes.byref(ms))
+    lib.mgg_event_elapsed(ctx, my_part, 100000, 100001, ctypes.byref(ms))
     total_ms = ms.value
     launches = eng.stats()["launches"] - launches0
     ops, nfw = eng.profile()
@@ -279,21 +319,21 @@ def main():
     if world > 1:
         total_ms = mdist.max_over_ranks(total_ms)
     ms_step = total_ms / args.steps
-    value = 2 * E / (ms_step * 1e-3) / 1e9
+    value = layers * E / (ms_step * 1e-3) / 1e9
 
-    # dominant kernel: aggregation (K1) launches inside the timed region
+    # dominant kernel: the first layer's K1 launch(es) inside the timed region
     st = eng.stats()
-    agg = [(w, t) for k, w, t in ops if k == "aggregate"]
-    agg_ms_per_launch = sum(t for _, t in agg) / (len(agg) * nfw)
+    agg = [t for k, w, t in ops if k == "aggregate" and w == w0]
+    agg_ms_per_launch = agg[0] / nfw if agg else float("nan")
     my_edges = st["local_edges"] + st["remote_edges"]
     my_parts = st["local_parts"] + st["remote_parts"]
-    rows = N_NODES if world == 1 else N_NODES // world
-    algo = agg_bytes(my_edges, my_parts, rows, HIDDEN)
+    rows = N if world == 1 else N // world
+    algo = agg_bytes(my_edges, my_parts, rows, w0)
     peak, peak_kind = _peaks()
     achieved = algo / (agg_ms_per_launch * 1e-3) / 1e9
-    share = sum(t for _, t in agg) / max(sum(t for _, _, t in ops), 1e-9)
+    total_op_ms = max(sum(t for _, _, t in ops), 1e-9)
+    share = sum(t for k, _, t in ops if k == "aggregate") / total_op_ms
 
-    # end to end through the C-ABI with host buffers
     e2e = None
     if not args.no_e2e:
         eng.forward_host(x, z)
@@ -306,39 +346,41 @@ def main():
         e2e_s = (time.perf_counter() - t0) / k2
         if world > 1:
             e2e_s = mdist.max_over_ranks(e2e_s)
-        e2e = {"value": round(2 * E / e2e_s / 1e9, 4), "unit": "GEdges/s",
+        shard = world if world > 1 else 1
+        e2e = {"value": round(layers * E / e2e_s / 1e9, 4), "unit": "GEdges/s",
                "ms_per_step": round(e2e_s * 1e3, 3),
-               "h2d_bytes_per_step": int(N_NODES * IN_DIM * 4 // (world if world > 1 else 1)),
-               "d2h_bytes_per_step": int(N_NODES * CLASSES * 4 // (world if world > 1 else 1)),
+               "h2d_bytes_per_step": int(N * model.in_dim * 4 // shard),
+               "d2h_bytes_per_step": int(N * model.out_dim * 4 // shard),
                "api": "mgg_engine_forward_host (pinned host X in, Z out)"}
 
     cpu = None
-    if rank == 0 and n == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            xs = np.asarray(x)
-            tc = cpu_forward_time(g, xs, model)
-            cpu = {"value": round(2 * E / tc / 1e9, 4), "unit": "GEdges/s",
+            tc = cpu_forward_time(g, np.asarray(x), model)
+            cpu = {"value": round(layers * E / tc / 1e9, 4), "unit": "GEdges/s",
                    "cores": os.cpu_count(), "kind": "port",
-                   "sample": "one full GCN-2L forward of the same workload "
-                             "(oracle.c, fp32 accumulate, OpenMP all host threads)",
+                   "sample": "one full forward of the same workload (oracle.c, fp32 "
+                             "accumulate, OpenMP all host threads)",
                    "seconds": round(tc, 3)}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "error": str(ex)[:200]}
 
     if rank == 0:
         line = {
-            "metric": "aggregation GEdges/s (GCN-2L forward)",
-            "value": round(value, 4), "unit": "GEdges/s", "n_gpus": n,
+            "metric": f"aggregation GEdges/s ({label.split()[0]} forward)",
+            "value": round(value, 4), "unit": "GEdges/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "graph": "powerlaw (reference generator) seed 0",
-                       "nodes": N_NODES, "edges": E, "dim": IN_DIM, "hidden": HIDDEN,
-                       "classes": CLASSES, "ps": args.ps, "dist": args.dist, "wpb": args.wpb,
-                       "parts": n, "l2": "inputs larger than L2 (X 561 MB + CSR), no flush",
+            "config": {"workload": label, "graph": f"{WORKLOADS[args.workload][1][0]} "
+                                                   "(reference/RMAT generator) seed 0",
+                       "nodes": N, "edges": E, "dim": model.in_dim, "hidden": model.hidden,
+                       "classes": model.out_dim, "layers": layers, "agg_widths": widths,
+                       "ps": args.ps, "dist": args.dist, "wpb": args.wpb, "parts": n,
+                       "l2": "inputs larger than L2 (X + CSR >= 1 GB), no flush",
                        "layer_forward_ms": round(ms_step, 4)},
-            "roofline": {"bound": "hbm", "kernel": "K1 aggregation (agg_kernel<4>)",
+            "roofline": {"bound": "hbm", "kernel": f"K1 aggregation, width {w0}",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": _traffic(args),
@@ -349,10 +391,9 @@ def main():
                              "peak": round(gather_peak, 1), "unit": "GB/s",
                              "frac": round(achieved / gather_peak, 4),
                              "source": "K5 probe (paper_2209_06800_b200/probes.py), this run"},
-                         "note": "the gathered rows (16-wide, 15 MB table) are L2-resident, so "
-                                 "the binding ceiling is the L2->SM gather rate (l2_gather); "
-                                 "algorithmic bytes count every gathered row as in SURVEY 8d; "
-                                 "traffic = ncu DRAM bytes per launch (profiles/)"},
+                         "note": "gathered rows are counted per edge (SURVEY 8d); when the "
+                                 "gather table fits L2 the binding ceiling is the L2->SM "
+                                 "gather rate (l2_gather); traffic = ncu DRAM bytes/launch"},
             "ops": [{"kind": k, "width": w, "ms": round(t / nfw, 4)} for k, w, t in ops],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
