@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -33,7 +34,14 @@ namespace {
 constexpr int BM = 128;            // rows per tile (UMMA M)
 constexpr int BK = 32;             // fp32 per 128-B swizzle row
 constexpr int kTileBytes = BM * BK * 4;  // 16 KB
-constexpr int kThreads = 256;
+constexpr uint32_t kMaxStages = 8;
+constexpr uint32_t kLoSlots = 2;  // Xl twin tiles (decoupled from the TMA ring)
+// Epilogue warpgroups: two (alternating accumulators) while a thread's row of
+// NP fp32 fits the 128-register budget of a 512-thread CTA, else one.
+template <int NP>
+constexpr int kEpiGroups = NP <= 48 ? 2 : 1;
+template <int NP>
+constexpr int kThreadsFor = 256 + 128 * kEpiGroups<NP>;
 
 struct TcArgs {
   uint64_t rows;
@@ -117,32 +125,44 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+#ifndef MGG_TC_WRITE_HI
+#define MGG_TC_WRITE_HI 0
+#endif
+constexpr bool kWriteHi = MGG_TC_WRITE_HI != 0;
+
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
 template <int NP>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
                    const __grid_constant__ CUtensorMap map_w, TcArgs a) {
-  constexpr uint32_t kAccCols = NP;  // fp32 columns per accumulator
-  constexpr uint32_t kTmemCols = (2 * NP <= 32) ? 32 : (2 * NP <= 64) ? 64 : (2 * NP <= 128) ? 128
-                                 : (2 * NP <= 256) ? 256 : 512;
-  constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                              (static_cast<uint32_t>(NP >> 3) << 17) | ((BM >> 4) << 24);
+  // Accumulator = [Xh·Wh + Xl·Wh | Xh·Wl]: 2·NP fp32 columns, so Xh feeds one
+  // N=2NP MMA against [Wh; Wl] and is read from smem once per k-step.
+  constexpr uint32_t kAccCols = 2 * NP;
+  constexpr uint32_t kTmemCols = (2 * kAccCols <= 32) ? 32 : (2 * kAccCols <= 64) ? 64
+                                 : (2 * kAccCols <= 128) ? 128 : (2 * kAccCols <= 256) ? 256 : 512;
+  constexpr uint32_t kIdescBase = (1u << 4) | (2u << 7) | (2u << 10) | ((BM >> 4) << 24);
+  constexpr uint32_t kIdesc2 = kIdescBase | (static_cast<uint32_t>((2 * NP) >> 3) << 17);
+  constexpr uint32_t kIdesc1 = kIdescBase | (static_cast<uint32_t>(NP >> 3) << 17);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const uint32_t wbytes = a.n_kb * 2 * NP * 128;
   uint8_t* w_s = smem;                          // [kb][hi|lo][NP][128 B]
-  uint8_t* x_s = smem + wbytes;                 // [stage][hi|lo][16 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(x_s + a.stages * 2 * kTileBytes);
+  uint8_t* x_s = smem + wbytes;                 // [stage][16 KB] raw X -> Xh in place
+  uint8_t* lo_s = x_s + a.stages * kTileBytes;  // [kLoSlots][16 KB] Xl
+  constexpr uint32_t kEpLd = NP + 4;  // padded row (floats): conflict-free float4 rows
+  float* ep_s = reinterpret_cast<float*>(lo_s + kLoSlots * kTileBytes);  // [groups][128][kEpLd]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpiGroups<NP> * BM * kEpLd);
   uint64_t* full = bars;
   uint64_t* split = bars + a.stages;
   uint64_t* empty = bars + 2 * a.stages;
   uint64_t* tfull = bars + 3 * a.stages;      // [2]
   uint64_t* tempty = tfull + 2;               // [2]
-  uint64_t* wfull = tempty + 2;
+  uint64_t* lofree = tempty + 2;              // [kLoSlots]
+  uint64_t* wfull = lofree + kLoSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 128);
     }
+    for (uint32_t i = 0; i < kLoSlots; ++i) mbar_init(&lofree[i], 1);
     mbar_init(wfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -185,49 +206,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], kTileBytes);
-          tma_2d(x_s + s * 2 * kTileBytes, &map_x, &full[s], kb * BK, t * BM);
+          tma_2d(x_s + s * kTileBytes, &map_x, &full[s], kb * BK, t * BM);
           if (++s == a.stages) s = 0, ph ^= 1;
         }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       mbar_wait(wfull, 0);
-      uint32_t s = 0, ph = 0, it = 0;
+      uint32_t s = 0, ph = 0, it = 0, kcount = 0;
       for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
         const uint32_t acc = it & 1, aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * kAccCols;
-        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb, ++kcount) {
+          const uint32_t l = kcount % kLoSlots;
           mbar_wait(&split[s], ph);
           tc_fence_after();
-          const uint64_t xh = umma_desc(su32(x_s + s * 2 * kTileBytes));
-          const uint64_t xl = umma_desc(su32(x_s + s * 2 * kTileBytes + kTileBytes));
-          const uint64_t wh = umma_desc(su32(w_s + kb * 2 * NP * 128));
-          const uint64_t wl = umma_desc(su32(w_s + kb * 2 * NP * 128 + NP * 128));
+          const uint64_t xh = umma_desc(su32(x_s + s * kTileBytes));
+          const uint64_t xl = umma_desc(su32(lo_s + l * kTileBytes));
+          const uint64_t wh = umma_desc(su32(w_s + kb * 2 * NP * 128));  // [Wh; Wl]
 #pragma unroll
           for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B
             const uint64_t o = 2 * k;
-            mma_tf32(d, xh + o, wh + o, kIdesc, (kb | k) != 0);
-            mma_tf32(d, xh + o, wl + o, kIdesc, 1);
-            mma_tf32(d, xl + o, wh + o, kIdesc, 1);
+            mma_tf32(d, xh + o, wh + o, kIdesc2, (kb | k) != 0);  // [Xh·Wh | Xh·Wl]
+            mma_tf32(d, xl + o, wh + o, kIdesc1, 1);              // += Xl·Wh
           }
-          mma_commit(&empty[s]);  // smem stage free once these MMAs retire
+          mma_commit(&empty[s]);   // X stage free once these MMAs retire
+          mma_commit(&lofree[l]);  // and the Xl slot
           if (++s == a.stages) s = 0, ph ^= 1;
         }
         mma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {
-    // ---------------- split + epilogue warpgroup
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- split warpgroup
     const int tid = threadIdx.x - 128;  // 0..127
-    const int g = warp - 4;             // TMEM lane quarter
-    uint32_t s = 0, ph = 0, it = 0;
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+    uint32_t s = 0, ph = 0, kcount = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (uint32_t kb = 0; kb < a.n_kb; ++kb, ++kcount) {
+        const uint32_t l = kcount % kLoSlots;
         mbar_wait(&full[s], ph);
-        float4* hi = reinterpret_cast<float4*>(x_s + s * 2 * kTileBytes);
-        float4* lo = reinterpret_cast<float4*>(x_s + s * 2 * kTileBytes + kTileBytes);
+        mbar_wait(&lofree[l], ((kcount / kLoSlots) & 1) ^ 1);
+        float4* hi = reinterpret_cast<float4*>(x_s + s * kTileBytes);
+        float4* lo = reinterpret_cast<float4*>(lo_s + l * kTileBytes);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int i = tid + 128 * j;  // float4 slot in the 16 KB tile
@@ -245,65 +267,88 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          hi[i] = h;
+          // The tf32 MMA reads only the top 19 bits of each fp32 operand, so
+          // the raw tile already is Xh; it is rewritten only when pre() changed it.
+          if (a.pre || kWriteHi) hi[i] = h;
           lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&split[s]);
         if (++s == a.stages) s = 0, ph ^= 1;
       }
-      // epilogue for tile t
+    }
+  } else if (warp >= 8) {
+    // ---------------- epilogue warpgroup(s) (overlap the next tiles' split);
+    // with two groups, group e drains accumulator e (tiles it % 2 == e)
+    const int eg = (warp - 8) / 4;
+    const int g = warp % 4;  // TMEM lane quarter
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      if (kEpiGroups<NP> == 2 && static_cast<int>(it & 1) != eg) continue;
       const uint32_t acc = it & 1, aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       float y[NP];
 #pragma unroll
-      for (int c = 0; c < NP; c += 16)
-        tmem_ld16(tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16) + c, y + c);
+      for (int c = 0; c < NP; c += 16) {
+        float y2[16];
+        const uint32_t ta = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16) + c;
+        tmem_ld16(ta, y + c);
+        tmem_ld16(ta + NP, y2);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) y[c + q] += y2[q];
+      }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      const uint64_t row = static_cast<uint64_t>(t) * BM + 32 * g + lane;
-      if (row < a.rows) {
-#pragma unroll
-        for (int c = 0; c < NP; ++c)
-          if (a.bias && c < static_cast<int>(a.m)) y[c] += __ldg(a.bias + c);
-        if (a.out2) {
-          float* o2 = a.out2 + row * a.out_pitch;
-#pragma unroll
-          for (int c = 0; c < NP; c += 4)
-            if (c < static_cast<int>(a.out_pitch))
-              *reinterpret_cast<float4*>(o2 + c) =
-                  make_float4(c + 0 < (int)a.m ? y[c + 0] * a.out2_scale : 0.f,
-                              c + 1 < (int)a.m ? y[c + 1] * a.out2_scale : 0.f,
-                              c + 2 < (int)a.m ? y[c + 2] * a.out2_scale : 0.f,
-                              c + 3 < (int)a.m ? y[c + 3] * a.out2_scale : 0.f);
-        }
-        if (a.act == 1) {
-#pragma unroll
-          for (int c = 0; c < NP; ++c) y[c] = fmaxf(y[c], 0.f);
-        } else if (a.act == 2) {
-          float mx = -FLT_MAX;
-#pragma unroll
-          for (int c = 0; c < NP; ++c)
-            if (c < static_cast<int>(a.m)) mx = fmaxf(mx, y[c]);
-          float sum = 0.f;
-#pragma unroll
-          for (int c = 0; c < NP; ++c) {
-            y[c] = c < static_cast<int>(a.m) ? __expf(y[c] - mx) : 0.f;
-            sum += y[c];
-          }
-          const float inv = 1.f / sum;
-#pragma unroll
-          for (int c = 0; c < NP; ++c) y[c] *= inv;
-        }
-        float* o = a.out + row * a.out_pitch;
+      // Each thread holds its row; stage the warp's 32 rows in padded smem and
+      // store them cooperatively (consecutive lanes -> consecutive float4 of a
+      // row: coalesced, full sectors) instead of 32 scattered row writes.
+      float* ep = ep_s + (eg * BM + 32 * g) * kEpLd;
+      const uint64_t row0 = static_cast<uint64_t>(t) * BM + 32 * g;
+      const uint64_t left = a.rows > row0 ? a.rows - row0 : 0;
+      const int nrows = left < 32 ? static_cast<int>(left) : 32;
+      constexpr int kF4 = NP / 4;  // float4 per staged row
+      const int out_f4 = static_cast<int>(a.out_pitch / 4);
+      auto stage_and_store = [&](float* dst, float scale) {
 #pragma unroll
         for (int c = 0; c < NP; c += 4)
-          if (c < static_cast<int>(a.out_pitch))
-            *reinterpret_cast<float4*>(o + c) =
-                make_float4(c + 0 < (int)a.m ? y[c + 0] : 0.f, c + 1 < (int)a.m ? y[c + 1] : 0.f,
-                            c + 2 < (int)a.m ? y[c + 2] : 0.f, c + 3 < (int)a.m ? y[c + 3] : 0.f);
+          *reinterpret_cast<float4*>(ep + lane * kEpLd + c) =
+              make_float4(c + 0 < (int)a.m ? y[c + 0] * scale : 0.f,
+                          c + 1 < (int)a.m ? y[c + 1] * scale : 0.f,
+                          c + 2 < (int)a.m ? y[c + 2] * scale : 0.f,
+                          c + 3 < (int)a.m ? y[c + 3] * scale : 0.f);
+        __syncwarp();
+        for (int i = lane; i < 32 * kF4; i += 32) {
+          const int r = i / kF4, c4 = i % kF4;
+          if (r < nrows && c4 < out_f4)
+            *reinterpret_cast<float4*>(dst + (row0 + r) * a.out_pitch + 4 * c4) =
+                *reinterpret_cast<const float4*>(ep + r * kEpLd + 4 * c4);
+        }
+        __syncwarp();
+      };
+#pragma unroll
+      for (int c = 0; c < NP; ++c)
+        if (a.bias && c < static_cast<int>(a.m)) y[c] += __ldg(a.bias + c);
+      if (a.out2) stage_and_store(a.out2, a.out2_scale);
+      if (a.act == 1) {
+#pragma unroll
+        for (int c = 0; c < NP; ++c) y[c] = fmaxf(y[c], 0.f);
+      } else if (a.act == 2) {
+        float mx = -FLT_MAX;
+#pragma unroll
+        for (int c = 0; c < NP; ++c)
+          if (c < static_cast<int>(a.m)) mx = fmaxf(mx, y[c]);
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          y[c] = c < static_cast<int>(a.m) ? __expf(y[c] - mx) : 0.f;
+          sum += y[c];
+        }
+        const float inv = 1.f / sum;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) y[c] *= inv;
       }
+      stage_and_store(a.out, 1.f);
     }
   }
   tc_fence_before();
@@ -365,11 +410,13 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
             const TcArgs& a, cudaStream_t st) {
   const size_t wbytes = static_cast<size_t>(a.n_kb) * 2 * NP * 128;
   TcArgs b = a;
-  b.stages = 4;
+  b.stages = kMaxStages;
   auto smem_for = [&](uint32_t stages) {
-    return 1024 + wbytes + stages * 2 * kTileBytes + (3 * stages + 5) * 8 + 16;
+    return 1024 + wbytes + (stages + kLoSlots) * kTileBytes +
+           kEpiGroups<NP> * BM * (NP + 4) * 4 + (3 * stages + 5 + kLoSlots) * 8 + 16;
   };
   while (b.stages > 2 && smem_for(b.stages) > 227 * 1024) --b.stages;
+  if (b.stages > 2 * a.n_kb + 2) b.stages = 2 * a.n_kb + 2;  // no use beyond ~2 tiles
   const size_t smem = smem_for(b.stages);
   if (smem > 227 * 1024) throw Status{MGG_E_CONFIG, "gemm_tc: W too large for smem"};
   const CUtensorMap mx = make_map(in, a.k, a.rows, size_t(in_pitch) * 4, BK, BM);
@@ -381,17 +428,22 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const uint64_t tiles = (a.rows + BM - 1) / BM;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, sms));
-  gemm_tc_kernel<NP><<<grid, kThreads, smem, st>>>(mx, mw, b);
+  gemm_tc_kernel<NP><<<grid, kThreadsFor<NP>, smem, st>>>(mx, mw, b);
   MGG_CUDA(cudaGetLastError());
 }
 
 }  // namespace
 
 bool gemm_tc_supported(uint32_t k, uint32_t m) {
-  if (m == 0 || m > 64 || k < 64) return false;  // narrow K: the SIMT kernel wins
+  static const uint32_t min_k = [] {
+    const char* e = std::getenv("MGG_TC_MINK");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 8u;
+  }();
+  if (m == 0 || m > 64 || k < min_k || k < 8) return false;
   const uint32_t np = (m + 15) / 16 * 16;
   const size_t wbytes = size_t((k + BK - 1) / BK) * 2 * np * 128;
-  return 1024 + wbytes + 2 * 2 * kTileBytes + 128 <= 227 * 1024;
+  return 1024 + wbytes + (2 + kLoSlots) * kTileBytes + 2 * BM * (np + 4) * 4 + 128 <=
+         227 * 1024;
 }
 
 // Returns the cached device W^T hi/lo block for `w`, building it on first use.
