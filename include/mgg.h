@@ -329,6 +329,12 @@ int mgg_engine_ipc_export(const mgg_engine* e, uint32_t part, void* blob,
                           size_t* len);
 int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob,
                           size_t len);
+/* Ablation mappings (R:proj/src/sim.cpp:571-595): mapping 1 = segregated
+ * (no_interleave), granularity 1 = whole_list (no_np). Re-plans. */
+int mgg_engine_set_mapping(mgg_engine* e, int mapping, int granularity);
+/* remote_partition_bytes (R:proj/src/sim.cpp:503-518): fine-grained or paged. */
+uint64_t mgg_remote_partition_bytes(uint64_t part_size, uint64_t dim, int paged,
+                                    uint64_t page_bytes);
 /* Re-plan with a new (ps, dist, wpb) (tuner hook). */
 int mgg_engine_set_config(mgg_engine* e, uint32_t ps, uint32_t dist, uint32_t wpb);
 /* x: num_nodes x in_dim host rows (only this process's rows are read). */

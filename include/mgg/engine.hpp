@@ -61,6 +61,9 @@ class Engine {
   void import_ipc(std::uint32_t part, const std::vector<std::uint8_t>& blob);
 
   void set_config(const KernelConfig& cfg);
+  /// Ablation knobs of the reference's baselines (R:proj/src/sim.cpp:571-595):
+  /// segregated = no_interleave, whole_list = no_np.
+  void set_mapping(MappingMode mapping, Granularity granularity);
   void set_input(const float* x);            // N x in_dim host rows
   void forward();                            // async, device resident
   void synchronize();
@@ -114,6 +117,8 @@ class Engine {
   std::uint32_t num_parts_;
   std::vector<std::int32_t> dev_;
   KernelConfig cfg_;
+  MappingMode mapping_ = MappingMode::interleaved;
+  Granularity granularity_ = Granularity::partitioned;
   ModelSpec spec_;
   WorkloadSplit split_;
   NePlacement ne_;

@@ -134,6 +134,8 @@ _sig("mgg_engine_destroy", I, vp)
 _sig("mgg_engine_ipc_export", I, vp, U32, vp, C.POINTER(SZ))
 _sig("mgg_engine_ipc_import", I, vp, U32, vp, SZ)
 _sig("mgg_engine_set_config", I, vp, U32, U32, U32)
+_sig("mgg_engine_set_mapping", I, vp, I, I)
+_sig("mgg_remote_partition_bytes", U64, U64, U64, I, U64)
 _sig("mgg_engine_set_input", I, vp, f32p)
 _sig("mgg_engine_forward", I, vp)
 _sig("mgg_engine_get_output", I, vp, f32p)

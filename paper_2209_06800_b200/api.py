@@ -235,6 +235,11 @@ def wpw(ps: int, dist: int, wpb: int, dim: int) -> int:
     return int(lib.mgg_wpw(ps, dist, wpb, dim))
 
 
+def remote_partition_bytes(part_size: int, dim: int, paged: bool = False,
+                           page_bytes: int = 4096) -> int:
+    return int(lib.mgg_remote_partition_bytes(part_size, dim, int(paged), page_bytes))
+
+
 def smem(ps: int, dist: int, wpb: int, dim: int) -> int:
     return int(lib.mgg_smem(ps, dist, wpb, dim))
 
@@ -415,6 +420,9 @@ class Engine:
 
     def set_config(self, ps: int, dist: int, wpb: int) -> None:
         check(lib.mgg_engine_set_config(self._h, ps, dist, wpb))
+
+    def set_mapping(self, mapping: int = INTERLEAVED, granularity: int = PARTITIONED) -> None:
+        check(lib.mgg_engine_set_mapping(self._h, mapping, granularity))
 
     def set_input(self, x: np.ndarray) -> None:
         assert x.dtype == np.float32 and x.flags.c_contiguous

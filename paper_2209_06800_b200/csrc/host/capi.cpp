@@ -446,6 +446,19 @@ int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob, size_t
 int mgg_engine_set_config(mgg_engine* e, uint32_t ps, uint32_t dist, uint32_t wpb) {
   return guard([&] { e->e->set_config(KernelConfig{ps, dist, wpb}); });
 }
+int mgg_engine_set_mapping(mgg_engine* e, int mapping, int granularity) {
+  return guard([&] {
+    e->e->set_mapping(mapping == 0 ? MappingMode::interleaved : MappingMode::segregated,
+                      granularity == 0 ? Granularity::partitioned : Granularity::whole_list);
+  });
+}
+
+uint64_t mgg_remote_partition_bytes(uint64_t part_size, uint64_t dim, int paged,
+                                    uint64_t page_bytes) {
+  return remote_partition_bytes(part_size, dim, paged ? Transport::paged : Transport::fine_grained,
+                                page_bytes);
+}
+
 int mgg_engine_set_input(mgg_engine* e, const float* x) {
   return guard([&] { e->e->set_input(x); });
 }

@@ -188,14 +188,15 @@ void Engine::build_plans() {
   const auto t0 = std::chrono::steady_clock::now();
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
     if (dev_[p] < 0) continue;
-    const FlatPlan fp = build_flat_plan(g_, split_, ne_, p, cfg_, spec_.in_dim);
+    const FlatPlan fp =
+        build_flat_plan(g_, split_, ne_, p, cfg_, spec_.in_dim, mapping_, granularity_);
     mgg_plan_desc d{};
     d.part = p;
     d.ps = cfg_.ps;
     d.dist = cfg_.dist;
     d.wpb = cfg_.wpb;
-    d.mapping = 0;
-    d.granularity = 0;
+    d.mapping = mapping_ == MappingMode::interleaved ? 0 : 1;
+    d.granularity = granularity_ == Granularity::partitioned ? 0 : 1;
     d.rows = fp.rows;
     d.n_local = fp.local.num_parts();
     d.n_remote = fp.remote.num_parts();
@@ -222,6 +223,13 @@ void Engine::set_config(const KernelConfig& cfg) {
   if (!v.empty()) throw ConfigError("engine: config violates " + v.front().constraint);
   ok(mgg_ctx_synchronize(ctx_));
   cfg_ = cfg;
+  build_plans();
+}
+
+void Engine::set_mapping(MappingMode mapping, Granularity granularity) {
+  ok(mgg_ctx_synchronize(ctx_));
+  mapping_ = mapping;
+  granularity_ = granularity;
   build_plans();
 }
 

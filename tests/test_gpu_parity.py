@@ -211,3 +211,22 @@ def test_dense_matches_oracle(mgg, oracle_mod, shape, mode):
         assert_rows_close(y, ref, what=f"dense {shape} {mode}")
     if mode == "seed":
         assert_rows_close(y2, 1.5 * oracle_mod.dense(xr, w, b), what="out2")
+
+
+@pytest.mark.parametrize("mapping,granularity", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("parts", [1, 2, 4])
+def test_ablation_mappings_match_oracle(mgg, oracle_mod, mapping, granularity, parts):
+    """The K4 ablation mappings (no_interleave = segregated, no_np =
+    whole_list; R:proj/src/sim.cpp:571-595) run through the same K1 and give
+    the same sums."""
+    g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 14, 6)
+    for dim in (16, 64, 200):
+        x = mgg.random_features(g.num_nodes, dim, seed=dim)
+        eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 8, 4), ps=8, dist=4, wpb=2)
+        eng.set_mapping(mapping, granularity)
+        assert_rows_close(eng.aggregate(x, 1.0, relu_in=True),
+                          oracle_mod.aggregate(g.row_ptr, g.col_idx, x, relu_in=True),
+                          what=f"map={mapping} gran={granularity} parts={parts} dim={dim}")
+        for phase in (0, 1, 2):
+            assert eng.time_aggregate(dim, reps=2, phase=phase) > 0
+        eng.close()

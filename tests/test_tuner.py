@@ -157,3 +157,14 @@ def test_profiles(mgg):
     assert mgg.resolve_profile("desk").max_warps_per_sm == 2
     wb = mgg.launch_geometry(4, 4, 1, 2, 1, "a100")
     assert wb[:2] == (2, 2)
+
+
+def test_remote_partition_bytes_acceptance(mgg):
+    """R:proj/tests/acceptance.cpp:378-390 (criterion 8)."""
+    for size in (1, 2, 5, 16, 32):
+        fine = mgg.remote_partition_bytes(size, 16, False, 4096)
+        paged = mgg.remote_partition_bytes(size, 16, True, 4096)
+        assert fine == size * 64 and paged == size * 4096
+        assert paged >= 64 * fine
+    assert mgg.remote_partition_bytes(3, 602, True, 4096) == 3 * 4096
+    assert mgg.remote_partition_bytes(3, 2000, True, 4096) == 3 * 8192
