@@ -36,12 +36,19 @@ namespace {
 __global__ void barrier_kernel(unsigned* const* shards, unsigned* own, uint32_t me,
                                uint32_t n, uint32_t epoch) {
   const uint32_t q = threadIdx.x;
+  __threadfence_system();  // this GPU's prior kernels' writes before the flag
   if (q < n) {
     unsigned* slot = shards[q] + me;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
     unsigned seen;
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(own + q) : "memory");
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      // a peer that never arrives (crashed rank) fails the launch instead of
+      // hanging the GPU: 60 s watchdog
+      if (t - t0 > 60ull * 1000000000ull) __trap();
     } while (static_cast<int>(seen - epoch) < 0);
   }
   __syncwarp();
