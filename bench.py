@@ -252,6 +252,9 @@ def main():
     from paper_2209_06800_b200._lib import lib
 
     world, rank, local_rank = mdist.env_world()
+    # MGG_BENCH_DEVICE pins every rank to one device: validates the multi-rank
+    # path (IPC + K3 across processes) on a one-GPU box; never set for numbers
+    local_rank = int(os.environ.get("MGG_BENCH_DEVICE", local_rank))
     dist = None
     if world > 1:
         import torch
