@@ -56,13 +56,13 @@ WORKLOADS = {
     "reddit-gcn": ("GCN-2L Reddit-shaped (BASELINE configs[1])",
                    ("powerlaw", 232_965, 492), ("gcn", 602, 16, 41, 2), (32, 16, 2)),
     "config1": ("GCN-2L RMAT 100K/1.6M dim 16, 2 logical partitions (BASELINE configs[0])",
-                ("rmat", 100_000, 1_600_000), ("gcn", 16, 16, 16, 2), (32, 16, 2)),
+                ("rmat", 100_000, 1_600_000), ("gcn", 16, 16, 16, 2), (32, 16, 1)),
     "products-gcn": ("GCN-2L ogbn-products-shaped (north_star target shape)",
-                     ("powerlaw", 2_449_029, 25.259), ("gcn", 100, 16, 47, 2), (32, 16, 2)),
+                     ("powerlaw", 2_449_029, 25.259), ("gcn", 100, 16, 47, 2), (32, 16, 4)),
     "products-gin": ("GIN-5L hidden 64 ogbn-products-shaped (BASELINE configs[2])",
-                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (32, 16, 2)),
+                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 16, 4)),
     "orkut-gcn": ("GCN-2L com-Orkut-shaped (BASELINE configs[3])",
-                  ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 2)),
+                  ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 4)),
 }
 
 

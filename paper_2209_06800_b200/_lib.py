@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmgg.so")
+# MGG_LIB selects an alternative in-tree build (A/B experiments); default libmgg.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("MGG_LIB", "libmgg.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -35,6 +35,10 @@
 
 #include "common.cuh"
 
+#ifndef MGG_AGG_UNROLL
+#define MGG_AGG_UNROLL 4
+#endif
+
 namespace mgg::dev {
 namespace {
 
@@ -144,18 +148,20 @@ struct Lanes {
     return x;
   }
 
-  // Sum rows [s0*RPW, n) of the window into acc, 4 steps of loads in flight.
+  // Sum rows [s0*RPW, n) of the window into acc, UNR steps of loads in flight
+  // (a 32-column window has 32/RPW steps: 4 at VEC=4, 16 at VEC=16).
+  static constexpr int UNR = MGG_AGG_UNROLL < (32 / RPW) ? MGG_AGG_UNROLL : (32 / RPW);
   template <bool REMOTE>
   __device__ __forceinline__ float4 window(const AggArgs& a, uint32_t colwin, int n, int s0,
                                            float4 acc, const float* tab_lane) const {
     const int steps = (n + RPW - 1) / RPW;
-    for (int s = s0; s < steps; s += 4) {
-      float4 t[4];
+    for (int s = s0; s < steps; s += UNR) {
+      float4 t[UNR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < UNR; ++u)
         t[u] = row<REMOTE>(a, colwin, (s + u) * RPW + sub, (s + u) < steps ? n : 0, tab_lane);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc = f4add(acc, t[u]);
+      for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
     }
     return acc;
   }
