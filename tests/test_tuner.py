@@ -168,3 +168,13 @@ def test_remote_partition_bytes_acceptance(mgg):
         assert paged >= 64 * fine
     assert mgg.remote_partition_bytes(3, 602, True, 4096) == 3 * 4096
     assert mgg.remote_partition_bytes(3, 2000, True, 4096) == 3 * 8192
+
+
+def test_shipped_profiles_match_builtins(mgg):
+    """R:proj/tests/test_costmodel.cpp:162-178, plus the b200 preset."""
+    import os
+    d = os.path.join(os.path.dirname(mgg.LIB_PATH), "profiles")
+    for name in ("a100", "v100", "desk", "b200"):
+        shipped = mgg.resolve_profile(os.path.join(d, name + ".json"))
+        built = mgg.resolve_profile(name)
+        assert shipped == built, name
