@@ -124,6 +124,11 @@ typedef struct {
   const uint32_t* local_cols; uint64_t local_cols_len;
   const int32_t* remote_meta; /* 2*(n_remote+1) */
   const uint32_t* remote_cols; uint64_t remote_cols_len;
+  /* optional deduplicated remote fetch (HaloPlan, include/mgg/workload.hpp):
+   * halo_len distinct packed remote rows, and remote_cols re-pointed at them
+   * (remote_cols_len entries); NULL/0 when unused */
+  const uint32_t* halo_rows; uint64_t halo_len;
+  const uint32_t* remote_halo_cols;
 } mgg_plan_desc;
 
 int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* desc, mgg_dplan** out);
@@ -143,9 +148,18 @@ typedef struct {
   int relu_in;
   int phase; /* 0 all, 1 local partitions only, 2 remote only (phase-split
                 measurement, R:proj/src/sim.cpp:127-142) */
+  const float* halo; /* non-NULL: remote partitions read this part's halo
+                        buffer (filled by mgg_halo_pull) instead of peers */
 } mgg_agg_opts;
 int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
                   mgg_store* out, const mgg_agg_opts* opts);
+
+/* Deduplicated remote fetch: copy the plan's distinct remote rows of `in`
+ * from the peer shards (NVLink) into `halo` (halo_len x pitch floats, device
+ * memory of the plan's part), one coalesced pass; the next mgg_aggregate
+ * with opts.halo reads them locally. */
+int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, float* halo);
+int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* halo_len);
 
 /* out[r] = scale * f(in[r]) for the part's own rows (self term / copies).
  * f: 0 identity, 1 ReLU. */
@@ -329,6 +343,10 @@ int mgg_engine_ipc_export(const mgg_engine* e, uint32_t part, void* blob,
                           size_t* len);
 int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob,
                           size_t len);
+/* Remote fetch: 0 auto (halo when it moves >= 2x fewer bytes), 1 fine
+ * (per-edge peer reads in K1, the paper's design), 2 halo (deduplicated
+ * pull, then local reads). Re-plans. */
+int mgg_engine_set_remote_fetch(mgg_engine* e, int mode);
 /* Ablation mappings (R:proj/src/sim.cpp:571-595): mapping 1 = segregated
  * (no_interleave), granularity 1 = whole_list (no_np). Re-plans. */
 int mgg_engine_set_mapping(mgg_engine* e, int mapping, int granularity);
@@ -355,8 +373,9 @@ int mgg_engine_aggregate_host(mgg_engine* e, const float* x, uint32_t dim,
  * config, max over local parts — the tuner's SimulateFn. */
 int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps,
                               int phase, uint64_t* median_ns);
-/* stats[8] = {local_parts_total, remote_parts_total, local_edges,
- * remote_edges, num_warps, num_blocks, kernel_launches, plan_build_ns} */
+/* stats[10] = {local_parts_total, remote_parts_total, local_edges,
+ * remote_edges, num_warps, num_blocks, kernel_launches, plan_build_ns,
+ * halo_rows, halo_parts} */
 int mgg_engine_stats(const mgg_engine* e, uint64_t* stats);
 mgg_ctx* mgg_engine_ctx(mgg_engine* e);
 /* Per-op device timing of subsequent forwards (events around every op of the

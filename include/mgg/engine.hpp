@@ -64,6 +64,11 @@ class Engine {
   /// Ablation knobs of the reference's baselines (R:proj/src/sim.cpp:571-595):
   /// segregated = no_interleave, whole_list = no_np.
   void set_mapping(MappingMode mapping, Granularity granularity);
+  /// Remote rows: per-edge peer reads inside K1 (fine, the paper's design),
+  /// one deduplicated halo pull per layer then local reads (halo, a B200
+  /// addition), or auto = halo when it moves >= 2x fewer NVLink bytes.
+  enum class RemoteFetch { automatic, fine, halo };
+  void set_remote_fetch(RemoteFetch mode);
   void set_input(const float* x);            // N x in_dim host rows
   void forward();                            // async, device resident
   void synchronize();
@@ -90,7 +95,7 @@ class Engine {
   struct Stats {
     std::uint64_t local_parts = 0, remote_parts = 0, local_edges = 0,
                   remote_edges = 0, warps = 0, blocks = 0, launches = 0,
-                  plan_build_ns = 0;
+                  plan_build_ns = 0, halo_rows = 0, halo_parts = 0;
   };
   Stats stats() const;
 
@@ -112,6 +117,11 @@ class Engine {
   void free_plans();
   void run(const Op& op);
   mgg_store* scratch(std::uint32_t dim, int slot);
+  /// Halo buffer of part p for gather width `dim` (null when p reads fine).
+  const float* halo_for(std::uint32_t p, std::uint32_t dim);
+  RemoteFetch fetch_ = RemoteFetch::automatic;
+  std::vector<std::uint8_t> halo_on_;                        // per part
+  std::vector<std::vector<std::pair<std::uint32_t, mgg_dbuf*>>> halo_bufs_;  // per part
 
   const CsrGraph& g_;
   std::uint32_t num_parts_;

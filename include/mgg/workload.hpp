@@ -140,6 +140,19 @@ struct FlatPlan {
   KernelLaunchPlan expand() const;
 };
 
+/// Deduplicated remote fetch plan of one gpu (a B200 addition; metadata of
+/// the partitions is unchanged): the distinct remote rows its remote
+/// partitions read, sorted by (owner, offset) so each peer shard is read in
+/// address order, and the remote columns re-pointed at that compact halo.
+/// One layer's remote traffic becomes unique_rows·D·4 bytes instead of
+/// remote_edges·D·4 (Reddit-shaped, 8 GPUs: ~60x fewer NVLink bytes).
+struct HaloPlan {
+  std::vector<std::uint32_t> rows;       // packed (owner << 28) | offset
+  std::vector<std::uint32_t> cols;       // remote column i -> halo row
+  double dedup_ratio() const;            // remote columns per halo row
+};
+HaloPlan build_halo_plan(const FlatPlan& plan);
+
 /// Split + partition + (implicit) warp/block mapping for one gpu, straight
 /// from the CSR, multi-threaded. Same errors as build_launch_plan for bad
 /// ps/dist/wpb; ConfigError if the packed encoding cannot address the

@@ -41,11 +41,12 @@ class PlanDesc(C.Structure):
                 ("wpb", C.c_uint32), ("mapping", C.c_uint32), ("granularity", C.c_uint32),
                 ("rows", C.c_uint64), ("n_local", C.c_uint64), ("n_remote", C.c_uint64),
                 ("local_meta", i32p), ("local_cols", u32p), ("local_cols_len", C.c_uint64),
-                ("remote_meta", i32p), ("remote_cols", u32p), ("remote_cols_len", C.c_uint64)]
+                ("remote_meta", i32p), ("remote_cols", u32p), ("remote_cols_len", C.c_uint64),
+                ("halo_rows", u32p), ("halo_len", C.c_uint64), ("remote_halo_cols", u32p)]
 
 
 class AggOpts(C.Structure):
-    _fields_ = [("relu_in", C.c_int), ("phase", C.c_int)]
+    _fields_ = [("relu_in", C.c_int), ("phase", C.c_int), ("halo", vp)]
 
 
 class DenseDesc(C.Structure):
@@ -136,6 +137,9 @@ _sig("mgg_engine_ipc_export", I, vp, U32, vp, C.POINTER(SZ))
 _sig("mgg_engine_ipc_import", I, vp, U32, vp, SZ)
 _sig("mgg_engine_set_config", I, vp, U32, U32, U32)
 _sig("mgg_engine_set_mapping", I, vp, I, I)
+_sig("mgg_engine_set_remote_fetch", I, vp, I)
+_sig("mgg_halo_pull", I, vp, vp, vp, vp)
+_sig("mgg_dplan_halo_len", I, vp, u64p)
 _sig("mgg_remote_partition_bytes", U64, U64, U64, I, U64)
 _sig("mgg_engine_set_input", I, vp, f32p)
 _sig("mgg_engine_forward", I, vp)

@@ -421,6 +421,11 @@ class Engine:
     def set_config(self, ps: int, dist: int, wpb: int) -> None:
         check(lib.mgg_engine_set_config(self._h, ps, dist, wpb))
 
+    FETCH = {"auto": 0, "fine": 1, "halo": 2}
+
+    def set_remote_fetch(self, mode: str = "auto") -> None:
+        check(lib.mgg_engine_set_remote_fetch(self._h, self.FETCH[mode]))
+
     def set_mapping(self, mapping: int = INTERLEAVED, granularity: int = PARTITIONED) -> None:
         check(lib.mgg_engine_set_mapping(self._h, mapping, granularity))
 
@@ -486,10 +491,10 @@ class Engine:
         return lib.mgg_engine_ctx(self._h)
 
     def stats(self) -> dict:
-        s = np.zeros(8, np.uint64)
+        s = np.zeros(10, np.uint64)
         check(lib.mgg_engine_stats(self._h, _p(s, C.c_uint64)))
         keys = ["local_parts", "remote_parts", "local_edges", "remote_edges", "warps",
-                "blocks", "launches", "plan_build_ns"]
+                "blocks", "launches", "plan_build_ns", "halo_rows", "halo_parts"]
         return {k: int(v) for k, v in zip(keys, s)}
 
 

@@ -60,6 +60,7 @@ struct AggArgs {
   uint32_t num_lblocks;       // logical CTAs = ceil(num_warps / wpb)
   uint32_t num_owners;
   int phase;                  // 0 all, 1 local only, 2 remote only
+  const float* halo;          // deduplicated remote rows (halo mode) or null
 };
 
 constexpr uint32_t kShift = 28;
@@ -139,7 +140,7 @@ struct Lanes {
                                         const float* tab_lane) const {
     const uint32_t c = __shfl_sync(kFull, colwin, r & 31);
     const float* base = a.own;
-    if (REMOTE) base = shfl_ptr(tab_lane, static_cast<int>(c >> kShift));
+    if (REMOTE) base = a.halo ? a.halo : shfl_ptr(tab_lane, static_cast<int>(c >> kShift));
     float4 x = f4zero();
     if (vlane && r < n) {
       x = ld_row4(base + static_cast<size_t>(c & kMask) * a.pitch + 4 * v);
@@ -332,7 +333,8 @@ __global__ void __launch_bounds__(512) agg_wide(AggArgs a) {
           for (int k = m0.y; k < end; ++k) {
             const uint32_t c = __ldg(cols + k);
             const float* row =
-                (remote ? a.table[c >> kShift] : a.own) + (size_t)(c & kMask) * a.pitch;
+                (remote ? (a.halo ? a.halo : a.table[c >> kShift]) : a.own) +
+                (size_t)(c & kMask) * a.pitch;
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
               const uint32_t col = c0 + lane + 32 * j;
@@ -420,15 +422,47 @@ __global__ void rows_init_kernel(const float4* __restrict__ in, float4* __restri
   }
 }
 
+// Deduplicated remote fetch: halo[r] = table[owner(r)][offset(r)] for the
+// plan's distinct remote rows (sorted by owner, offset: each peer shard is
+// streamed in address order). Consecutive threads copy consecutive float4
+// of a row: coalesced NVLink reads, coalesced local writes.
+__global__ void __launch_bounds__(256) halo_pull_kernel(const uint32_t* __restrict__ rows,
+                                                        uint64_t n,
+                                                        const float* const* __restrict__ table,
+                                                        uint32_t pitch,
+                                                        float4* __restrict__ halo) {
+  const uint32_t vec = pitch / 4;
+  const uint64_t total = n * vec;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+#pragma unroll 4
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint64_t r = i / vec;
+    const uint32_t c4 = static_cast<uint32_t>(i - r * vec);
+    const uint32_t c = __ldg(rows + r);
+    halo[i] = ld_row4(table[c >> kShift] + static_cast<size_t>(c & kMask) * pitch + 4 * c4);
+  }
+}
+
 }  // namespace
 
+void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st) {
+  if (!p->halo_len) return;
+  const uint64_t total = p->halo_len * (in->pitch / 4);
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148 * 8));
+  halo_pull_kernel<<<blocks, 256, 0, st>>>(p->halo_rows, p->halo_len, in->dtable[p->part],
+                                           in->pitch, reinterpret_cast<float4*>(halo));
+  MGG_CUDA(cudaGetLastError());
+}
+
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
-                      mgg_store* out, int relu_in, int phase, cudaStream_t st) {
+                      mgg_store* out, int relu_in, int phase, const float* halo,
+                      cudaStream_t st) {
   AggArgs a{};
   a.lmeta = p->lmeta;
   a.lcols = p->lcols;
   a.rmeta = p->rmeta;
-  a.rcols = p->rcols;
+  a.rcols = halo ? p->rcols_halo : p->rcols;
+  a.halo = halo;
   a.table = in->dtable[p->part];
   a.own = in->shard[p->part];
   a.out = out->shard[p->part];

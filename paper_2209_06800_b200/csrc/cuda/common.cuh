@@ -69,6 +69,9 @@ struct mgg_dplan {
   int2* rmeta = nullptr;
   uint32_t* rcols = nullptr;
   uint64_t num_warps = 0, num_local_warps = 0;
+  uint32_t* halo_rows = nullptr;   // distinct packed remote rows
+  uint64_t halo_len = 0;
+  uint32_t* rcols_halo = nullptr;  // remote columns -> halo rows
 };
 
 namespace mgg::dev {
@@ -79,7 +82,9 @@ void count_launch(mgg_ctx* ctx, uint64_t n = 1);
 
 // launchers (aggregate.cu / dense.cu)
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
-                      mgg_store* out, int relu_in, int phase, cudaStream_t st);
+                      mgg_store* out, int relu_in, int phase, const float* halo,
+                      cudaStream_t st);
+void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st);
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
                       float scale, int relu_in, cudaStream_t st);
 void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,

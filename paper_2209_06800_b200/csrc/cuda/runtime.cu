@@ -487,6 +487,11 @@ int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* d, mgg_dplan** out) {
       p->rmeta = reinterpret_cast<int2*>(upload_array(d->remote_meta, 2 * (d->n_remote + 1)));
       p->lcols = upload_array(d->local_cols, d->local_cols_len);
       p->rcols = upload_array(d->remote_cols, d->remote_cols_len);
+      if (d->halo_rows && d->halo_len && d->remote_halo_cols) {
+        p->halo_rows = upload_array(d->halo_rows, d->halo_len);
+        p->halo_len = d->halo_len;
+        p->rcols_halo = upload_array(d->remote_halo_cols, d->remote_cols_len);
+      }
       p->num_local_warps = (d->n_local + d->dist - 1) / d->dist;
       const uint64_t nr_w = (d->n_remote + d->dist - 1) / d->dist;
       p->num_warps = d->mapping == 0 ? std::max(p->num_local_warps, nr_w)
@@ -506,6 +511,8 @@ int mgg_dplan_destroy(mgg_dplan* p) {
   cudaFree(p->rmeta);
   cudaFree(p->lcols);
   cudaFree(p->rcols);
+  cudaFree(p->halo_rows);
+  cudaFree(p->rcols_halo);
   delete p;
   return MGG_OK;
 }
@@ -516,8 +523,26 @@ int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
     if (!plan || !in || !out) throw Status{MGG_E_INPUT, "aggregate: null argument"};
     if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "aggregate: in/out width differ"};
     cudaStream_t st = enter(ctx, plan->part);
-    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, st);
+    const float* halo = opts ? opts->halo : nullptr;
+    if (halo && !plan->rcols_halo) throw Status{MGG_E_INPUT, "aggregate: plan has no halo"};
+    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, halo,
+                     st);
   });
+}
+
+int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, float* halo) {
+  return guard([&] {
+    if (!plan || !in || !halo) throw Status{MGG_E_INPUT, "halo_pull: null argument"};
+    cudaStream_t st = enter(ctx, plan->part);
+    launch_halo_pull(plan, in, halo, st);
+    count_launch(ctx);
+  });
+}
+
+int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* n) {
+  if (!plan || !n) return MGG_E_INPUT;
+  *n = plan->halo_len;
+  return MGG_OK;
 }
 
 int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
@@ -598,10 +623,14 @@ int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
     cudaStream_t st = enter(ctx, plan->part);
     reps = std::max(reps, 1u);
     std::vector<float> ms(reps);
-    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, st);
+    const float* halo = opts ? opts->halo : nullptr;
+    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, halo,
+                     st);
     for (uint32_t r = 0; r < reps; ++r) {
       MGG_CUDA(cudaEventRecord(ctx->ev0[plan->part], st));
-      launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, st);
+      if (halo) launch_halo_pull(plan, in, const_cast<float*>(halo), st);
+      launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0,
+                       halo, st);
       MGG_CUDA(cudaEventRecord(ctx->ev1[plan->part], st));
       MGG_CUDA(cudaEventSynchronize(ctx->ev1[plan->part]));
       MGG_CUDA(cudaEventElapsedTime(&ms[r], ctx->ev0[plan->part], ctx->ev1[plan->part]));

@@ -446,6 +446,14 @@ int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob, size_t
 int mgg_engine_set_config(mgg_engine* e, uint32_t ps, uint32_t dist, uint32_t wpb) {
   return guard([&] { e->e->set_config(KernelConfig{ps, dist, wpb}); });
 }
+int mgg_engine_set_remote_fetch(mgg_engine* e, int mode) {
+  return guard([&] {
+    e->e->set_remote_fetch(mode == 1   ? Engine::RemoteFetch::fine
+                           : mode == 2 ? Engine::RemoteFetch::halo
+                                       : Engine::RemoteFetch::automatic);
+  });
+}
+
 int mgg_engine_set_mapping(mgg_engine* e, int mapping, int granularity) {
   return guard([&] {
     e->e->set_mapping(mapping == 0 ? MappingMode::interleaved : MappingMode::segregated,
@@ -488,8 +496,9 @@ int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps, int ph
 int mgg_engine_stats(const mgg_engine* e, uint64_t* s) {
   return guard([&] {
     const auto st = e->e->stats();
-    const uint64_t v[8] = {st.local_parts, st.remote_parts, st.local_edges, st.remote_edges,
-                           st.warps,       st.blocks,       st.launches,    st.plan_build_ns};
+    const uint64_t v[10] = {st.local_parts, st.remote_parts, st.local_edges, st.remote_edges,
+                            st.warps,       st.blocks,       st.launches,    st.plan_build_ns,
+                            st.halo_rows,   st.halo_parts};
     std::memcpy(s, v, sizeof(v));
   });
 }

@@ -179,18 +179,53 @@ void Engine::free_plans() {
     mgg_dplan_destroy(p);
     p = nullptr;
   }
+  for (auto& per : halo_bufs_)
+    for (auto& [dim, buf] : per) mgg_dbuf_destroy(buf);
+  halo_bufs_.assign(num_parts_, {});
+}
+
+const float* Engine::halo_for(std::uint32_t p, std::uint32_t dim) {
+  if (!halo_on_[p]) return nullptr;
+  for (auto& [w, buf] : halo_bufs_[p])
+    if (w == dim) return static_cast<const float*>(mgg_dbuf_ptr(buf));
+  std::uint64_t rows = 0;
+  ok(mgg_dplan_halo_len(plans_[p], &rows));
+  mgg_dbuf* buf = nullptr;
+  ok(mgg_dbuf_create(ctx_, p, nullptr, std::max<std::uint64_t>(rows, 1) * ((dim + 3) / 4 * 4) * 4,
+                     &buf));
+  halo_bufs_[p].push_back({dim, buf});
+  return static_cast<const float*>(mgg_dbuf_ptr(buf));
+}
+
+void Engine::set_remote_fetch(RemoteFetch mode) {
+  ok(mgg_ctx_synchronize(ctx_));
+  fetch_ = mode;
+  build_plans();
 }
 
 void Engine::build_plans() {
   free_plans();
   plans_.assign(num_parts_, nullptr);
+  halo_on_.assign(num_parts_, 0);
   stats_ = {};
   const auto t0 = std::chrono::steady_clock::now();
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
     if (dev_[p] < 0) continue;
     const FlatPlan fp =
         build_flat_plan(g_, split_, ne_, p, cfg_, spec_.in_dim, mapping_, granularity_);
+    HaloPlan halo;
+    if (fetch_ != RemoteFetch::fine && !fp.remote.cols.empty()) {
+      halo = build_halo_plan(fp);
+      halo_on_[p] = fetch_ == RemoteFetch::halo || halo.dedup_ratio() >= 2.0;
+    }
     mgg_plan_desc d{};
+    if (halo_on_[p]) {
+      d.halo_rows = halo.rows.data();
+      d.halo_len = halo.rows.size();
+      d.remote_halo_cols = halo.cols.data();
+      stats_.halo_rows += halo.rows.size();
+      stats_.halo_parts += 1;
+    }
     d.part = p;
     d.ps = cfg_.ps;
     d.dist = cfg_.dist;
@@ -277,7 +312,11 @@ void Engine::run(const Op& op) {
         ok(mgg_rows_init(ctx_, p, stores_[op.in], stores_[op.out], op.scale, op.relu));
         break;
       case OpKind::aggregate: {
-        mgg_agg_opts o{op.relu, 0};
+        std::uint32_t w = 0;
+        ok(mgg_store_info(stores_[op.in], &w, nullptr));
+        const float* halo = halo_for(p, w);
+        if (halo) ok(mgg_halo_pull(ctx_, plans_[p], stores_[op.in], const_cast<float*>(halo)));
+        mgg_agg_opts o{op.relu, 0, halo};
         ok(mgg_aggregate(ctx_, plans_[p], stores_[op.in], stores_[op.out], &o));
         break;
       }
@@ -385,8 +424,12 @@ void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
   for (std::uint32_t p = 0; p < num_parts_; ++p)
     ok(mgg_rows_init(ctx_, p, in, acc, self_scale, relu_in ? 1 : 0));
   ok(mgg_barrier(ctx_, flags_));
-  mgg_agg_opts o{relu_in ? 1 : 0, 0};
-  for (std::uint32_t p = 0; p < num_parts_; ++p) ok(mgg_aggregate(ctx_, plans_[p], in, acc, &o));
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    const float* halo = halo_for(p, dim);
+    if (halo) ok(mgg_halo_pull(ctx_, plans_[p], in, const_cast<float*>(halo)));
+    mgg_agg_opts o{relu_in ? 1 : 0, 0, halo};
+    ok(mgg_aggregate(ctx_, plans_[p], in, acc, &o));
+  }
   ok(mgg_store_download(acc, out, 0, g_.num_nodes, dim));
   synchronize();
 }
@@ -409,10 +452,11 @@ std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int 
     out = scratch(dim, 1);
   }
   std::uint64_t worst = 0;
-  mgg_agg_opts o{0, phase};
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
     if (dev_[p] < 0) continue;
     std::uint64_t ns = 0;
+    // halo mode: each timed rep includes the deduplicated pull
+    mgg_agg_opts o{0, phase, halo_for(p, dim)};
     ok(mgg_time_aggregate(ctx_, plans_[p], in, out, &o, reps, &ns));
     worst = std::max(worst, ns);
   }

@@ -413,3 +413,42 @@ FlatPlan build_flat_plan(const CsrGraph& g, const WorkloadSplit& split,
 }
 
 }  // namespace mgg
+
+namespace mgg {
+
+double HaloPlan::dedup_ratio() const {
+  return rows.empty() ? 0.0 : static_cast<double>(cols.size()) / static_cast<double>(rows.size());
+}
+
+HaloPlan build_halo_plan(const FlatPlan& plan) {
+  HaloPlan h;
+  const auto& rc = plan.remote.cols;
+  h.cols.resize(rc.size());
+  if (rc.empty()) return h;
+  // Packed ids order as (owner, offset): mark + compact per owner shard.
+  std::vector<std::uint64_t> base(plan.owner_ranges.size() + 1, 0);
+  for (std::size_t o = 0; o < plan.owner_ranges.size(); ++o)
+    base[o + 1] = base[o] + plan.owner_ranges[o].size();
+  const std::uint64_t total = base.back();
+  auto dense = [&](std::uint32_t c) { return base[c >> kOwnerShift] + (c & kOffsetMask); };
+  std::vector<std::uint32_t> slot(total, 0);  // 1 + halo row, 0 = unused
+  detail::parallel_for(rc.size(), 1 << 18, [&](std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t i = b; i < e; ++i)
+      std::atomic_ref<std::uint32_t>(slot[dense(rc[i])]).store(1, std::memory_order_relaxed);
+  });
+  std::uint32_t next = 0;
+  for (std::size_t o = 0; o + 1 < base.size(); ++o)
+    for (std::uint64_t d = base[o]; d < base[o + 1]; ++d)
+      if (slot[d]) {
+        slot[d] = ++next;
+        h.rows.push_back(static_cast<std::uint32_t>(o << kOwnerShift) |
+                         static_cast<std::uint32_t>(d - base[o]));
+      }
+  if (next > kOffsetMask + 1u) throw ConfigError("halo plan: more than 2^28 halo rows");
+  detail::parallel_for(rc.size(), 1 << 18, [&](std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t i = b; i < e; ++i) h.cols[i] = slot[dense(rc[i])] - 1;
+  });
+  return h;
+}
+
+}  // namespace mgg

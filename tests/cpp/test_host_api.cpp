@@ -127,6 +127,17 @@ static void workload_tests() {
     KernelLaunchPlan back = plan_from_json(plan_to_json(ref));
     CHECK(back.warps.size() == ref.warps.size());
   }
+  // halo plan: distinct remote rows, (owner, offset)-sorted, columns map back
+  for (uint32_t gpu = 0; gpu < 3; ++gpu) {
+    FlatPlan fp = build_flat_plan(g, sp, ne, gpu, {4, 3, 2}, 8);
+    HaloPlan h = build_halo_plan(fp);
+    CHECK(h.cols.size() == fp.remote.cols.size());
+    for (size_t i = 1; i < h.rows.size(); ++i) CHECK(h.rows[i - 1] < h.rows[i]);
+    bool back = true;
+    for (size_t i = 0; i < h.cols.size(); ++i) back &= h.rows[h.cols[i]] == fp.remote.cols[i];
+    CHECK(back);
+    CHECK(h.rows.empty() || h.dedup_ratio() >= 1.0);
+  }
   KernelLaunchPlan broken = plan;
   broken.warps[1].tasks[0].index = 0;
   CHECK_THROWS_AS(validate_plan(broken), IntegrityError);

@@ -230,3 +230,29 @@ def test_ablation_mappings_match_oracle(mgg, oracle_mod, mapping, granularity, p
         for phase in (0, 1, 2):
             assert eng.time_aggregate(dim, reps=2, phase=phase) > 0
         eng.close()
+
+
+@pytest.mark.parametrize("fetch", ["fine", "halo", "auto"])
+@pytest.mark.parametrize("parts", [2, 3, 4])
+def test_remote_fetch_modes(mgg, oracle_mod, fetch, parts):
+    """Per-edge peer reads (the paper's design) and the deduplicated halo pull
+    give the same aggregation and forward."""
+    g = mgg.gen_synthetic(mgg.POWERLAW, 4000, 20, 9)
+    for dim in (16, 64, 200):
+        x = mgg.random_features(g.num_nodes, dim, seed=dim + 3)
+        eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 24), ps=16, dist=4, wpb=4)
+        eng.set_remote_fetch(fetch)
+        st = eng.stats()
+        if fetch == "halo":
+            assert st["halo_parts"] == parts and st["halo_rows"] > 0
+        if fetch == "fine":
+            assert st["halo_parts"] == 0
+        assert_rows_close(eng.aggregate(x, 1.0, relu_in=True),
+                          oracle_mod.aggregate(g.row_ptr, g.col_idx, x, relu_in=True),
+                          what=f"{fetch} parts={parts} dim={dim}")
+        z = np.zeros((g.num_nodes, 24), np.float32)
+        eng.forward_host(x, z)
+        _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, eng.model)
+        assert np.abs(z - zr).max() <= TOL
+        assert eng.time_aggregate(dim, reps=2) > 0
+        eng.close()
