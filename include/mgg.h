@@ -149,7 +149,9 @@ typedef struct {
   int phase; /* 0 all, 1 local partitions only, 2 remote only (phase-split
                 measurement, R:proj/src/sim.cpp:127-142) */
   const float* halo; /* non-NULL: remote partitions read this part's halo
-                        buffer (filled by mgg_halo_pull) instead of peers */
+                        buffer instead of peers (local pass, then remote pass) */
+  int halo_pull;     /* with halo: refill it first (mgg_halo_pull) on the
+                        part's aux stream, overlapped with the local pass */
 } mgg_agg_opts;
 int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
                   mgg_store* out, const mgg_agg_opts* opts);

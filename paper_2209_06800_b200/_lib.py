@@ -46,7 +46,7 @@ class PlanDesc(C.Structure):
 
 
 class AggOpts(C.Structure):
-    _fields_ = [("relu_in", C.c_int), ("phase", C.c_int), ("halo", vp)]
+    _fields_ = [("relu_in", C.c_int), ("phase", C.c_int), ("halo", vp), ("halo_pull", C.c_int)]
 
 
 class DenseDesc(C.Structure):

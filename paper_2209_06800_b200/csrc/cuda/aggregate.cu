@@ -476,11 +476,28 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   a.local_warps = static_cast<uint32_t>(p->num_local_warps);
   a.num_owners = ctx->num_parts;
   a.phase = phase;
-  if (p->num_warps == 0) return;
-  if (p->num_warps > 0xffffffffull) throw Status{MGG_E_CONFIG, "aggregate: too many warps"};
-  a.num_warps = static_cast<uint32_t>(p->num_warps);
+  uint64_t warps = p->num_warps;
+  if (halo) {
+    // Halo mode runs one kind per launch with the local-read kernel: pass 1
+    // = the local partitions, pass 2 = the remote partitions gathered from
+    // the local halo (remote columns already re-pointed at halo rows).
+    if (phase == 2) {
+      a.lmeta = p->rmeta;
+      a.lcols = p->rcols_halo;
+      a.own = halo;
+      a.nL = a.nR;
+    }
+    a.nR = 0;
+    a.phase = 0;
+    a.mapping = 0;
+    a.halo = nullptr;
+    warps = (a.nL + a.dist - 1) / a.dist;
+  }
+  if (warps == 0) return;
+  if (warps > 0xffffffffull) throw Status{MGG_E_CONFIG, "aggregate: too many warps"};
+  a.num_warps = static_cast<uint32_t>(warps);
   a.num_lblocks = (a.num_warps + a.wpb - 1) / a.wpb;
-  const bool remote = a.nR > 0 && phase != 1;
+  const bool remote = a.nR > 0 && a.phase != 1;
   KernelFn k = relu_in ? (remote ? pick<true, true>(a.vec) : pick<true, false>(a.vec))
                        : (remote ? pick<false, true>(a.vec) : pick<false, false>(a.vec));
   const int threads = 32 * static_cast<int>(p->wpb);

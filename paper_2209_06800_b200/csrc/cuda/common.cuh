@@ -31,6 +31,8 @@ struct mgg_ctx {
   std::vector<int32_t> device;         // -1: remote process
   std::vector<cudaStream_t> stream;    // per part (null for remote)
   std::vector<cudaEvent_t> ev0, ev1;   // timing events per part
+  std::vector<cudaStream_t> aux;       // per part: halo pulls overlap local K1
+  std::vector<cudaEvent_t> fork, join; // per part: main->aux, aux->main
   std::vector<std::vector<cudaEvent_t>> evpool;  // mgg_event_record slots
   uint64_t launches = 0;
   uint32_t epoch = 0;                  // barrier generation
@@ -85,6 +87,8 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                       mgg_store* out, int relu_in, int phase, const float* halo,
                       cudaStream_t st);
 void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st);
+void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg_store* out,
+                   const mgg_agg_opts* o, cudaStream_t st);
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
                       float scale, int relu_in, cudaStream_t st);
 void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,

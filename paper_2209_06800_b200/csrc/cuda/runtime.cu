@@ -105,6 +105,35 @@ void launch_barrier(unsigned* const* shards, unsigned* own, uint32_t me, uint32_
   MGG_CUDA(cudaGetLastError());
 }
 
+// K1 entry: fine-grained (one launch, remote rows read from peers in the
+// pair loop), or halo mode — the deduplicated pull runs on the part's aux
+// stream while the local partitions are reduced on the main stream, then the
+// remote partitions are reduced from the local halo.
+void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg_store* out,
+                   const mgg_agg_opts* o, cudaStream_t st) {
+  const int relu = o ? o->relu_in : 0, phase = o ? o->phase : 0;
+  const float* halo = o ? o->halo : nullptr;
+  if (!halo) {
+    launch_aggregate(ctx, plan, in, out, relu, phase, nullptr, st);
+    return;
+  }
+  if (!plan->rcols_halo) throw Status{MGG_E_INPUT, "aggregate: plan has no halo"};
+  const uint32_t p = plan->part;
+  const bool pull = o->halo_pull && phase != 1;
+  if (pull) {
+    MGG_CUDA(cudaEventRecord(ctx->fork[p], st));
+    MGG_CUDA(cudaStreamWaitEvent(ctx->aux[p], ctx->fork[p], 0));
+    launch_halo_pull(plan, in, const_cast<float*>(halo), ctx->aux[p]);
+    MGG_CUDA(cudaEventRecord(ctx->join[p], ctx->aux[p]));
+    count_launch(ctx);
+  }
+  if (phase != 2) launch_aggregate(ctx, plan, in, out, relu, 1, halo, st);
+  if (phase != 1) {
+    if (pull) MGG_CUDA(cudaStreamWaitEvent(st, ctx->join[p], 0));
+    launch_aggregate(ctx, plan, in, out, relu, 2, halo, st);
+  }
+}
+
 }  // namespace mgg::dev
 
 using namespace mgg::dev;
@@ -136,6 +165,9 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
       c->stream.assign(num_parts, nullptr);
       c->ev0.assign(num_parts, nullptr);
       c->ev1.assign(num_parts, nullptr);
+      c->aux.assign(num_parts, nullptr);
+      c->fork.assign(num_parts, nullptr);
+      c->join.assign(num_parts, nullptr);
       c->evpool.assign(num_parts, {});
       int first = -1;
       for (uint32_t p = 0; p < num_parts; ++p) {
@@ -155,6 +187,11 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
         if (!c->stream[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->stream[p], cudaStreamNonBlocking));
         MGG_CUDA(cudaEventCreate(&c->ev0[p]));
         MGG_CUDA(cudaEventCreate(&c->ev1[p]));
+        for (uint32_t q = 0; q < p; ++q)
+          if (c->device[q] == d) c->aux[p] = c->aux[q];
+        if (!c->aux[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->aux[p], cudaStreamNonBlocking));
+        MGG_CUDA(cudaEventCreateWithFlags(&c->fork[p], cudaEventDisableTiming));
+        MGG_CUDA(cudaEventCreateWithFlags(&c->join[p], cudaEventDisableTiming));
       }
       // peer access between every pair of local devices (single-process
       // multi-GPU); imported IPC shards enable it lazily
@@ -190,6 +227,11 @@ int mgg_ctx_destroy(mgg_ctx* c) {
     if (c->stream[p] && !shared) cudaStreamDestroy(c->stream[p]);
     if (c->ev0[p]) cudaEventDestroy(c->ev0[p]);
     if (c->ev1[p]) cudaEventDestroy(c->ev1[p]);
+    bool shared_aux = false;
+    for (uint32_t q = 0; q < p; ++q) shared_aux |= c->aux[q] == c->aux[p];
+    if (c->aux[p] && !shared_aux) cudaStreamDestroy(c->aux[p]);
+    if (c->fork[p]) cudaEventDestroy(c->fork[p]);
+    if (c->join[p]) cudaEventDestroy(c->join[p]);
     for (cudaEvent_t e : c->evpool[p])
       if (e) cudaEventDestroy(e);
   }
@@ -523,10 +565,7 @@ int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
     if (!plan || !in || !out) throw Status{MGG_E_INPUT, "aggregate: null argument"};
     if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "aggregate: in/out width differ"};
     cudaStream_t st = enter(ctx, plan->part);
-    const float* halo = opts ? opts->halo : nullptr;
-    if (halo && !plan->rcols_halo) throw Status{MGG_E_INPUT, "aggregate: plan has no halo"};
-    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, halo,
-                     st);
+    run_aggregate(ctx, plan, in, out, opts, st);
   });
 }
 
@@ -623,14 +662,10 @@ int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
     cudaStream_t st = enter(ctx, plan->part);
     reps = std::max(reps, 1u);
     std::vector<float> ms(reps);
-    const float* halo = opts ? opts->halo : nullptr;
-    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0, halo,
-                     st);
+    run_aggregate(ctx, plan, in, out, opts, st);
     for (uint32_t r = 0; r < reps; ++r) {
       MGG_CUDA(cudaEventRecord(ctx->ev0[plan->part], st));
-      if (halo) launch_halo_pull(plan, in, const_cast<float*>(halo), st);
-      launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0,
-                       halo, st);
+      run_aggregate(ctx, plan, in, out, opts, st);
       MGG_CUDA(cudaEventRecord(ctx->ev1[plan->part], st));
       MGG_CUDA(cudaEventSynchronize(ctx->ev1[plan->part]));
       MGG_CUDA(cudaEventElapsedTime(&ms[r], ctx->ev0[plan->part], ctx->ev1[plan->part]));

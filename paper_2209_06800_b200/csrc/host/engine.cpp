@@ -314,9 +314,7 @@ void Engine::run(const Op& op) {
       case OpKind::aggregate: {
         std::uint32_t w = 0;
         ok(mgg_store_info(stores_[op.in], &w, nullptr));
-        const float* halo = halo_for(p, w);
-        if (halo) ok(mgg_halo_pull(ctx_, plans_[p], stores_[op.in], const_cast<float*>(halo)));
-        mgg_agg_opts o{op.relu, 0, halo};
+        mgg_agg_opts o{op.relu, 0, halo_for(p, w), 1};
         ok(mgg_aggregate(ctx_, plans_[p], stores_[op.in], stores_[op.out], &o));
         break;
       }
@@ -425,9 +423,7 @@ void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
     ok(mgg_rows_init(ctx_, p, in, acc, self_scale, relu_in ? 1 : 0));
   ok(mgg_barrier(ctx_, flags_));
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
-    const float* halo = halo_for(p, dim);
-    if (halo) ok(mgg_halo_pull(ctx_, plans_[p], in, const_cast<float*>(halo)));
-    mgg_agg_opts o{relu_in ? 1 : 0, 0, halo};
+    mgg_agg_opts o{relu_in ? 1 : 0, 0, halo_for(p, dim), 1};
     ok(mgg_aggregate(ctx_, plans_[p], in, acc, &o));
   }
   ok(mgg_store_download(acc, out, 0, g_.num_nodes, dim));
@@ -456,7 +452,7 @@ std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int 
     if (dev_[p] < 0) continue;
     std::uint64_t ns = 0;
     // halo mode: each timed rep includes the deduplicated pull
-    mgg_agg_opts o{0, phase, halo_for(p, dim)};
+    mgg_agg_opts o{0, phase, halo_for(p, dim), 1};
     ok(mgg_time_aggregate(ctx_, plans_[p], in, out, &o, reps, &ns));
     worst = std::max(worst, ns);
   }
