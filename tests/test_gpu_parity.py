@@ -256,3 +256,38 @@ def test_remote_fetch_modes(mgg, oracle_mod, fetch, parts):
         assert np.abs(z - zr).max() <= TOL
         assert eng.time_aggregate(dim, reps=2) > 0
         eng.close()
+
+
+@pytest.mark.parametrize("workload", ["reddit", "products"])
+def test_full_size_properties(mgg, workload):
+    """BASELINE-size graphs, where the fp64 oracle is too slow to replay every
+    row: size-independent identities.
+      * column sums: sum_v out[v] = sum_u (self + indeg(u)) * x[u]  (exact in
+        real arithmetic; fp64 bincount on the host),
+      * partition independence: 1, 4 and 8 parts (fine and halo) agree,
+      * linearity: agg(2x - y) = 2 agg(x) - agg(y)."""
+    if workload == "reddit":
+        g, dim = mgg.gen_synthetic(mgg.POWERLAW, 232_965, 492, 0), 16
+    else:
+        g, dim = mgg.gen_synthetic(mgg.POWERLAW, 2_449_029, 25.259, 0), 64
+    n = g.num_nodes
+    x = mgg.random_features(n, dim, seed=11)
+    y = mgg.random_features(n, dim, seed=12)
+    indeg = np.bincount(g.col_idx.astype(np.int64), minlength=n).astype(np.float64)
+    want = ((1.0 + indeg)[:, None] * x.astype(np.float64)).sum(axis=0)
+    model = mgg.make_gcn(dim, 8, 4)
+    outs = {}
+    for parts, fetch in [(1, "fine"), (4, "fine"), (8, "halo")]:
+        eng = mgg.Engine(g, parts, [0] * parts, model, ps=32, dist=16, wpb=2)
+        eng.set_remote_fetch(fetch)
+        outs[(parts, fetch)] = eng.aggregate(x)
+        if parts == 1:
+            lin = eng.aggregate(2 * x - y)
+            ay = eng.aggregate(y)
+        eng.close()
+    ref = outs[(1, "fine")]
+    got = ref.astype(np.float64).sum(axis=0)
+    assert np.abs(got - want).max() <= 1e-4 * np.abs((1.0 + indeg)[:, None] * x).sum(axis=0).max()
+    for k, o in outs.items():
+        assert_rows_close(o, ref.astype(np.float64), tol=1e-4, what=f"parts/fetch {k}")
+    assert_rows_close(lin, 2 * ref.astype(np.float64) - ay, tol=1e-4, what="linearity")
