@@ -379,8 +379,83 @@ int reg_cap_mode() {
   return m;
 }
 
+// Lean local-only K1 (single-part launches, halo passes): the same
+// partition / warp / CTA geometry without the pairing machinery, so the
+// register footprint — hence resident warps, hence row loads in flight —
+// is set by the gather alone.
+template <int VEC, bool RELU, int MINB>
+__global__ void __launch_bounds__(512, MINB) agg_local(AggArgs a) {
+  using L = Lanes<VEC, RELU>;
+  const L ln(a.vec);
+  const int lane = ln.lane;
+  float4 acc = f4zero();
+  int cur = -1;
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    const uint32_t l0 = w * a.dist;
+    const int nl = static_cast<int>(min(l0 + a.dist, a.nL) - l0);
+    const int2 ml = lane <= nl ? __ldg(a.lmeta + l0 + lane) : make_int2(0, 0);
+    int beg = __shfl_sync(kFull, ml.y, 0);
+    int end = __shfl_sync(kFull, ml.y, 1);
+    uint32_t win = load_colwin(a.lcols, beg, min(end - beg, 32));
+    for (int i = 0; i < nl; ++i) {
+      const int t = __shfl_sync(kFull, ml.x, i);
+      const int nend = __shfl_sync(kFull, ml.y, i + 2);
+      const uint32_t next = i + 1 < nl ? load_colwin(a.lcols, end, min(nend - end, 32)) : 0u;
+      if (t != cur) {
+        if (cur >= 0) ln.flush(a, acc, cur);
+        acc = f4zero();
+        cur = t;
+      }
+      acc = ln.template window<false>(a, win, min(end - beg, 32), 0, acc, nullptr);
+      for (int b = beg + 32; b < end; b += 32) {  // whole-list tails
+        const int n = min(end - b, 32);
+        acc = ln.template window<false>(a, load_colwin(a.lcols, b, n), n, 0, acc, nullptr);
+      }
+      win = next;
+      beg = end;
+      end = nend;
+    }
+  }
+  if (cur >= 0) ln.flush(a, acc, cur);
+}
+
+template <bool RELU, int MINB>
+KernelFn pick_local(uint32_t v) {
+  if (v <= 1) return agg_local<1, RELU, MINB>;
+  if (v <= 2) return agg_local<2, RELU, MINB>;
+  if (v <= 4) return agg_local<4, RELU, MINB>;
+  if (v <= 8) return agg_local<8, RELU, MINB>;
+  if (v <= 16) return agg_local<16, RELU, MINB>;
+  if (v <= 32) return agg_local<32, RELU, MINB>;
+  return agg_wide<RELU>;
+}
+
+int lean_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_LEAN");
+    return e ? std::atoi(e) : 2;
+  }();
+  return m;
+}
+
 template <bool RELU, bool REMOTE>
 KernelFn pick(uint32_t v) {
+  if (!REMOTE && lean_mode() > 0) {
+    switch (lean_mode()) {
+      case 3: return pick_local<RELU, 3>(v);
+      case 4: return pick_local<RELU, 4>(v);
+      case 5: return pick_local<RELU, 2>(v);
+      // measured (profiles/r01_k1_experiments.md): narrow rows (<= 16 floats,
+      // L2-resident tables) want 64 regs/36 warps; wider rows want 40 regs/48
+      // warps despite a few spilled bytes
+      default: return v <= 4 ? pick_local<RELU, 2>(v) : pick_local<RELU, 3>(v);
+    }
+  }
   // measured on B200 (profiles/): local-only is best at a 64-register cap
   // (no spills, 36 warps/SM); the remote variant's staging buffer wants the
   // uncapped allocation
