@@ -167,6 +167,11 @@ int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* halo_len);
  * f: 0 identity, 1 ReLU. */
 int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
                   mgg_store* out, float scale, int relu_in);
+/* mgg_rows_init that also writes copy[r] = f(in[r]) (same width; null = no
+ * copy): the activated layer input, which the next mgg_aggregate then
+ * gathers with relu_in = 0 instead of applying f once per edge. */
+int mgg_rows_init_copy(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
+                       mgg_store* out, float scale, int relu_in, mgg_store* copy);
 
 /* Row softmax over the `dim` columns of the part's rows (in place allowed). */
 int mgg_rows_softmax(mgg_ctx* ctx, uint32_t part, const mgg_store* in,

@@ -113,6 +113,7 @@ class Engine {
   int add_store(std::uint32_t dim);
   int add_weight(const float* src, std::size_t n);
   void build_program();
+  int activated(int h, std::uint32_t width, int relu, int a, float scale);
   void build_plans();
   void free_plans();
   void run(const Op& op);

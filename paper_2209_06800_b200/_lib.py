@@ -96,6 +96,7 @@ _sig("mgg_dplan_upload", I, vp, C.POINTER(PlanDesc), PP)
 _sig("mgg_dplan_destroy", I, vp)
 _sig("mgg_aggregate", I, vp, vp, vp, vp, C.POINTER(AggOpts))
 _sig("mgg_rows_init", I, vp, U32, vp, vp, C.c_float, I)
+_sig("mgg_rows_init_copy", I, vp, U32, vp, vp, C.c_float, I, vp)
 _sig("mgg_rows_softmax", I, vp, U32, vp, vp)
 _sig("mgg_dense", I, vp, U32, vp, C.POINTER(DenseDesc), vp, vp)
 _sig("mgg_barrier", I, vp, vp)

@@ -67,8 +67,18 @@ constexpr uint32_t kShift = 28;
 constexpr uint32_t kMask = (1u << kShift) - 1;
 constexpr unsigned kFull = 0xffffffffu;
 
+// Two packed FADD2 (add.rn.f32x2, sm_100+): per-element IEEE round-to-
+// nearest adds, bit-identical to four FADDs at half the issue slots.
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
-  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+  float4 r;
+  asm("{\n\t.reg .b64 a0, a1, b0, b1, d0, d1;\n\t"
+      "mov.b64 a0, {%4, %5};\n\tmov.b64 a1, {%6, %7};\n\t"
+      "mov.b64 b0, {%8, %9};\n\tmov.b64 b1, {%10, %11};\n\t"
+      "add.rn.f32x2 d0, a0, b0;\n\tadd.rn.f32x2 d1, a1, b1;\n\t"
+      "mov.b64 {%0, %1}, d0;\n\tmov.b64 {%2, %3}, d1;\n\t}"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w));
+  return r;
 }
 __device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ float4 f4relu(float4 a) {
@@ -125,12 +135,32 @@ struct Lanes {
   static constexpr int PF = 4;          // remote steps staged ahead
   int lane, sub, v;
   bool vlane;
+  uint32_t voff;       // byte offset of this lane's float4 in a row
+  uint32_t pb;         // row pitch in bytes
+  const char* lbase;   // own shard + voff
 
-  __device__ __forceinline__ explicit Lanes(uint32_t vec) {
+  // Lanes past the row width (v >= vec) re-read the row's first float4
+  // instead of predicating: their sums never leave the warp (flush skips
+  // them), and every load stays unpredicated.
+  __device__ __forceinline__ Lanes(const AggArgs& a) {
     lane = threadIdx.x & 31;
     sub = lane / VEC;
     v = lane % VEC;
-    vlane = v < static_cast<int>(vec);
+    vlane = v < static_cast<int>(a.vec);
+    voff = vlane ? 16u * v : 0u;
+    pb = a.pitch * 4u;
+    lbase = reinterpret_cast<const char*>(a.own) + voff;
+    // opaque to the optimizer: otherwise it re-associates own + voff + c*pb
+    // into a per-row 64-bit add
+    asm("mov.b64 %0, %0;" : "+l"(lbase));
+  }
+
+  // `off` is a row offset: device-side local columns carry no owner bits
+  // (stripped at plan upload), remote columns are masked by the caller.
+  __device__ __forceinline__ float4 load(const char* base, uint32_t off) const {
+    float4 x = __ldg(reinterpret_cast<const float4*>(base + static_cast<size_t>(off) * pb));
+    if (RELU) x = f4relu(x);
+    return x;
   }
 
   // Row `r` (< n) of the current column window; base from the lane table for
@@ -139,13 +169,13 @@ struct Lanes {
   __device__ __forceinline__ float4 row(const AggArgs& a, uint32_t colwin, int r, int n,
                                         const float* tab_lane) const {
     const uint32_t c = __shfl_sync(kFull, colwin, r & 31);
-    const float* base = a.own;
-    if (REMOTE) base = a.halo ? a.halo : shfl_ptr(tab_lane, static_cast<int>(c >> kShift));
+    const char* base = lbase;
+    if (REMOTE)
+      base = reinterpret_cast<const char*>(
+                 a.halo ? a.halo : shfl_ptr(tab_lane, static_cast<int>(c >> kShift))) +
+             voff;
     float4 x = f4zero();
-    if (vlane && r < n) {
-      x = ld_row4(base + static_cast<size_t>(c & kMask) * a.pitch + 4 * v);
-      if (RELU) x = f4relu(x);
-    }
+    if (r < n) x = load(base, REMOTE ? (c & kMask) : c);
     return x;
   }
 
@@ -155,6 +185,19 @@ struct Lanes {
   template <bool REMOTE>
   __device__ __forceinline__ float4 window(const AggArgs& a, uint32_t colwin, int n, int s0,
                                            float4 acc, const float* tab_lane) const {
+    if (!REMOTE && s0 == 0 && n % (RPW * UNR) == 0) {
+      // whole step groups (every full ps=32 window): no predicates at all —
+      // per row a shuffle, a mask, one IMAD.WIDE, the load and two FADD2
+      for (int s = 0; s < n / RPW; s += UNR) {
+        float4 t[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          t[u] = load(lbase, __shfl_sync(kFull, colwin, (s + u) * RPW + sub));
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+      }
+      return acc;
+    }
     const int steps = (n + RPW - 1) / RPW;
     for (int s = s0; s < steps; s += UNR) {
       float4 t[UNR];
@@ -207,7 +250,7 @@ __device__ __forceinline__ WarpMeta load_warp_meta(const AggArgs& a, uint32_t w,
 template <int VEC, bool RELU, bool REMOTE, int MINB>
 __global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
   using L = Lanes<VEC, RELU>;
-  const L ln(a.vec);
+  const L ln(a);
   const int lane = ln.lane;
   const float* tab_lane = nullptr;
   if (REMOTE && lane < static_cast<int>(a.num_owners)) tab_lane = a.table[lane];
@@ -386,7 +429,7 @@ int reg_cap_mode() {
 template <int VEC, bool RELU, int MINB>
 __global__ void __launch_bounds__(512, MINB) agg_local(AggArgs a) {
   using L = Lanes<VEC, RELU>;
-  const L ln(a.vec);
+  const L ln(a);
   const int lane = ln.lane;
   float4 acc = f4zero();
   int cur = -1;
@@ -485,16 +528,27 @@ unsigned resident_grid(KernelFn k, int threads) {
   return g;
 }
 
-// out[r] = scale * f(in[r]) over rows*pitch floats
+// out[r] = scale * f(in[r]) over rows*pitch floats; copy[r] = f(in[r]) when
+// given (the activated layer input, so the following K1 gathers it without
+// a per-edge ReLU)
 template <bool RELU>
 __global__ void rows_init_kernel(const float4* __restrict__ in, float4* __restrict__ out,
-                                 size_t n4, float scale) {
+                                 float4* __restrict__ copy, size_t n4, float scale) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
        i += (size_t)gridDim.x * blockDim.x) {
     float4 x = __ldg(in + i);
     if (RELU) x = f4relu(x);
     out[i] = make_float4(x.x * scale, x.y * scale, x.z * scale, x.w * scale);
+    if (copy) copy[i] = x;
   }
+}
+
+// Local column ids lose their owner bits on the device (owner == this part),
+// so K1's local gathers index the own shard with no mask.
+__global__ void strip_owner_kernel(uint32_t* __restrict__ cols, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    cols[i] &= kMask;
 }
 
 // Deduplicated remote fetch: halo[r] = table[owner(r)][offset(r)] for the
@@ -526,6 +580,13 @@ void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cuda
   const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148 * 8));
   halo_pull_kernel<<<blocks, 256, 0, st>>>(p->halo_rows, p->halo_len, in->dtable[p->part],
                                            in->pitch, reinterpret_cast<float4*>(halo));
+  MGG_CUDA(cudaGetLastError());
+}
+
+void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st) {
+  if (!n) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 8));
+  strip_owner_kernel<<<blocks, 256, 0, st>>>(cols, n);
   MGG_CUDA(cudaGetLastError());
 }
 
@@ -583,17 +644,19 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
 }
 
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
-                      float scale, int relu_in, cudaStream_t st) {
+                      float scale, int relu_in, float* copy, cudaStream_t st) {
   const size_t n4 = rows * (size_t)pitch / 4;
   if (n4 == 0) return;
   const unsigned blocks =
       static_cast<unsigned>(std::min<size_t>((n4 + 255) / 256, 148 * 16));
+  auto* o = reinterpret_cast<float4*>(out);
+  auto* c = reinterpret_cast<float4*>(copy);
   if (relu_in)
-    rows_init_kernel<true><<<blocks, 256, 0, st>>>(
-        reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), n4, scale);
+    rows_init_kernel<true><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), o, c,
+                                                   n4, scale);
   else
-    rows_init_kernel<false><<<blocks, 256, 0, st>>>(
-        reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), n4, scale);
+    rows_init_kernel<false><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), o, c,
+                                                    n4, scale);
   MGG_CUDA(cudaGetLastError());
 }
 

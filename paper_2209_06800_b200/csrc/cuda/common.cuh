@@ -86,11 +86,12 @@ void count_launch(mgg_ctx* ctx, uint64_t n = 1);
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                       mgg_store* out, int relu_in, int phase, const float* halo,
                       cudaStream_t st);
+void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st);
 void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st);
 void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg_store* out,
                    const mgg_agg_opts* o, cudaStream_t st);
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
-                      float scale, int relu_in, cudaStream_t st);
+                      float scale, int relu_in, float* copy, cudaStream_t st);
 void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                   const float* w, const float* bias, const float* pre_bias,
                   uint32_t m, uint32_t pre, uint32_t act, float* out,

@@ -528,6 +528,7 @@ int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* d, mgg_dplan** out) {
       p->lmeta = reinterpret_cast<int2*>(upload_array(d->local_meta, 2 * (d->n_local + 1)));
       p->rmeta = reinterpret_cast<int2*>(upload_array(d->remote_meta, 2 * (d->n_remote + 1)));
       p->lcols = upload_array(d->local_cols, d->local_cols_len);
+      launch_strip_owner(p->lcols, d->local_cols_len, ctx->stream[d->part]);
       p->rcols = upload_array(d->remote_cols, d->remote_cols_len);
       if (d->halo_rows && d->halo_len && d->remote_halo_cols) {
         p->halo_rows = upload_array(d->halo_rows, d->halo_len);
@@ -586,11 +587,18 @@ int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* n) {
 
 int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
                   float scale, int relu_in) {
+  return mgg_rows_init_copy(ctx, part, in, out, scale, relu_in, nullptr);
+}
+
+int mgg_rows_init_copy(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
+                       float scale, int relu_in, mgg_store* copy) {
   return guard([&] {
-    if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "rows_init: in/out width differ"};
+    if (!in || !out) throw Status{MGG_E_INPUT, "rows_init: null store"};
+    if (in->pitch != out->pitch || (copy && copy->pitch != in->pitch))
+      throw Status{MGG_E_INPUT, "rows_init: in/out width differ"};
     cudaStream_t st = enter(ctx, part);
     launch_rows_init(in->shard[part], out->shard[part], in->rows(part), in->pitch, scale,
-                     relu_in, st);
+                     relu_in, copy ? copy->shard[part] : nullptr, st);
     count_launch(ctx);
   });
 }

@@ -87,6 +87,15 @@ int Engine::add_weight(const float* src, std::size_t n) {
   return static_cast<int>(weights_.size()) - 1;
 }
 
+// Self term A = scale * f(H). With a pending ReLU f, the init also writes
+// G = ReLU(H) once per row and the aggregation gathers G (no per-edge ReLU,
+// H itself stays readable through get_hidden); returns the store to gather.
+int Engine::activated(int h, std::uint32_t width, int relu, int a, float scale) {
+  const int g = relu ? add_store(width) : h;
+  program_.push_back({OpKind::init, h, a, relu ? g : -1, -1, -1, -1, 0, 0, scale, relu});
+  return g;
+}
+
 void Engine::build_program() {
   const auto& s = spec_;
   input_ = add_store(s.in_dim);
@@ -121,9 +130,9 @@ void Engine::build_program() {
         cur = A;
       } else {  // aggregate first: A = f(H) + Σ f(H_u), then A·W
         const int A = add_store(a), Y = add_store(b);
-        program_.push_back({OpKind::init, cur, A, -1, -1, -1, -1, 0, 0, 1.f, fin});
+        const int G = activated(cur, a, fin, A, 1.f);
         program_.push_back({OpKind::barrier});
-        program_.push_back({OpKind::aggregate, cur, A, -1, -1, -1, -1, 0, 0, 1.f, fin});
+        program_.push_back({OpKind::aggregate, G, A});
         hidden_.push_back(A);
         program_.push_back({OpKind::dense, A, Y, -1, W, -1, -1, 0, last ? 2u : 0u, 1.f, 0});
         if (last) output_ = Y;
@@ -158,9 +167,9 @@ void Engine::build_program() {
         program_.push_back({OpKind::dense, A, O, -1, W2, B2, B1, 2, last ? 2u : 0u, 1.f, 0});
       } else {  // A = (1+eps) f(H) + Σ f(H_u); M = ReLU(A·W1+b1); O = M·W2+b2
         const int A = add_store(a), M = add_store(h);
-        program_.push_back({OpKind::init, cur, A, -1, -1, -1, -1, 0, 0, self, fin});
+        const int G = activated(cur, a, fin, A, self);
         program_.push_back({OpKind::barrier});
-        program_.push_back({OpKind::aggregate, cur, A, -1, -1, -1, -1, 0, 0, 1.f, fin});
+        program_.push_back({OpKind::aggregate, G, A});
         hidden_.push_back(A);
         program_.push_back({OpKind::dense, A, M, -1, W1, B1, -1, 0, 1, 1.f, 0});
         program_.push_back({OpKind::dense, M, O, -1, W2, B2, -1, 0, last ? 2u : 0u, 1.f, 0});
@@ -309,7 +318,8 @@ void Engine::run(const Op& op) {
         break;
       }
       case OpKind::init:
-        ok(mgg_rows_init(ctx_, p, stores_[op.in], stores_[op.out], op.scale, op.relu));
+        ok(mgg_rows_init_copy(ctx_, p, stores_[op.in], stores_[op.out], op.scale, op.relu,
+                              op.out2 >= 0 ? stores_[op.out2] : nullptr));
         break;
       case OpKind::aggregate: {
         std::uint32_t w = 0;
