@@ -337,6 +337,24 @@ def main():
     total_op_ms = max(sum(t for _, _, t in ops), 1e-9)
     share = sum(t for k, _, t in ops if k == "aggregate") / total_op_ms
 
+    # remote-access hiding (mirrors the phase-separated
+    # decomposition R:proj/src/sim.cpp:127-142, 530-569): K1 of the first
+    # aggregation width with only remote partitions (comm), only local ones
+    # (compute) and both pipelined in one launch; max over parts
+    overlap = None
+    if st["remote_parts"] > 0:
+        t_pipe = eng.time_aggregate(w0, 5, 0)
+        t_loc = eng.time_aggregate(w0, 5, 1)
+        t_rem = eng.time_aggregate(w0, 5, 2)
+        if world > 1:
+            t_pipe, t_loc, t_rem = (mdist.max_over_ranks(float(t)) for t in
+                                    (t_pipe, t_loc, t_rem))
+        overlap = {"k1_pipelined_ns": int(t_pipe), "k1_local_only_ns": int(t_loc),
+                   "k1_remote_only_ns": int(t_rem),
+                   "hidden_remote_fraction": round(
+                       max(0.0, (t_rem + t_loc - t_pipe)) / max(t_rem, 1), 4),
+                   "remote_fetch": "halo" if st.get("halo_rows", 0) else "fine"}
+
     e2e = None
     if not args.no_e2e:
         eng.forward_host(x, z)
@@ -399,6 +417,7 @@ def main():
                                  "gather rate (l2_gather); traffic = ncu DRAM bytes/launch"},
             "ops": [{"kind": k, "width": w, "ms": round(t / nfw, 4)} for k, w, t in ops],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "overlap": overlap,
             "clocks": clk.summary(),
             "setup": {"graph_gen_s": round(gen_s, 2), "engine_setup_s": round(setup_s, 2),
                       "plan_build_ms": round(st["plan_build_ns"] / 1e6, 1),
