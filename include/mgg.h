@@ -93,6 +93,23 @@ int mgg_store_upload(mgg_store* s, const float* host, uint64_t row_begin,
                      uint64_t row_count, uint32_t ld);
 int mgg_store_download(const mgg_store* s, float* host, uint64_t row_begin,
                        uint64_t row_count, uint32_t ld);
+/* Copy lanes. Every local part has a compute stream (lane 0, where all
+ * kernels run) and two copy streams shared by the parts of a device, so host
+ * transfers of one forward overlap the kernels of another:
+ * MGG_LANE_H2D (1) and MGG_LANE_D2H (2). The _on variants enqueue the copy
+ * (and its re-pitch kernel, when host rows are dense) on `lane`. */
+enum { MGG_LANE_COMPUTE = 0, MGG_LANE_H2D = 1, MGG_LANE_D2H = 2 };
+int mgg_store_upload_on(mgg_store* s, const float* host, uint64_t row_begin,
+                        uint64_t row_count, uint32_t ld, int lane);
+int mgg_store_download_on(const mgg_store* s, float* host, uint64_t row_begin,
+                          uint64_t row_count, uint32_t ld, int lane);
+/* Orders lane `to` after everything enqueued on lane `from` so far (device
+ * side; the host does not block). */
+int mgg_lane_fence(mgg_ctx* ctx, uint32_t part, int from, int to);
+/* Host-waitable marks: record `slot` at the current tail of `lane`; wait
+ * (blocking the calling thread) until the device reaches it. */
+int mgg_lane_mark(mgg_ctx* ctx, uint32_t part, int lane, uint32_t slot);
+int mgg_lane_wait_host(mgg_ctx* ctx, uint32_t part, uint32_t slot);
 /* Device pointer of a shard as seen by this process (local or imported). */
 int mgg_store_shard(const mgg_store* s, uint32_t part, void** dptr);
 
@@ -370,6 +387,15 @@ int mgg_engine_forward(mgg_engine* e);
 int mgg_engine_get_output(mgg_engine* e, float* z);
 /* End to end: H2D x, forward, D2H z (synchronous). */
 int mgg_engine_forward_host(mgg_engine* e, const float* x, float* z);
+/* Streamed end to end: enqueue one forward whose H2D of x runs on the copy
+ * lane as soon as the previous forward has consumed its input, and whose
+ * D2H of z runs on the other copy lane, so consecutive forwards overlap
+ * their PCIe transfers with each other's kernels. Returns immediately with a
+ * ticket; x must stay valid and z untouched until mgg_engine_wait(ticket).
+ * At most 32 forwards may be outstanding (the call then waits for the
+ * oldest). forward_host == submit + wait. */
+int mgg_engine_submit_host(mgg_engine* e, const float* x, float* z, uint64_t* ticket);
+int mgg_engine_wait(mgg_engine* e, uint64_t ticket);
 /* Layer-k intermediate (post-aggregation accumulator) rows, for parity. */
 int mgg_engine_get_hidden(mgg_engine* e, uint32_t which, float* rows, uint32_t* width);
 /* Standalone aggregation through the engine's plans (K1 over every local

@@ -73,7 +73,13 @@ class Engine {
   void forward();                            // async, device resident
   void synchronize();
   void get_output(float* z);                 // N x out_dim host rows
-  void forward_host(const float* x, float* z);
+  void forward_host(const float* x, float* z);  // submit_host + wait
+  /// Streamed end to end (see mgg_engine_submit_host): the H2D of x and the
+  /// D2H of z run on copy lanes fenced against the compute stream, so
+  /// consecutive submissions overlap PCIe with kernels. x must stay valid and
+  /// z untouched until wait(ticket).
+  std::uint64_t submit_host(const float* x, float* z);
+  void wait(std::uint64_t ticket);
   /// Post-aggregation accumulator of layer `which` (N x width host rows).
   std::uint32_t get_hidden(std::uint32_t which, float* rows);
 
@@ -117,6 +123,11 @@ class Engine {
   void build_plans();
   void free_plans();
   void run(const Op& op);
+  void forward_ops(bool streamed);
+  void find_io_points();
+  static constexpr std::uint64_t kMaxInFlight = 32, kMarkSlots = 64;
+  int in_last_use_ = -1, out_first_write_ = -1;
+  std::uint64_t submitted_ = 0, completed_ = 0;
   mgg_store* scratch(std::uint32_t dim, int slot);
   /// Halo buffer of part p for gather width `dim` (null when p reads fine).
   const float* halo_for(std::uint32_t p, std::uint32_t dim);

@@ -146,6 +146,13 @@ _sig("mgg_engine_set_input", I, vp, f32p)
 _sig("mgg_engine_forward", I, vp)
 _sig("mgg_engine_get_output", I, vp, f32p)
 _sig("mgg_engine_forward_host", I, vp, f32p, f32p)
+_sig("mgg_engine_submit_host", I, vp, f32p, f32p, u64p)
+_sig("mgg_engine_wait", I, vp, U64)
+_sig("mgg_store_upload_on", I, vp, f32p, U64, U64, U32, I)
+_sig("mgg_store_download_on", I, vp, f32p, U64, U64, U32, I)
+_sig("mgg_lane_fence", I, vp, U32, I, I)
+_sig("mgg_lane_mark", I, vp, U32, I, U32)
+_sig("mgg_lane_wait_host", I, vp, U32, U32)
 _sig("mgg_engine_get_hidden", I, vp, U32, f32p, u32p)
 _sig("mgg_engine_aggregate_host", I, vp, f32p, U32, C.c_float, I, f32p)
 _sig("mgg_engine_time_aggregate", I, vp, U32, U32, I, u64p)

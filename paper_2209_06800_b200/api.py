@@ -449,6 +449,19 @@ class Engine:
         check(lib.mgg_engine_forward_host(self._h, _p(x, C.c_float), _p(z, C.c_float)))
         return z
 
+    def submit_host(self, x: np.ndarray, z: np.ndarray) -> int:
+        """Streamed forward (mgg_engine_submit_host): returns a ticket at once;
+        keep x alive and z untouched until wait(ticket)."""
+        assert x.dtype == np.float32 and x.flags.c_contiguous
+        assert z.dtype == np.float32 and z.flags.c_contiguous
+        t = C.c_uint64()
+        check(lib.mgg_engine_submit_host(self._h, _p(x, C.c_float), _p(z, C.c_float),
+                                         C.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        check(lib.mgg_engine_wait(self._h, ticket))
+
     def get_hidden(self, which: int) -> np.ndarray:
         w = C.c_uint32()
         check(lib.mgg_engine_get_hidden(self._h, which, None, C.byref(w)))

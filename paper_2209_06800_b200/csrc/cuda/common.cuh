@@ -34,6 +34,10 @@ struct mgg_ctx {
   std::vector<cudaStream_t> aux;       // per part: halo pulls overlap local K1
   std::vector<cudaEvent_t> fork, join; // per part: main->aux, aux->main
   std::vector<std::vector<cudaEvent_t>> evpool;  // mgg_event_record slots
+  // copy lanes (MGG_LANE_H2D / MGG_LANE_D2H): per device, shared by its parts
+  std::vector<cudaStream_t> h2d, d2h;
+  std::vector<std::vector<cudaEvent_t>> lane_ev;  // per part: [from*3+to] fences
+  std::vector<std::vector<cudaEvent_t>> marks;    // per part: host-waitable slots
   uint64_t launches = 0;
   uint32_t epoch = 0;                  // barrier generation
   bool all_local = true;

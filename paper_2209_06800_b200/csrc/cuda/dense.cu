@@ -43,6 +43,40 @@ struct Shape {
 };
 
 template <int CG>
+__device__ __forceinline__ void stage_x(const DenseArgs& a, float (*xs)[KT + 1], uint64_t row0,
+                                        uint32_t k0) {
+  using S = Shape<CG>;
+  for (int idx = threadIdx.x; idx < S::ROWS * (KT / 4); idx += 256) {
+    const int r = idx / (KT / 4), c4 = idx % (KT / 4);
+    const uint64_t row = row0 + r;
+    const uint32_t kk = k0 + 4 * c4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < a.rows && kk < a.in_pitch)
+      v = __ldg(reinterpret_cast<const float4*>(a.in + row * a.in_pitch + kk));
+    float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float x = (kk + j < a.k) ? e[j] : 0.f;
+      if (a.pre == 2) x += (kk + j < a.k) ? __ldg(a.pre_bias + kk + j) : 0.f;
+      if (a.pre >= 1) x = fmaxf(x, 0.f);
+      xs[r][4 * c4 + j] = x;
+    }
+  }
+}
+
+template <int CG>
+__device__ __forceinline__ void stage_w(const DenseArgs& a, float (*ws)[4 * CG], uint32_t k0) {
+  for (int idx = threadIdx.x; idx < KT * 4 * CG; idx += 256) {
+    const int kr = idx / (4 * CG), c = idx % (4 * CG);
+    const uint32_t kk = k0 + kr, col = a.col0 + c;
+    ws[kr][c] = (kk < a.k && col < a.m) ? __ldg(a.w + (size_t)kk * a.m + col) : 0.f;
+  }
+}
+
+// Persistent over row tiles (grid = resident CTAs): when the whole reduction
+// fits one k-tile (k <= 32: the GCN head, narrow hidden layers) W is staged
+// once per CTA instead of once per 64-row tile.
+template <int CG>
 __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
   using S = Shape<CG>;
   __shared__ float xs[S::ROWS][KT + 1];
@@ -50,108 +84,102 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
 
   const int t = threadIdx.x;
   const int cg = t % CG, rg = t / CG;
-  const uint64_t row0 = (uint64_t)blockIdx.x * S::ROWS;
   const int c_base = a.col0 + 4 * cg;  // absolute output column of lane's group
+  const bool w_once = a.k <= KT;
+  const uint64_t tiles = (a.rows + S::ROWS - 1) / S::ROWS;
 
-  float4 acc[S::RPT];
-#pragma unroll
-  for (int i = 0; i < S::RPT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-
-  for (uint32_t k0 = 0; k0 < a.k; k0 += KT) {
-    // stage x[row0 .. row0+ROWS) x [k0, k0+KT) (pre-transform applied here)
-    for (int idx = t; idx < S::ROWS * (KT / 4); idx += 256) {
-      const int r = idx / (KT / 4), c4 = idx % (KT / 4);
-      const uint64_t row = row0 + r;
-      const uint32_t kk = k0 + 4 * c4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row < a.rows && kk < a.in_pitch)
-        v = __ldg(reinterpret_cast<const float4*>(a.in + row * a.in_pitch + kk));
-      float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float x = (kk + j < a.k) ? e[j] : 0.f;
-        if (a.pre == 2) x += (kk + j < a.k) ? __ldg(a.pre_bias + kk + j) : 0.f;
-        if (a.pre >= 1) x = fmaxf(x, 0.f);
-        xs[r][4 * c4 + j] = x;
-      }
-    }
-    // stage W[k0 .. k0+KT) x [col0, col0 + 4*CG)
-    for (int idx = t; idx < KT * 4 * CG; idx += 256) {
-      const int kr = idx / (4 * CG), c = idx % (4 * CG);
-      const uint32_t kk = k0 + kr, col = a.col0 + c;
-      ws[kr][c] = (kk < a.k && col < a.m) ? __ldg(a.w + (size_t)kk * a.m + col) : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int kk = 0; kk < KT; ++kk) {
-      const float4 w4 = *reinterpret_cast<const float4*>(&ws[kk][4 * cg]);
-#pragma unroll
-      for (int i = 0; i < S::RPT; ++i) {
-        const float x = xs[rg + i * S::RG][kk];
-        acc[i].x = fmaf(x, w4.x, acc[i].x);
-        acc[i].y = fmaf(x, w4.y, acc[i].y);
-        acc[i].z = fmaf(x, w4.z, acc[i].z);
-        acc[i].w = fmaf(x, w4.w, acc[i].w);
-      }
-    }
-    __syncthreads();
-  }
-
-  // epilogue
   float b[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     if (a.bias && c_base + j < (int)a.m) b[j] = __ldg(a.bias + c_base + j);
+  if (w_once) stage_w<CG>(a, ws, 0);
+
+  for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint64_t row0 = tile * S::ROWS;
+    float4 acc[S::RPT];
 #pragma unroll
-  for (int i = 0; i < S::RPT; ++i) {
-    const uint64_t row = row0 + rg + i * S::RG;
-    float y[4] = {acc[i].x + b[0], acc[i].y + b[1], acc[i].z + b[2], acc[i].w + b[3]};
-    if (a.out2 && row < a.rows && c_base < (int)a.out_pitch) {
-      float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
-      float* po = &o2.x;
+    for (int i = 0; i < S::RPT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    for (uint32_t k0 = 0; k0 < a.k; k0 += KT) {
+      stage_x<CG>(a, xs, row0, k0);
+      if (!w_once) stage_w<CG>(a, ws, k0);
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < KT; ++kk) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&ws[kk][4 * cg]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) po[j] = (c_base + j < (int)a.m) ? y[j] * a.out2_scale : 0.f;
-      *reinterpret_cast<float4*>(a.out2 + row * a.out_pitch + c_base) = o2;
-    }
-    if (a.act == 1) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) y[j] = fmaxf(y[j], 0.f);
-    } else if (a.act == 2) {
-      // row softmax across the CG lanes holding this row (m <= 4*CG here)
-      float mx = -FLT_MAX;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (c_base + j < (int)a.m) mx = fmaxf(mx, y[j]);
-#pragma unroll
-      for (int off = CG / 2; off >= 1; off >>= 1)
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      float s = 0.f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        y[j] = (c_base + j < (int)a.m) ? __expf(y[j] - mx) : 0.f;
-        s += y[j];
+        for (int i = 0; i < S::RPT; ++i) {
+          const float x = xs[rg + i * S::RG][kk];
+          acc[i].x = fmaf(x, w4.x, acc[i].x);
+          acc[i].y = fmaf(x, w4.y, acc[i].y);
+          acc[i].z = fmaf(x, w4.z, acc[i].z);
+          acc[i].w = fmaf(x, w4.w, acc[i].w);
+        }
       }
-#pragma unroll
-      for (int off = CG / 2; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      const float inv = 1.f / s;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) y[j] *= inv;
+      __syncthreads();
     }
-    if (row < a.rows && c_base < (int)a.out_pitch) {
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-      float* po = &o.x;
+
+    // epilogue
 #pragma unroll
-      for (int j = 0; j < 4; ++j) po[j] = (c_base + j < (int)a.m) ? y[j] : 0.f;
-      *reinterpret_cast<float4*>(a.out + row * a.out_pitch + c_base) = o;
+    for (int i = 0; i < S::RPT; ++i) {
+      const uint64_t row = row0 + rg + i * S::RG;
+      float y[4] = {acc[i].x + b[0], acc[i].y + b[1], acc[i].z + b[2], acc[i].w + b[3]};
+      if (a.out2 && row < a.rows && c_base < (int)a.out_pitch) {
+        float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float* po = &o2.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) po[j] = (c_base + j < (int)a.m) ? y[j] * a.out2_scale : 0.f;
+        *reinterpret_cast<float4*>(a.out2 + row * a.out_pitch + c_base) = o2;
+      }
+      if (a.act == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y[j] = fmaxf(y[j], 0.f);
+      } else if (a.act == 2) {
+        // row softmax across the CG lanes holding this row (m <= 4*CG here)
+        float mx = -FLT_MAX;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c_base + j < (int)a.m) mx = fmaxf(mx, y[j]);
+#pragma unroll
+        for (int off = CG / 2; off >= 1; off >>= 1)
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          y[j] = (c_base + j < (int)a.m) ? __expf(y[j] - mx) : 0.f;
+          s += y[j];
+        }
+#pragma unroll
+        for (int off = CG / 2; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        const float inv = 1.f / s;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y[j] *= inv;
+      }
+      if (row < a.rows && c_base < (int)a.out_pitch) {
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float* po = &o.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) po[j] = (c_base + j < (int)a.m) ? y[j] : 0.f;
+        *reinterpret_cast<float4*>(a.out + row * a.out_pitch + c_base) = o;
+      }
     }
   }
 }
 
 template <int CG>
 void run(const DenseArgs& a, cudaStream_t st) {
-  const uint64_t blocks = (a.rows + Shape<CG>::ROWS - 1) / Shape<CG>::ROWS;
-  if (blocks == 0) return;
-  dense_kernel<CG><<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
+  const uint64_t tiles = (a.rows + Shape<CG>::ROWS - 1) / Shape<CG>::ROWS;
+  if (tiles == 0) return;
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    int dev = 0;
+    MGG_CUDA(cudaGetDevice(&dev));
+    MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_kernel<CG>, 256, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)sms * per_sm);
+  dense_kernel<CG><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
 }
 
 // Row softmax over the first m columns (one warp per row), in place allowed.

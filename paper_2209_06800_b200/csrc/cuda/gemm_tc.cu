@@ -415,8 +415,13 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
     return 1024 + wbytes + (stages + kLoSlots) * kTileBytes +
            kEpiGroups<NP> * BM * (NP + 4) * 4 + (3 * stages + 5 + kLoSlots) * 8 + 16;
   };
+  static const uint32_t cap_env = [] {
+    const char* e = std::getenv("MGG_TC_STAGES");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  if (cap_env) b.stages = std::min<uint32_t>(cap_env, kMaxStages);
   while (b.stages > 2 && smem_for(b.stages) > 227 * 1024) --b.stages;
-  if (b.stages > 2 * a.n_kb + 2) b.stages = 2 * a.n_kb + 2;  // no use beyond ~2 tiles
+  if (!cap_env && b.stages > 2 * a.n_kb + 2) b.stages = 2 * a.n_kb + 2;  // no use beyond ~2 tiles
   const size_t smem = smem_for(b.stages);
   if (smem > 227 * 1024) throw Status{MGG_E_CONFIG, "gemm_tc: W too large for smem"};
   const CUtensorMap mx = make_map(in, a.k, a.rows, size_t(in_pitch) * 4, BK, BM);

@@ -169,6 +169,10 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
       c->fork.assign(num_parts, nullptr);
       c->join.assign(num_parts, nullptr);
       c->evpool.assign(num_parts, {});
+      c->h2d.assign(num_parts, nullptr);
+      c->d2h.assign(num_parts, nullptr);
+      c->lane_ev.assign(num_parts, std::vector<cudaEvent_t>(9, nullptr));
+      c->marks.assign(num_parts, {});
       int first = -1;
       for (uint32_t p = 0; p < num_parts; ++p) {
         const int d = c->device[p];
@@ -190,6 +194,15 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
         for (uint32_t q = 0; q < p; ++q)
           if (c->device[q] == d) c->aux[p] = c->aux[q];
         if (!c->aux[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->aux[p], cudaStreamNonBlocking));
+        for (uint32_t q = 0; q < p; ++q)
+          if (c->device[q] == d) {
+            c->h2d[p] = c->h2d[q];
+            c->d2h[p] = c->d2h[q];
+          }
+        if (!c->h2d[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->h2d[p], cudaStreamNonBlocking));
+        if (!c->d2h[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->d2h[p], cudaStreamNonBlocking));
+        for (auto& e : c->lane_ev[p])
+          MGG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         MGG_CUDA(cudaEventCreateWithFlags(&c->fork[p], cudaEventDisableTiming));
         MGG_CUDA(cudaEventCreateWithFlags(&c->join[p], cudaEventDisableTiming));
       }
@@ -234,6 +247,16 @@ int mgg_ctx_destroy(mgg_ctx* c) {
     if (c->join[p]) cudaEventDestroy(c->join[p]);
     for (cudaEvent_t e : c->evpool[p])
       if (e) cudaEventDestroy(e);
+    bool shared_cp = false;
+    for (uint32_t q = 0; q < p; ++q) shared_cp |= c->h2d[q] == c->h2d[p];
+    if (!shared_cp) {
+      if (c->h2d[p]) cudaStreamDestroy(c->h2d[p]);
+      if (c->d2h[p]) cudaStreamDestroy(c->d2h[p]);
+    }
+    for (cudaEvent_t e : c->lane_ev[p])
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->marks[p])
+      if (e) cudaEventDestroy(e);
   }
   delete c;
   return MGG_OK;
@@ -244,8 +267,49 @@ int mgg_ctx_synchronize(mgg_ctx* c) {
     for (uint32_t p = 0; p < c->num_parts; ++p) {
       if (c->device[p] < 0) continue;
       MGG_CUDA(cudaSetDevice(c->device[p]));
+      MGG_CUDA(cudaStreamSynchronize(c->h2d[p]));
       MGG_CUDA(cudaStreamSynchronize(c->stream[p]));
+      MGG_CUDA(cudaStreamSynchronize(c->d2h[p]));
     }
+  });
+}
+
+static cudaStream_t lane_stream(mgg_ctx* ctx, uint32_t part, int lane) {
+  cudaStream_t st = enter(ctx, part);
+  switch (lane) {
+    case MGG_LANE_COMPUTE: return st;
+    case MGG_LANE_H2D: return ctx->h2d[part];
+    case MGG_LANE_D2H: return ctx->d2h[part];
+    default: throw Status{MGG_E_INPUT, "lane must be 0 (compute), 1 (h2d) or 2 (d2h)"};
+  }
+}
+
+int mgg_lane_fence(mgg_ctx* ctx, uint32_t part, int from, int to) {
+  return guard([&] {
+    cudaStream_t a = lane_stream(ctx, part, from), b = lane_stream(ctx, part, to);
+    if (a == b) return;
+    cudaEvent_t e = ctx->lane_ev[part][from * 3 + to];
+    MGG_CUDA(cudaEventRecord(e, a));
+    MGG_CUDA(cudaStreamWaitEvent(b, e, 0));
+  });
+}
+
+int mgg_lane_mark(mgg_ctx* ctx, uint32_t part, int lane, uint32_t slot) {
+  return guard([&] {
+    cudaStream_t st = lane_stream(ctx, part, lane);
+    auto& m = ctx->marks[part];
+    if (slot >= m.size()) m.resize(slot + 1, nullptr);
+    if (!m[slot]) MGG_CUDA(cudaEventCreateWithFlags(&m[slot], cudaEventDisableTiming));
+    MGG_CUDA(cudaEventRecord(m[slot], st));
+  });
+}
+
+int mgg_lane_wait_host(mgg_ctx* ctx, uint32_t part, uint32_t slot) {
+  return guard([&] {
+    enter(ctx, part);
+    const auto& m = ctx->marks[part];
+    if (slot >= m.size() || !m[slot]) throw Status{MGG_E_INPUT, "lane_wait_host: slot never marked"};
+    MGG_CUDA(cudaEventSynchronize(m[slot]));
   });
 }
 
@@ -402,7 +466,7 @@ constexpr size_t kStageBytes = 32u << 20;
 extern "C" {
 
 static int copy_rows(const mgg_store* cs, float* host_rw, const float* host_ro,
-                     uint64_t row_begin, uint64_t row_count, uint32_t ld, bool up) {
+                     uint64_t row_begin, uint64_t row_count, uint32_t ld, bool up, int lane) {
   return guard([&] {
     if (!cs) throw Status{MGG_E_INPUT, "store copy: null store"};
     if (ld < cs->dim) throw Status{MGG_E_INPUT, "store copy: ld < dim"};
@@ -413,7 +477,7 @@ static int copy_rows(const mgg_store* cs, float* host_rw, const float* host_ro,
       if (ctx->device[p] < 0) continue;
       const uint64_t a = std::max(row_begin, s->lb[p]), b = std::min(end, s->lb[p + 1]);
       if (a >= b) continue;
-      cudaStream_t st = enter(ctx, p);
+      cudaStream_t st = lane_stream(ctx, p, lane);
       float* dev = s->shard[p] + (a - s->lb[p]) * s->pitch;
       const size_t hoff = (a - row_begin) * (size_t)ld;
       const size_t row_bytes = size_t(s->dim) * 4;
@@ -454,12 +518,22 @@ static int copy_rows(const mgg_store* cs, float* host_rw, const float* host_ro,
 
 int mgg_store_upload(mgg_store* s, const float* host, uint64_t row_begin,
                      uint64_t row_count, uint32_t ld) {
-  return copy_rows(s, nullptr, host, row_begin, row_count, ld, true);
+  return copy_rows(s, nullptr, host, row_begin, row_count, ld, true, MGG_LANE_COMPUTE);
 }
 
 int mgg_store_download(const mgg_store* s, float* host, uint64_t row_begin,
                        uint64_t row_count, uint32_t ld) {
-  return copy_rows(s, host, nullptr, row_begin, row_count, ld, false);
+  return copy_rows(s, host, nullptr, row_begin, row_count, ld, false, MGG_LANE_COMPUTE);
+}
+
+int mgg_store_upload_on(mgg_store* s, const float* host, uint64_t row_begin,
+                        uint64_t row_count, uint32_t ld, int lane) {
+  return copy_rows(s, nullptr, host, row_begin, row_count, ld, true, lane);
+}
+
+int mgg_store_download_on(const mgg_store* s, float* host, uint64_t row_begin,
+                          uint64_t row_count, uint32_t ld, int lane) {
+  return copy_rows(s, host, nullptr, row_begin, row_count, ld, false, lane);
 }
 
 int mgg_store_shard(const mgg_store* s, uint32_t part, void** dptr) {

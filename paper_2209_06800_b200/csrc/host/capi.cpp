@@ -479,6 +479,15 @@ int mgg_engine_get_output(mgg_engine* e, float* z) {
 int mgg_engine_forward_host(mgg_engine* e, const float* x, float* z) {
   return guard([&] { e->e->forward_host(x, z); });
 }
+int mgg_engine_submit_host(mgg_engine* e, const float* x, float* z, uint64_t* ticket) {
+  return guard([&] {
+    if (!ticket) throw mgg::InputError("submit_host: null ticket");
+    *ticket = e->e->submit_host(x, z);
+  });
+}
+int mgg_engine_wait(mgg_engine* e, uint64_t ticket) {
+  return guard([&] { e->e->wait(ticket); });
+}
 int mgg_engine_get_hidden(mgg_engine* e, uint32_t which, float* rows, uint32_t* width) {
   return guard([&] {
     const std::uint32_t w = e->e->get_hidden(which, rows);

@@ -46,6 +46,7 @@ Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
     for (std::uint32_t p = 0; p <= num_parts_; ++p) flag_lb[p] = p;
     ok(mgg_store_create(ctx_, flag_lb.data(), kMaxOwners, &flags_));
     build_program();
+    find_io_points();
     build_plans();
   } catch (...) {
     free_plans();
@@ -158,7 +159,11 @@ void Engine::build_program() {
       ob2 += b;
       const float self = 1.f + s.eps;
       const int O = add_store(b);
-      if (h < a) {  // T = f(H)·W1; A = (1+eps)T + Σ T_u; O = ReLU(A+b1)·W2 + b2
+      // h <= a: T = f(H)·W1; A = (1+eps)T + Σ T_u; O = ReLU(A+b1)·W2 + b2.
+      // At h == a the aggregation width is the same either way, but this
+      // order needs no separate self-term pass (the GEMM epilogue seeds A)
+      // and one GEMM after the aggregation instead of two.
+      if (h <= a) {
         const int T = add_store(h), A = add_store(h);
         program_.push_back({OpKind::dense, cur, T, A, W1, -1, -1, std::uint32_t(fin), 0, self, 0});
         program_.push_back({OpKind::barrier});
@@ -341,19 +346,82 @@ void Engine::set_input(const float* x) {
   ok(mgg_store_upload(stores_[input_], x, 0, g_.num_nodes, spec_.in_dim));
 }
 
-void Engine::forward() {
+void Engine::forward() { forward_ops(false); }
+
+// `streamed`: the forward of submit_host — its input arrives on the H2D lane
+// and its output leaves on the D2H lane, fenced so that the next forward's
+// H2D starts as soon as this one has consumed the input store.
+void Engine::forward_ops(bool streamed) {
+  auto fence_all = [&](int from, int to) {
+    for (std::uint32_t p = 0; p < num_parts_; ++p)
+      if (dev_[p] >= 0) ok(mgg_lane_fence(ctx_, p, from, to));
+  };
   // inputs of every part must be resident before the first peer gather
   ok(mgg_barrier(ctx_, flags_));
-  if (!profiling_) {
-    for (const Op& op : program_) run(op);
-    return;
-  }
-  prof_starts_.push_back(next_slot_);
-  ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
-  for (const Op& op : program_) {
-    run(op);
+  if (profiling_) {
+    prof_starts_.push_back(next_slot_);
     ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
   }
+  for (std::size_t i = 0; i < program_.size(); ++i) {
+    if (streamed && static_cast<int>(i) == out_first_write_)
+      fence_all(MGG_LANE_D2H, MGG_LANE_COMPUTE);  // previous z has left the device
+    run(program_[i]);
+    if (profiling_) ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
+    if (streamed && static_cast<int>(i) == in_last_use_)
+      fence_all(MGG_LANE_COMPUTE, MGG_LANE_H2D);  // next x may overwrite the input
+  }
+}
+
+// Last op after which no kernel (of any part) reads the input store, and the
+// first op writing the output store.
+void Engine::find_io_points() {
+  in_last_use_ = -1;
+  out_first_write_ = -1;
+  bool peer_read = false;
+  for (std::size_t i = 0; i < program_.size(); ++i) {
+    const Op& op = program_[i];
+    if (op.in == input_) {
+      in_last_use_ = static_cast<int>(i);
+      peer_read = op.kind == OpKind::aggregate && num_parts_ > 1;
+    }
+    if (out_first_write_ < 0 && (op.out == output_ || op.out2 == output_))
+      out_first_write_ = static_cast<int>(i);
+  }
+  if (peer_read) {
+    // peers gather the input too: it is free once every part has passed the
+    // next K3 barrier (each part reaches it only after its own gathers)
+    int j = in_last_use_ + 1;
+    while (j < static_cast<int>(program_.size()) && program_[j].kind != OpKind::barrier) ++j;
+    in_last_use_ = std::min(j, static_cast<int>(program_.size()) - 1);
+  }
+}
+
+std::uint64_t Engine::submit_host(const float* x, float* z) {
+  if (submitted_ - completed_ >= kMaxInFlight) wait(submitted_ - kMaxInFlight + 1);
+  const std::uint64_t ticket = ++submitted_;
+  ok(mgg_store_upload_on(stores_[input_], x, 0, g_.num_nodes, spec_.in_dim, MGG_LANE_H2D));
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0) ok(mgg_lane_fence(ctx_, p, MGG_LANE_H2D, MGG_LANE_COMPUTE));
+  forward_ops(true);
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0) ok(mgg_lane_fence(ctx_, p, MGG_LANE_COMPUTE, MGG_LANE_D2H));
+  ok(mgg_store_download_on(stores_[output_], z, 0, g_.num_nodes, spec_.out_dim, MGG_LANE_D2H));
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0)
+      ok(mgg_lane_mark(ctx_, p, MGG_LANE_D2H, static_cast<std::uint32_t>(ticket % kMarkSlots)));
+  return ticket;
+}
+
+void Engine::wait(std::uint64_t ticket) {
+  if (ticket == 0 || ticket > submitted_) throw InputError("engine: unknown ticket");
+  if (ticket <= completed_) return;
+  // marks are recorded in ticket order on one lane: waiting for `ticket`
+  // also completes every earlier one (a slot re-marked by a newer ticket
+  // only waits longer)
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0)
+      ok(mgg_lane_wait_host(ctx_, p, static_cast<std::uint32_t>(ticket % kMarkSlots)));
+  completed_ = ticket;
 }
 
 void Engine::set_profiling(bool on) {
@@ -391,11 +459,7 @@ void Engine::get_output(float* z) {
   synchronize();
 }
 
-void Engine::forward_host(const float* x, float* z) {
-  set_input(x);
-  forward();
-  get_output(z);
-}
+void Engine::forward_host(const float* x, float* z) { wait(submit_host(x, z)); }
 
 std::uint32_t Engine::get_hidden(std::uint32_t which, float* rows) {
   if (which >= hidden_.size()) throw InputError("engine: no such hidden layer");

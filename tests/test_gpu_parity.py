@@ -104,6 +104,39 @@ def test_gcn2_forward(mgg, oracle_mod, parts):
     eng.close()
 
 
+@pytest.mark.parametrize("kind,parts", [("gcn", 1), ("gcn", 3), ("gin", 2), ("gcn-agg-first", 2)])
+def test_streamed_submit_matches_oracle(mgg, oracle_mod, kind, parts):
+    # several forwards in flight (H2D of step k+1 overlapping step k's
+    # kernels, D2H on the other copy lane), each with its own input: every z
+    # must be its own input's forward. "gcn-agg-first": dim <= hidden, so the
+    # input store itself is gathered by peers (freed only after a barrier).
+    g = mgg.gen_rmat(3000, 40000, seed=13)
+    if kind == "gin":
+        din, model = 100, mgg.make_gin(100, 64, 47, layers=3, seed=8)
+    elif kind == "gcn":
+        din, model = 96, mgg.make_gcn(96, 16, 41, seed=3)
+    else:
+        din, model = 12, mgg.make_gcn(12, 16, 5, seed=3)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=16, dist=2, wpb=4)
+    steps = 6
+    xs = [mgg.host_alloc((g.num_nodes, din)) for _ in range(steps)]
+    zs = [mgg.host_alloc((g.num_nodes, model.out_dim)) for _ in range(steps)]
+    for i in range(steps):
+        xs[i][:] = mgg.random_features(g.num_nodes, din, seed=100 + i)
+        zs[i][:] = np.nan
+    tickets = [eng.submit_host(xs[i], zs[i]) for i in range(steps)]
+    eng.wait(tickets[-1])
+    for i in range(steps):
+        if kind == "gin":
+            _, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, xs[i], model)
+        else:
+            _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, xs[i], model)
+        err = np.abs(zs[i] - zr).max()
+        assert err <= TOL, f"step {i}: {err}"
+    eng.wait(tickets[0])  # already complete: no-op
+    eng.close()
+
+
 def test_gcn2_update_first_second_layer(mgg, oracle_mod):
     # classes < hidden: layer 2 runs dense-first then aggregation + softmax
     g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 10, 2)
