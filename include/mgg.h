@@ -110,6 +110,8 @@ int mgg_lane_fence(mgg_ctx* ctx, uint32_t part, int from, int to);
  * (blocking the calling thread) until the device reaches it. */
 int mgg_lane_mark(mgg_ctx* ctx, uint32_t part, int lane, uint32_t slot);
 int mgg_lane_wait_host(mgg_ctx* ctx, uint32_t part, uint32_t slot);
+/* Device-side: lane `lane` waits until the device reaches mark `slot`. */
+int mgg_lane_wait_mark(mgg_ctx* ctx, uint32_t part, int lane, uint32_t slot);
 /* Device pointer of a shard as seen by this process (local or imported). */
 int mgg_store_shard(const mgg_store* s, uint32_t part, void** dptr);
 

@@ -128,6 +128,10 @@ class Engine {
   static constexpr std::uint64_t kMaxInFlight = 32, kMarkSlots = 64;
   int in_last_use_ = -1, out_first_write_ = -1;
   std::uint64_t submitted_ = 0, completed_ = 0;
+  // Streamed input double buffer (only when no peer gathers the input):
+  // submission t uploads into in_bufs_[t % 2] while t-1 computes on the other
+  mgg_store* in_bufs_[2] = {nullptr, nullptr};
+  bool in_marked_[2] = {false, false};
   mgg_store* scratch(std::uint32_t dim, int slot);
   /// Halo buffer of part p for gather width `dim` (null when p reads fine).
   const float* halo_for(std::uint32_t p, std::uint32_t dim);

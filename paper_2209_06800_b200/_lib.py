@@ -153,6 +153,7 @@ _sig("mgg_store_download_on", I, vp, f32p, U64, U64, U32, I)
 _sig("mgg_lane_fence", I, vp, U32, I, I)
 _sig("mgg_lane_mark", I, vp, U32, I, U32)
 _sig("mgg_lane_wait_host", I, vp, U32, U32)
+_sig("mgg_lane_wait_mark", I, vp, U32, I, U32)
 _sig("mgg_engine_get_hidden", I, vp, U32, f32p, u32p)
 _sig("mgg_engine_aggregate_host", I, vp, f32p, U32, C.c_float, I, f32p)
 _sig("mgg_engine_time_aggregate", I, vp, U32, U32, I, u64p)

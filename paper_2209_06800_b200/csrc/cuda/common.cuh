@@ -36,6 +36,7 @@ struct mgg_ctx {
   std::vector<std::vector<cudaEvent_t>> evpool;  // mgg_event_record slots
   // copy lanes (MGG_LANE_H2D / MGG_LANE_D2H): per device, shared by its parts
   std::vector<cudaStream_t> h2d, d2h;
+  std::vector<cudaStream_t> rp;                   // per device: staging re-pitch kernels
   std::vector<std::vector<cudaEvent_t>> lane_ev;  // per part: [from*3+to] fences
   std::vector<std::vector<cudaEvent_t>> marks;    // per part: host-waitable slots
   uint64_t launches = 0;
@@ -52,7 +53,11 @@ struct mgg_store {
   std::vector<uint8_t> owned, imported;
   // per local part: device copy of the shard table for that part's device
   std::vector<const float**> dtable;
-  std::vector<float*> stage;           // per local part: dense H2D/D2H slab
+  // per local part: two dense H2D/D2H slabs (2p, 2p+1) and their events
+  // (5p + {full0, full1, free0, free1, tail}) — copies and re-pitch kernels
+  // alternate slabs so the DMA engine never waits for a re-pitch
+  std::vector<float*> stage;
+  std::vector<cudaEvent_t> stage_ev;
   uint64_t rows(uint32_t p) const { return lb[p + 1] - lb[p]; }
 };
 

@@ -33,7 +33,7 @@ struct DenseArgs {
   float out2_scale;
 };
 
-constexpr int KT = 32;
+// k-tile: 16 when the whole reduction is <= 16 (the GCN heads), else 32
 
 template <int CG>
 struct Shape {
@@ -42,7 +42,7 @@ struct Shape {
   static constexpr int ROWS = RG * RPT;               // rows per CTA
 };
 
-template <int CG>
+template <int CG, int KT>
 __device__ __forceinline__ void stage_x(const DenseArgs& a, float (*xs)[KT + 1], uint64_t row0,
                                         uint32_t k0) {
   using S = Shape<CG>;
@@ -64,7 +64,7 @@ __device__ __forceinline__ void stage_x(const DenseArgs& a, float (*xs)[KT + 1],
   }
 }
 
-template <int CG>
+template <int CG, int KT>
 __device__ __forceinline__ void stage_w(const DenseArgs& a, float (*ws)[4 * CG], uint32_t k0) {
   for (int idx = threadIdx.x; idx < KT * 4 * CG; idx += 256) {
     const int kr = idx / (4 * CG), c = idx % (4 * CG);
@@ -76,7 +76,7 @@ __device__ __forceinline__ void stage_w(const DenseArgs& a, float (*ws)[4 * CG],
 // Persistent over row tiles (grid = resident CTAs): when the whole reduction
 // fits one k-tile (k <= 32: the GCN head, narrow hidden layers) W is staged
 // once per CTA instead of once per 64-row tile.
-template <int CG>
+template <int CG, int KT>
 __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
   using S = Shape<CG>;
   __shared__ float xs[S::ROWS][KT + 1];
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     if (a.bias && c_base + j < (int)a.m) b[j] = __ldg(a.bias + c_base + j);
-  if (w_once) stage_w<CG>(a, ws, 0);
+  if (w_once) stage_w<CG, KT>(a, ws, 0);
 
   for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint64_t row0 = tile * S::ROWS;
@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
     for (int i = 0; i < S::RPT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     for (uint32_t k0 = 0; k0 < a.k; k0 += KT) {
-      stage_x<CG>(a, xs, row0, k0);
-      if (!w_once) stage_w<CG>(a, ws, k0);
+      stage_x<CG, KT>(a, xs, row0, k0);
+      if (!w_once) stage_w<CG, KT>(a, ws, k0);
       __syncthreads();
 #pragma unroll 8
       for (int kk = 0; kk < KT; ++kk) {
@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
   }
 }
 
-template <int CG>
-void run(const DenseArgs& a, cudaStream_t st) {
+template <int CG, int KT>
+void run_kt(const DenseArgs& a, cudaStream_t st) {
   const uint64_t tiles = (a.rows + Shape<CG>::ROWS - 1) / Shape<CG>::ROWS;
   if (tiles == 0) return;
   static int per_sm = 0, sms = 0;
@@ -175,11 +175,19 @@ void run(const DenseArgs& a, cudaStream_t st) {
     int dev = 0;
     MGG_CUDA(cudaGetDevice(&dev));
     MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_kernel<CG>, 256, 0));
+    MGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_kernel<CG, KT>, 256, 0));
     per_sm = std::max(per_sm, 1);
   }
   const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)sms * per_sm);
-  dense_kernel<CG><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
+  dense_kernel<CG, KT><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
+}
+
+template <int CG>
+void run(const DenseArgs& a, cudaStream_t st) {
+  if (a.k <= 16)
+    run_kt<CG, 16>(a, st);
+  else
+    run_kt<CG, 32>(a, st);
 }
 
 // Row softmax over the first m columns (one warp per row), in place allowed.

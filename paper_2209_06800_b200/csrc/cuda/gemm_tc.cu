@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   constexpr uint32_t kIdesc2 = kIdescBase | (static_cast<uint32_t>((2 * NP) >> 3) << 17);
   constexpr uint32_t kIdesc1 = kIdescBase | (static_cast<uint32_t>(NP >> 3) << 17);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-B alignment for the 128-B swizzle, by offsetting the shared array
+  // itself (a round trip through uintptr_t would lose the address space and
+  // turn every staging access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const uint32_t wbytes = a.n_kb * 2 * NP * 128;
   uint8_t* w_s = smem;                          // [kb][hi|lo][NP][128 B]
   uint8_t* x_s = smem + wbytes;                 // [stage][16 KB] raw X -> Xh in place
@@ -164,6 +166,16 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   uint64_t* lofree = tempty + 2;              // [kLoSlots]
   uint64_t* wfull = lofree + kLoSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
+  // bias (NP) and pre-bias (n_kb*BK) staged once: the epilogue and split read
+  // them as shared-memory broadcasts instead of per-element global loads
+  uint8_t* tail = reinterpret_cast<uint8_t*>(wfull + 2);
+  float* bias_s = reinterpret_cast<float*>(tail + ((16u - (su32(tail) & 15u)) & 15u));
+  float* pb_s = bias_s + NP;
+  for (uint32_t i = threadIdx.x; i < NP; i += blockDim.x)
+    bias_s[i] = (a.bias && i < a.m) ? __ldg(a.bias + i) : 0.f;
+  if (a.pre == 2)
+    for (uint32_t i = threadIdx.x; i < a.n_kb * BK; i += blockDim.x)
+      pb_s[i] = i < a.k ? __ldg(a.pre_bias + i) : 0.f;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n_tiles = static_cast<uint32_t>((a.rows + BM - 1) / BM);
@@ -262,7 +274,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float x = e[q];
-              if (a.pre == 2 && k0 + q < a.k) x += __ldg(a.pre_bias + k0 + q);
+              if (a.pre == 2) x += pb_s[k0 + q];
               e[q] = fmaxf(x, 0.f);
             }
           }
@@ -326,9 +338,16 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
         }
         __syncwarp();
       };
+      if (a.bias) {
 #pragma unroll
-      for (int c = 0; c < NP; ++c)
-        if (a.bias && c < static_cast<int>(a.m)) y[c] += __ldg(a.bias + c);
+        for (int c = 0; c < NP; c += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c);
+          y[c] += b4.x;
+          y[c + 1] += b4.y;
+          y[c + 2] += b4.z;
+          y[c + 3] += b4.w;
+        }
+      }
       if (a.out2) stage_and_store(a.out2, a.out2_scale);
       if (a.act == 1) {
 #pragma unroll
@@ -413,7 +432,8 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   b.stages = kMaxStages;
   auto smem_for = [&](uint32_t stages) {
     return 1024 + wbytes + (stages + kLoSlots) * kTileBytes +
-           kEpiGroups<NP> * BM * (NP + 4) * 4 + (3 * stages + 5 + kLoSlots) * 8 + 16;
+           kEpiGroups<NP> * BM * (NP + 4) * 4 + (3 * stages + 5 + kLoSlots) * 8 + 16 +
+           16 + 4 * (NP + a.n_kb * BK);
   };
   static const uint32_t cap_env = [] {
     const char* e = std::getenv("MGG_TC_STAGES");
@@ -447,7 +467,9 @@ bool gemm_tc_supported(uint32_t k, uint32_t m) {
   if (m == 0 || m > 64 || k < min_k || k < 8) return false;
   const uint32_t np = (m + 15) / 16 * 16;
   const size_t wbytes = size_t((k + BK - 1) / BK) * 2 * np * 128;
-  return 1024 + wbytes + (2 + kLoSlots) * kTileBytes + 2 * BM * (np + 4) * 4 + 128 <=
+  const size_t kpad = size_t((k + BK - 1) / BK) * BK;
+  return 1024 + wbytes + (2 + kLoSlots) * kTileBytes + 2 * BM * (np + 4) * 4 + 128 + 16 +
+             4 * (np + kpad) <=
          227 * 1024;
 }
 

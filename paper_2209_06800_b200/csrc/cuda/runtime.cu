@@ -171,6 +171,7 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
       c->evpool.assign(num_parts, {});
       c->h2d.assign(num_parts, nullptr);
       c->d2h.assign(num_parts, nullptr);
+      c->rp.assign(num_parts, nullptr);
       c->lane_ev.assign(num_parts, std::vector<cudaEvent_t>(9, nullptr));
       c->marks.assign(num_parts, {});
       int first = -1;
@@ -198,9 +199,11 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
           if (c->device[q] == d) {
             c->h2d[p] = c->h2d[q];
             c->d2h[p] = c->d2h[q];
+            c->rp[p] = c->rp[q];
           }
         if (!c->h2d[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->h2d[p], cudaStreamNonBlocking));
         if (!c->d2h[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->d2h[p], cudaStreamNonBlocking));
+        if (!c->rp[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->rp[p], cudaStreamNonBlocking));
         for (auto& e : c->lane_ev[p])
           MGG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         MGG_CUDA(cudaEventCreateWithFlags(&c->fork[p], cudaEventDisableTiming));
@@ -252,6 +255,7 @@ int mgg_ctx_destroy(mgg_ctx* c) {
     if (!shared_cp) {
       if (c->h2d[p]) cudaStreamDestroy(c->h2d[p]);
       if (c->d2h[p]) cudaStreamDestroy(c->d2h[p]);
+      if (c->rp[p]) cudaStreamDestroy(c->rp[p]);
     }
     for (cudaEvent_t e : c->lane_ev[p])
       if (e) cudaEventDestroy(e);
@@ -304,6 +308,15 @@ int mgg_lane_mark(mgg_ctx* ctx, uint32_t part, int lane, uint32_t slot) {
   });
 }
 
+int mgg_lane_wait_mark(mgg_ctx* ctx, uint32_t part, int lane, uint32_t slot) {
+  return guard([&] {
+    cudaStream_t st = lane_stream(ctx, part, lane);
+    const auto& m = ctx->marks[part];
+    if (slot >= m.size() || !m[slot]) throw Status{MGG_E_INPUT, "lane_wait_mark: slot never marked"};
+    MGG_CUDA(cudaStreamWaitEvent(st, m[slot], 0));
+  });
+}
+
 int mgg_lane_wait_host(mgg_ctx* ctx, uint32_t part, uint32_t slot) {
   return guard([&] {
     enter(ctx, part);
@@ -352,7 +365,8 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
       s->owned.assign(ctx->num_parts, 0);
       s->imported.assign(ctx->num_parts, 0);
       s->dtable.assign(ctx->num_parts, nullptr);
-      s->stage.assign(ctx->num_parts, nullptr);
+      s->stage.assign(2 * ctx->num_parts, nullptr);
+      s->stage_ev.assign(5 * ctx->num_parts, nullptr);
       for (uint32_t p = 0; p < ctx->num_parts; ++p) {
         if (ctx->device[p] < 0) continue;
         MGG_CUDA(cudaSetDevice(ctx->device[p]));
@@ -385,10 +399,13 @@ int mgg_store_destroy(mgg_store* s) {
       cudaSetDevice(ctx->device[p]);
       cudaFree(s->dtable[p]);
     }
-    if (s->stage[p]) {
-      cudaSetDevice(ctx->device[p]);
-      cudaFree(s->stage[p]);
-    }
+    for (int i = 0; i < 2; ++i)
+      if (s->stage[2 * p + i]) {
+        cudaSetDevice(ctx->device[p]);
+        cudaFree(s->stage[2 * p + i]);
+      }
+    for (int i = 0; i < 5; ++i)
+      if (s->stage_ev[5 * p + i]) cudaEventDestroy(s->stage_ev[5 * p + i]);
   }
   delete s;
   return MGG_OK;
@@ -442,11 +459,15 @@ namespace mgg::dev {
 __global__ void repitch_kernel(const float* __restrict__ src, uint32_t src_ld,
                                float* __restrict__ dst, uint32_t dst_ld, uint64_t rows,
                                uint32_t cols) {
-  const uint64_t total = rows * cols;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = i / cols, c = i % cols;
-    dst[r * dst_ld + c] = src[r * src_ld + c];
+  // one warp per row, lanes stride the columns (coalesced on both sides;
+  // no per-element division)
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += warps) {
+    const float* a = src + r * src_ld;
+    float* b = dst + r * dst_ld;
+    for (uint32_t c = lane; c < cols; c += 32) b[c] = __ldg(a + c);
   }
 }
 
@@ -454,7 +475,7 @@ void repitch(const float* src, uint32_t src_ld, float* dst, uint32_t dst_ld, uin
              uint32_t cols, cudaStream_t st) {
   const uint64_t total = rows * cols;
   if (!total) return;
-  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148 * 16));
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, 148 * 16));
   repitch_kernel<<<blocks, 256, 0, st>>>(src, src_ld, dst, dst_ld, rows, cols);
   MGG_CUDA(cudaGetLastError());
 }
@@ -497,20 +518,48 @@ static int copy_rows(const mgg_store* cs, float* host_rw, const float* host_ro,
                                      cudaMemcpyDeviceToHost, st));
         continue;
       }
-      // dense host rows, padded device rows: 1D DMA through a staging slab
-      if (!s->stage[p]) MGG_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->stage[p]), kStageBytes));
+      // dense host rows, padded device rows: 1D DMA through two staging
+      // slabs; the re-pitch kernels run on the device's rp stream so the
+      // copy of chunk i+1 proceeds while chunk i is re-pitched
+      float** slab = &s->stage[2 * p];
+      cudaEvent_t* ev = &s->stage_ev[5 * p];  // full0 full1 free0 free1 tail
+      if (!slab[0]) {
+        for (int i = 0; i < 2; ++i) {
+          MGG_CUDA(cudaMalloc(reinterpret_cast<void**>(&slab[i]), kStageBytes));
+          MGG_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+          MGG_CUDA(cudaEventCreateWithFlags(&ev[2 + i], cudaEventDisableTiming));
+        }
+        MGG_CUDA(cudaEventCreateWithFlags(&ev[4], cudaEventDisableTiming));
+      }
+      cudaStream_t rs = ctx->rp[p];
+      // the re-pitch stream starts after whatever the lane was ordered behind
+      MGG_CUDA(cudaEventRecord(ev[4], st));
+      MGG_CUDA(cudaStreamWaitEvent(rs, ev[4], 0));
       const uint64_t chunk = std::max<uint64_t>(1, kStageBytes / row_bytes);
-      for (uint64_t r = a; r < b; r += chunk) {
+      int i = 0;
+      for (uint64_t r = a; r < b; r += chunk, i ^= 1) {
         const uint64_t n = std::min(chunk, b - r);
         float* d = s->shard[p] + (r - s->lb[p]) * s->pitch;
         const size_t h = (r - row_begin) * (size_t)ld;
         if (up) {
-          MGG_CUDA(cudaMemcpyAsync(s->stage[p], host_ro + h, n * row_bytes, cudaMemcpyHostToDevice, st));
-          repitch(s->stage[p], s->dim, d, s->pitch, n, s->dim, st);
+          MGG_CUDA(cudaStreamWaitEvent(st, ev[2 + i], 0));  // slab drained
+          MGG_CUDA(cudaMemcpyAsync(slab[i], host_ro + h, n * row_bytes, cudaMemcpyHostToDevice, st));
+          MGG_CUDA(cudaEventRecord(ev[i], st));
+          MGG_CUDA(cudaStreamWaitEvent(rs, ev[i], 0));
+          repitch(slab[i], s->dim, d, s->pitch, n, s->dim, rs);
+          MGG_CUDA(cudaEventRecord(ev[2 + i], rs));
         } else {
-          repitch(d, s->pitch, s->stage[p], s->dim, n, s->dim, st);
-          MGG_CUDA(cudaMemcpyAsync(host_rw + h, s->stage[p], n * row_bytes, cudaMemcpyDeviceToHost, st));
+          MGG_CUDA(cudaStreamWaitEvent(rs, ev[2 + i], 0));  // slab copied out
+          repitch(d, s->pitch, slab[i], s->dim, n, s->dim, rs);
+          MGG_CUDA(cudaEventRecord(ev[i], rs));
+          MGG_CUDA(cudaStreamWaitEvent(st, ev[i], 0));
+          MGG_CUDA(cudaMemcpyAsync(host_rw + h, slab[i], n * row_bytes, cudaMemcpyDeviceToHost, st));
+          MGG_CUDA(cudaEventRecord(ev[2 + i], st));
         }
+      }
+      if (up) {  // the lane completes only when the last re-pitch has
+        MGG_CUDA(cudaEventRecord(ev[4], rs));
+        MGG_CUDA(cudaStreamWaitEvent(st, ev[4], 0));
       }
     }
   });

@@ -50,6 +50,7 @@ Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
     build_plans();
   } catch (...) {
     free_plans();
+    mgg_store_destroy(in_bufs_[1]);
     for (auto* s : stores_) mgg_store_destroy(s);
     for (auto& slot : weights_)
       for (auto* b : slot) mgg_dbuf_destroy(b);
@@ -62,6 +63,8 @@ Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
 Engine::~Engine() {
   if (ctx_) mgg_ctx_synchronize(ctx_);
   free_plans();
+  for (auto* s : in_bufs_)  // the one not currently installed as the input
+    if (s && s != stores_[input_]) mgg_store_destroy(s);
   for (auto* s : stores_) mgg_store_destroy(s);
   for (auto* s : scratch_) mgg_store_destroy(s);
   for (auto& slot : weights_)
@@ -367,8 +370,17 @@ void Engine::forward_ops(bool streamed) {
       fence_all(MGG_LANE_D2H, MGG_LANE_COMPUTE);  // previous z has left the device
     run(program_[i]);
     if (profiling_) ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
-    if (streamed && static_cast<int>(i) == in_last_use_)
-      fence_all(MGG_LANE_COMPUTE, MGG_LANE_H2D);  // next x may overwrite the input
+    if (streamed && static_cast<int>(i) == in_last_use_) {
+      if (in_bufs_[1]) {  // this buffer is free for the submission after next
+        const int b = stores_[input_] == in_bufs_[0] ? 0 : 1;
+        for (std::uint32_t p = 0; p < num_parts_; ++p)
+          if (dev_[p] >= 0)
+            ok(mgg_lane_mark(ctx_, p, MGG_LANE_COMPUTE, static_cast<std::uint32_t>(kMarkSlots + b)));
+        in_marked_[b] = true;
+      } else {
+        fence_all(MGG_LANE_COMPUTE, MGG_LANE_H2D);  // next x may overwrite the input
+      }
+    }
   }
 }
 
@@ -387,6 +399,8 @@ void Engine::find_io_points() {
     if (out_first_write_ < 0 && (op.out == output_ || op.out2 == output_))
       out_first_write_ = static_cast<int>(i);
   }
+  bool any_gather = false;
+  for (const Op& op : program_) any_gather |= op.kind == OpKind::aggregate && op.in == input_;
   if (peer_read) {
     // peers gather the input too: it is free once every part has passed the
     // next K3 barrier (each part reaches it only after its own gathers)
@@ -394,11 +408,28 @@ void Engine::find_io_points() {
     while (j < static_cast<int>(program_.size()) && program_[j].kind != OpKind::barrier) ++j;
     in_last_use_ = std::min(j, static_cast<int>(program_.size()) - 1);
   }
+  if (!any_gather) {
+    // the input is read only by this part's own GEMM: a second buffer lets
+    // the next H2D run while the current forward still reads the first
+    in_bufs_[0] = stores_[input_];
+    std::vector<std::uint64_t> lb(num_parts_ + 1);
+    for (std::uint32_t p = 0; p < num_parts_; ++p) lb[p] = ne_.ranges[p].lb;
+    lb[num_parts_] = g_.num_nodes;
+    ok(mgg_store_create(ctx_, lb.data(), spec_.in_dim, &in_bufs_[1]));
+  }
 }
 
 std::uint64_t Engine::submit_host(const float* x, float* z) {
   if (submitted_ - completed_ >= kMaxInFlight) wait(submitted_ - kMaxInFlight + 1);
   const std::uint64_t ticket = ++submitted_;
+  if (in_bufs_[1]) {
+    const int b = static_cast<int>(ticket & 1);
+    stores_[input_] = in_bufs_[b];
+    if (in_marked_[b])  // the forward that last read this buffer is done with it
+      for (std::uint32_t p = 0; p < num_parts_; ++p)
+        if (dev_[p] >= 0)
+          ok(mgg_lane_wait_mark(ctx_, p, MGG_LANE_H2D, static_cast<std::uint32_t>(kMarkSlots + b)));
+  }
   ok(mgg_store_upload_on(stores_[input_], x, 0, g_.num_nodes, spec_.in_dim, MGG_LANE_H2D));
   for (std::uint32_t p = 0; p < num_parts_; ++p)
     if (dev_[p] >= 0) ok(mgg_lane_fence(ctx_, p, MGG_LANE_H2D, MGG_LANE_COMPUTE));
