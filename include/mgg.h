@@ -175,6 +175,28 @@ typedef struct {
 int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
                   mgg_store* out, const mgg_agg_opts* opts);
 
+/* Device event trace of K1 — the reference's per-warp trace
+ * (TraceEvent, R:proj/include/pipeshard/sim.hpp:71; CSV
+ * R:proj/src/sim.cpp:626-635) recorded by the real kernel: per logical warp
+ * and pair, LR (remote get: issue -> staged rows landed), LL (local
+ * partition load + reduce) and AC (accumulate of the remote partition)
+ * begin/end stamps from %globaltimer, plus the SM id. Only logical warps
+ * < warp_limit record; at most `capacity` events are kept. */
+typedef struct mgg_trace mgg_trace;
+int mgg_trace_create(mgg_ctx* ctx, uint32_t part, uint64_t capacity, uint32_t warp_limit,
+                     mgg_trace** out);
+int mgg_trace_destroy(mgg_trace* t);
+/* One traced K1 launch (always the fine-grained pipelined kernel; no
+ * ReLU-on-load; rows <= 128 floats). Same result as mgg_aggregate. */
+int mgg_aggregate_traced(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
+                         mgg_store* out, const mgg_agg_opts* opts, mgg_trace* trace);
+/* Waits for the part's stream, then copies up to `cap` events as 4 x u64
+ * {cycle, sm, warp, stage*2 + begin} (stage 0 LR, 1 LL, 2 AC; cycle = SM
+ * clocks since the earliest recorded event). *n = events returned,
+ * *emitted = events the kernel tried to record (> capacity: truncated). */
+int mgg_trace_read(mgg_trace* t, uint64_t* events, uint64_t cap, uint64_t* n,
+                   uint64_t* emitted);
+
 /* Deduplicated remote fetch: copy the plan's distinct remote rows of `in`
  * from the peer shards (NVLink) into `halo` (halo_len x pitch floats, device
  * memory of the plan's part), one coalesced pass; the next mgg_aggregate
@@ -408,6 +430,13 @@ int mgg_engine_aggregate_host(mgg_engine* e, const float* x, uint32_t dim,
  * config, max over local parts — the tuner's SimulateFn. */
 int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps,
                               int phase, uint64_t* median_ns);
+/* Device event trace of one K1 launch at width `dim` on every local part
+ * (mgg_aggregate_traced), as the reference's multi-GPU trace CSV
+ * (R:proj/tools/cli.cpp:144-155): "gpu,cycle,sm,warp,stage,event" rows,
+ * stage LR/LL/AC, event begin/end, per part sorted by cycle. Free with
+ * mgg_free. */
+int mgg_engine_trace_csv(mgg_engine* e, uint32_t dim, uint64_t capacity, uint32_t warp_limit,
+                         char** csv);
 /* stats[10] = {local_parts_total, remote_parts_total, local_edges,
  * remote_edges, num_warps, num_blocks, kernel_launches, plan_build_ns,
  * halo_rows, halo_parts} */

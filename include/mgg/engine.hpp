@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mgg/costmodel.hpp"
@@ -88,6 +89,9 @@ class Engine {
                       bool relu_in, float* out);
   /// Median K1 ns at width `dim`, max over local parts (tuner SimulateFn).
   std::uint64_t time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase);
+  /// Device event trace of one K1 at width `dim` on every local part, in the
+  /// reference's multi-GPU trace CSV schema (R:proj/tools/cli.cpp:144-155).
+  std::string trace_csv(std::uint32_t dim, std::uint64_t capacity, std::uint32_t warp_limit);
 
   /// Per-op device timing (CUDA events on the first local part's stream).
   void set_profiling(bool on);
@@ -133,6 +137,7 @@ class Engine {
   mgg_store* in_bufs_[2] = {nullptr, nullptr};
   bool in_marked_[2] = {false, false};
   mgg_store* scratch(std::uint32_t dim, int slot);
+  std::pair<mgg_store*, mgg_store*> agg_stores(std::uint32_t dim);
   /// Halo buffer of part p for gather width `dim` (null when p reads fine).
   const float* halo_for(std::uint32_t p, std::uint32_t dim);
   RemoteFetch fetch_ = RemoteFetch::automatic;

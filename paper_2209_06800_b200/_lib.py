@@ -158,6 +158,11 @@ _sig("mgg_engine_get_hidden", I, vp, U32, f32p, u32p)
 _sig("mgg_engine_aggregate_host", I, vp, f32p, U32, C.c_float, I, f32p)
 _sig("mgg_engine_time_aggregate", I, vp, U32, U32, I, u64p)
 _sig("mgg_engine_stats", I, vp, u64p)
+_sig("mgg_engine_trace_csv", I, vp, U32, U64, U32, C.POINTER(C.c_void_p))
+_sig("mgg_trace_create", I, vp, U32, U64, U32, PP)
+_sig("mgg_trace_destroy", I, vp)
+_sig("mgg_aggregate_traced", I, vp, vp, vp, vp, C.POINTER(AggOpts), vp)
+_sig("mgg_trace_read", I, vp, u64p, U64, u64p, u64p)
 _sig("mgg_engine_ctx", vp, vp)
 _sig("mgg_engine_set_profiling", I, vp, I)
 _sig("mgg_engine_profile", I, vp, C.POINTER(C.c_double), u32p, u32p, SZ, C.POINTER(SZ), u64p)

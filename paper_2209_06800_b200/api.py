@@ -481,6 +481,16 @@ class Engine:
         check(lib.mgg_engine_time_aggregate(self._h, dim, reps, phase, C.byref(ns)))
         return ns.value
 
+    def trace_csv(self, dim: int, capacity: int = 1 << 20, warp_limit: int = 0xFFFFFFFF) -> str:
+        """Device event trace of one K1 at width `dim` (mgg_engine_trace_csv):
+        the reference's "gpu,cycle,sm,warp,stage,event" CSV."""
+        out = C.c_void_p()
+        check(lib.mgg_engine_trace_csv(self._h, dim, capacity, warp_limit, C.byref(out)))
+        try:
+            return C.string_at(out.value).decode()
+        finally:
+            lib.mgg_free(out)
+
     def set_profiling(self, on: bool) -> None:
         check(lib.mgg_engine_set_profiling(self._h, int(on)))
 

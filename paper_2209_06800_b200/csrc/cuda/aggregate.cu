@@ -61,6 +61,11 @@ struct AggArgs {
   uint32_t num_owners;
   int phase;                  // 0 all, 1 local only, 2 remote only
   const float* halo;          // deduplicated remote rows (halo mode) or null
+  // device event trace (traced launches only): 16-B records
+  // {globaltimer lo, hi, (smid << 8) | (stage << 1) | begin, logical warp}
+  uint4* trace;
+  unsigned long long* trace_n;
+  uint32_t trace_cap, trace_warps;  // capacity; only warps < trace_warps record
 };
 
 constexpr uint32_t kShift = 28;
@@ -95,6 +100,31 @@ __device__ __forceinline__ void red_add4(float* p, float4 v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
+// Stage codes of the reference's TraceEvent (R:proj/include/pipeshard/sim.hpp:71,
+// names R:proj/src/sim.cpp:627): LR remote get, LL local load, AC accumulate.
+enum : uint32_t { kLR = 0, kLL = 1, kAC = 2 };
+
+// Global-timer stamp ordered after `dep` is available (a fake operand: the
+// read cannot issue before the loads feeding `dep` have landed).
+__device__ __forceinline__ uint64_t stamp_after(float dep) {
+  uint64_t t;
+  asm volatile("{\n\t.reg .f32 d;\n\tmov.f32 d, %1;\n\tmov.u64 %0, %%globaltimer;\n\t}"
+               : "=l"(t)
+               : "f"(dep)
+               : "memory");
+  return t;
+}
+__device__ __forceinline__ void trace_emit(const AggArgs& a, uint32_t w, uint32_t stage,
+                                           bool begin, uint64_t t) {
+  if ((threadIdx.x & 31) != 0 || w >= a.trace_warps) return;
+  const unsigned long long i = atomicAdd(a.trace_n, 1ull);
+  if (i >= a.trace_cap) return;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  a.trace[i] = make_uint4(static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
+                          (sm << 8) | (stage << 1) | (begin ? 1u : 0u), w);
+}
+
 __device__ __forceinline__ const float* shfl_ptr(const float* p, int src) {
   const unsigned long long v = reinterpret_cast<unsigned long long>(p);
   return reinterpret_cast<const float*>(__shfl_sync(kFull, v, src));
@@ -247,7 +277,7 @@ __device__ __forceinline__ WarpMeta load_warp_meta(const AggArgs& a, uint32_t w,
   return m;
 }
 
-template <int VEC, bool RELU, bool REMOTE, int MINB>
+template <int VEC, bool RELU, bool REMOTE, int MINB, bool TRACE = false>
 __global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
   using L = Lanes<VEC, RELU>;
   const L ln(a);
@@ -289,6 +319,7 @@ __global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
         rend = __shfl_sync(kFull, mr.y, i + 1);
         rn = min(rend - rbeg, 32);
         rwin = load_colwin(a.rcols, rbeg, rn);
+        if (TRACE) trace_emit(a, w, kLR, true, stamp_after(0.f));
 #pragma unroll
         for (int s = 0; s < L::PF; ++s)
           pre[s] = ln.template row<true>(a, rwin, s * L::RPW + ln.sub, rn, tab_lane);
@@ -309,11 +340,13 @@ __global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
           accL = f4zero();
           curL = lt;
         }
+        if (TRACE) trace_emit(a, w, kLL, true, stamp_after(accL.x));
         accL = ln.template window<false>(a, lwin, min(end - beg, 32), 0, accL, nullptr);
         for (int b = beg + 32; b < end; b += 32) {  // whole-list tails
           const int n = min(end - b, 32);
           accL = ln.template window<false>(a, load_colwin(a.lcols, b, n), n, 0, accL, nullptr);
         }
+        if (TRACE) trace_emit(a, w, kLL, false, stamp_after(accL.x));
         lwin = lnext;
       }
       // (3) consume R_i
@@ -323,6 +356,11 @@ __global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
           accR = f4zero();
           curR = rt;
         }
+        if (TRACE) {  // R_i's staged rows have arrived: the get ends, AC starts
+          const uint64_t t = stamp_after(pre[L::PF - 1].x);
+          trace_emit(a, w, kLR, false, t);
+          trace_emit(a, w, kAC, true, t);
+        }
 #pragma unroll
         for (int s = 0; s < L::PF; ++s) accR = f4add(accR, pre[s]);
         accR = ln.template window<true>(a, rwin, rn, L::PF, accR, tab_lane);
@@ -330,6 +368,7 @@ __global__ void __launch_bounds__(512, MINB) agg_kernel(AggArgs a) {
           const int n = min(rend - beg, 32);
           accR = ln.template window<true>(a, load_colwin(a.rcols, beg, n), n, 0, accR, tab_lane);
         }
+        if (TRACE) trace_emit(a, w, kAC, false, stamp_after(accR.x));
       }
     }
   }
@@ -590,9 +629,19 @@ void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st) {
   MGG_CUDA(cudaGetLastError());
 }
 
+KernelFn pick_traced(uint32_t v) {
+  if (v <= 1) return agg_kernel<1, false, true, 1, true>;
+  if (v <= 2) return agg_kernel<2, false, true, 1, true>;
+  if (v <= 4) return agg_kernel<4, false, true, 1, true>;
+  if (v <= 8) return agg_kernel<8, false, true, 1, true>;
+  if (v <= 16) return agg_kernel<16, false, true, 1, true>;
+  if (v <= 32) return agg_kernel<32, false, true, 1, true>;
+  throw Status{MGG_E_CONFIG, "trace: rows wider than 128 floats are not traced"};
+}
+
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                       mgg_store* out, int relu_in, int phase, const float* halo,
-                      cudaStream_t st) {
+                      cudaStream_t st, const TraceSink* trace) {
   AggArgs a{};
   a.lmeta = p->lmeta;
   a.lcols = p->lcols;
@@ -636,6 +685,14 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const bool remote = a.nR > 0 && a.phase != 1;
   KernelFn k = relu_in ? (remote ? pick<true, true>(a.vec) : pick<true, false>(a.vec))
                        : (remote ? pick<false, true>(a.vec) : pick<false, false>(a.vec));
+  if (trace) {  // the pipelined kernel with stage stamps, whatever the plan
+    if (relu_in || halo) throw Status{MGG_E_CONFIG, "trace: fine-grained, no ReLU-on-load"};
+    k = pick_traced(a.vec);
+    a.trace = reinterpret_cast<uint4*>(trace->events);
+    a.trace_n = reinterpret_cast<unsigned long long*>(trace->count);
+    a.trace_cap = trace->capacity;
+    a.trace_warps = trace->warp_limit;
+  }
   const int threads = 32 * static_cast<int>(p->wpb);
   const unsigned grid = std::min<unsigned>(resident_grid(k, threads), a.num_lblocks);
   k<<<grid, threads, 0, st>>>(a);

@@ -70,6 +70,15 @@ struct mgg_dbuf {
   uint32_t tc_k = 0, tc_m = 0;
 };
 
+struct mgg_trace {
+  mgg_ctx* ctx = nullptr;
+  uint32_t part = 0;
+  uint64_t capacity = 0;
+  uint32_t warp_limit = 0;
+  void* events = nullptr;  // capacity x 16 B
+  unsigned long long* count = nullptr;
+};
+
 struct mgg_dplan {
   mgg_ctx* ctx = nullptr;
   uint32_t part = 0;
@@ -92,9 +101,15 @@ cudaStream_t enter(mgg_ctx* ctx, uint32_t part);
 void count_launch(mgg_ctx* ctx, uint64_t n = 1);
 
 // launchers (aggregate.cu / dense.cu)
+// Device event trace of a K1 launch (mgg_trace): 16-B records + counter.
+struct TraceSink {
+  void* events;
+  void* count;
+  uint32_t capacity, warp_limit;
+};
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                       mgg_store* out, int relu_in, int phase, const float* halo,
-                      cudaStream_t st);
+                      cudaStream_t st, const TraceSink* trace = nullptr);
 void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st);
 void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st);
 void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg_store* out,

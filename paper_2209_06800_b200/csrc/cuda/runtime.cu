@@ -693,6 +693,84 @@ int mgg_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
   });
 }
 
+int mgg_trace_create(mgg_ctx* ctx, uint32_t part, uint64_t capacity, uint32_t warp_limit,
+                     mgg_trace** out) {
+  return guard([&] {
+    if (!out) throw Status{MGG_E_INPUT, "trace_create: null argument"};
+    if (capacity == 0 || capacity > 0xffffffffull)
+      throw Status{MGG_E_CONFIG, "trace_create: capacity must be in [1, 2^32)"};
+    enter(ctx, part);
+    auto* t = new mgg_trace();
+    t->ctx = ctx;
+    t->part = part;
+    t->capacity = capacity;
+    t->warp_limit = warp_limit;
+    if (cudaMalloc(&t->events, capacity * 16) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&t->count), 8) != cudaSuccess) {
+      cudaFree(t->events);
+      delete t;
+      throw Status{MGG_E_CUDA, "trace_create: cudaMalloc failed"};
+    }
+    MGG_CUDA(cudaMemset(t->count, 0, 8));
+    *out = t;
+  });
+}
+
+int mgg_trace_destroy(mgg_trace* t) {
+  if (!t) return MGG_OK;
+  cudaSetDevice(t->ctx->device[t->part]);
+  cudaFree(t->events);
+  cudaFree(t->count);
+  delete t;
+  return MGG_OK;
+}
+
+int mgg_aggregate_traced(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
+                         mgg_store* out, const mgg_agg_opts* opts, mgg_trace* trace) {
+  return guard([&] {
+    if (!plan || !in || !out || !trace) throw Status{MGG_E_INPUT, "aggregate_traced: null argument"};
+    if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "aggregate: in/out width differ"};
+    if (trace->part != plan->part) throw Status{MGG_E_INPUT, "aggregate_traced: trace of another part"};
+    cudaStream_t st = enter(ctx, plan->part);
+    MGG_CUDA(cudaMemsetAsync(trace->count, 0, 8, st));
+    TraceSink sink{trace->events, trace->count, static_cast<uint32_t>(trace->capacity),
+                   trace->warp_limit};
+    launch_aggregate(ctx, plan, in, out, opts ? opts->relu_in : 0, opts ? opts->phase : 0,
+                     nullptr, st, &sink);
+  });
+}
+
+int mgg_trace_read(mgg_trace* t, uint64_t* events, uint64_t cap, uint64_t* n,
+                   uint64_t* emitted) {
+  return guard([&] {
+    if (!t || !n) throw Status{MGG_E_INPUT, "trace_read: null argument"};
+    cudaStream_t st = enter(t->ctx, t->part);
+    MGG_CUDA(cudaStreamSynchronize(st));
+    unsigned long long cnt = 0;
+    MGG_CUDA(cudaMemcpy(&cnt, t->count, 8, cudaMemcpyDeviceToHost));
+    const uint64_t have = std::min<uint64_t>(cnt, t->capacity);
+    if (emitted) *emitted = cnt;
+    *n = have;
+    if (!events || !cap) return;
+    const uint64_t m = std::min(have, cap);
+    std::vector<uint32_t> raw(4 * m);
+    if (m) MGG_CUDA(cudaMemcpy(raw.data(), t->events, m * 16, cudaMemcpyDeviceToHost));
+    int clk_khz = 0;
+    MGG_CUDA(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, t->ctx->device[t->part]));
+    uint64_t t0 = ~0ull;
+    for (uint64_t i = 0; i < m; ++i)
+      t0 = std::min(t0, uint64_t(raw[4 * i]) | (uint64_t(raw[4 * i + 1]) << 32));
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint64_t ns = (uint64_t(raw[4 * i]) | (uint64_t(raw[4 * i + 1]) << 32)) - t0;
+      events[4 * i] = static_cast<uint64_t>(double(ns) * clk_khz * 1e-6);  // SM cycles
+      events[4 * i + 1] = raw[4 * i + 2] >> 8;                             // sm
+      events[4 * i + 2] = raw[4 * i + 3];                                  // logical warp
+      events[4 * i + 3] = raw[4 * i + 2] & 0xff;                           // stage*2+begin
+    }
+    *n = m;
+  });
+}
+
 int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, float* halo) {
   return guard([&] {
     if (!plan || !in || !halo) throw Status{MGG_E_INPUT, "halo_pull: null argument"};

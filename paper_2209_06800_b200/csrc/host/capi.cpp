@@ -502,6 +502,13 @@ int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps, int ph
                               uint64_t* ns) {
   return guard([&] { *ns = e->e->time_aggregate(dim, reps, phase); });
 }
+int mgg_engine_trace_csv(mgg_engine* e, uint32_t dim, uint64_t capacity, uint32_t warp_limit,
+                         char** csv) {
+  return guard([&] {
+    if (!csv) throw mgg::InputError("trace_csv: null output");
+    *csv = dup(e->e->trace_csv(dim, capacity, warp_limit));
+  });
+}
 int mgg_engine_stats(const mgg_engine* e, uint64_t* s) {
   return guard([&] {
     const auto st = e->e->stats();

@@ -535,23 +535,20 @@ void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
   synchronize();
 }
 
-std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase) {
-  // Prefer a model store pair of that width (valid across processes).
-  mgg_store *in = nullptr, *out = nullptr;
+// A model store pair of width `dim` (valid across processes: peers imported
+// them), else the scratch pair (single-process only).
+std::pair<mgg_store*, mgg_store*> Engine::agg_stores(std::uint32_t dim) {
   for (const Op& op : program_)
     if (op.kind == OpKind::aggregate) {
       std::uint32_t w = 0;
       ok(mgg_store_info(stores_[op.in], &w, nullptr));
-      if (w == dim) {
-        in = stores_[op.in];
-        out = stores_[op.out];
-        break;
-      }
+      if (w == dim) return {stores_[op.in], stores_[op.out]};
     }
-  if (!in) {
-    in = scratch(dim, 0);
-    out = scratch(dim, 1);
-  }
+  return {scratch(dim, 0), scratch(dim, 1)};
+}
+
+std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase) {
+  auto [in, out] = agg_stores(dim);
   std::uint64_t worst = 0;
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
     if (dev_[p] < 0) continue;
@@ -562,6 +559,47 @@ std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int 
     worst = std::max(worst, ns);
   }
   return worst;
+}
+
+std::string Engine::trace_csv(std::uint32_t dim, std::uint64_t capacity,
+                              std::uint32_t warp_limit) {
+  static constexpr const char* kStage[] = {"LR", "LL", "AC"};
+  auto [in, out] = agg_stores(dim);
+  std::string csv = "# mgg device trace: K1 width " + std::to_string(dim) + ", ps=" +
+                    std::to_string(cfg_.ps) + " dist=" + std::to_string(cfg_.dist) +
+                    " wpb=" + std::to_string(cfg_.wpb) +
+                    "; cycle = SM clocks since the part's first event\n";
+  csv += "gpu,cycle,sm,warp,stage,event\n";
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    if (dev_[p] < 0) continue;
+    mgg_trace* tr = nullptr;
+    ok(mgg_trace_create(ctx_, p, capacity, warp_limit, &tr));
+    std::vector<std::uint64_t> ev;
+    std::uint64_t n = 0, emitted = 0;
+    try {
+      mgg_agg_opts o{0, 0, nullptr, 0};
+      ok(mgg_aggregate_traced(ctx_, plans_[p], in, out, &o, tr));
+      ok(mgg_trace_read(tr, nullptr, 0, &n, &emitted));
+      ev.resize(4 * n);
+      ok(mgg_trace_read(tr, ev.data(), n, &n, &emitted));
+    } catch (...) {
+      mgg_trace_destroy(tr);
+      throw;
+    }
+    mgg_trace_destroy(tr);
+    std::vector<std::uint64_t> order(n);
+    for (std::uint64_t i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](std::uint64_t a, std::uint64_t b) { return ev[4 * a] < ev[4 * b]; });
+    for (std::uint64_t i : order) {
+      const std::uint64_t code = ev[4 * i + 3];
+      csv += std::to_string(p) + ',' + std::to_string(ev[4 * i]) + ',' +
+             std::to_string(ev[4 * i + 1]) + ',' + std::to_string(ev[4 * i + 2]) + ',' +
+             kStage[std::min<std::uint64_t>(code >> 1, 2)] + ',' +
+             ((code & 1) ? "begin" : "end") + '\n';
+    }
+  }
+  return csv;
 }
 
 Engine::Stats Engine::stats() const {

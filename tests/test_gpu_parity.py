@@ -324,3 +324,37 @@ def test_full_size_properties(mgg, workload):
     for k, o in outs.items():
         assert_rows_close(o, ref.astype(np.float64), tol=1e-4, what=f"parts/fetch {k}")
     assert_rows_close(lin, 2 * ref.astype(np.float64) - ay, tol=1e-4, what="linearity")
+
+
+@pytest.mark.parametrize("parts,cfg", [(2, (8, 2, 4)), (3, (32, 4, 2)), (1, (16, 1, 4))])
+def test_device_trace_schema_and_counts(mgg, parts, cfg):
+    # the reference's multi-GPU trace CSV (R:proj/tools/cli.cpp:144-155) from
+    # the real kernel: every local partition yields one LL begin/end pair,
+    # every remote partition one LR and one AC pair, on the warp that owns it
+    g = mgg.gen_rmat(3000, 40000, seed=17)
+    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(16, 8, 4), *cfg)
+    csv = eng.trace_csv(16)
+    lines = csv.strip().split("\n")
+    assert lines[0].startswith("#")
+    assert lines[1] == "gpu,cycle,sm,warp,stage,event"
+    from collections import Counter
+    cnt = Counter()
+    last = {}
+    for ln in lines[2:]:
+        gpu, cyc, sm, warp, stage, ev = ln.split(",")
+        assert stage in ("LR", "LL", "AC") and ev in ("begin", "end")
+        assert 0 <= int(sm) < 1000
+        cyc = int(cyc)
+        assert cyc >= last.get(gpu, 0), "rows sorted by cycle within a gpu"
+        last[gpu] = cyc
+        cnt[(int(gpu), stage, ev)] += 1
+    for p in range(parts):
+        fp = mgg.build_flat_plan(g, parts, p, *cfg, 16)
+        nl, nr = fp.n_local, fp.n_remote
+        assert cnt[(p, "LL", "begin")] == cnt[(p, "LL", "end")] == nl
+        assert cnt[(p, "LR", "begin")] == cnt[(p, "LR", "end")] == nr
+        assert cnt[(p, "AC", "begin")] == cnt[(p, "AC", "end")] == nr
+    # capacity bound: truncation keeps the schema
+    short = eng.trace_csv(16, capacity=10).strip().split("\n")
+    assert len(short) - 2 <= 10 * parts
+    eng.close()
