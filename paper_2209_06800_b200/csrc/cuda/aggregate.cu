@@ -35,6 +35,21 @@
 
 #include "common.cuh"
 
+// Row-load flavour (A/B builds): 0 __ldg, 1 L1::no_allocate, 2 .cg (L2
+// only), 3 L1::evict_first. Measured (profiles/r01_k1_experiments.md): .cg
+// equals __ldg on L2-resident tables and is 3.6% faster on the HBM-resident
+// GIN table; the L1 qualifiers are 30-40% slower.
+#ifndef MGG_LD_MODE
+#define MGG_LD_MODE 2
+#endif
+#if MGG_LD_MODE == 1
+#define MGG_LD_INSN "ld.global.nc.L1::no_allocate.v4.f32"
+#elif MGG_LD_MODE == 2
+#define MGG_LD_INSN "ld.global.cg.v4.f32"
+#elif MGG_LD_MODE == 3
+#define MGG_LD_INSN "ld.global.nc.L1::evict_first.v4.f32"
+#endif
+
 #ifndef MGG_AGG_UNROLL
 #define MGG_AGG_UNROLL 4
 #endif
@@ -188,7 +203,16 @@ struct Lanes {
   // `off` is a row offset: device-side local columns carry no owner bits
   // (stripped at plan upload), remote columns are masked by the caller.
   __device__ __forceinline__ float4 load(const char* base, uint32_t off) const {
-    float4 x = __ldg(reinterpret_cast<const float4*>(base + static_cast<size_t>(off) * pb));
+    const char* p = base + static_cast<size_t>(off) * pb;
+#if MGG_LD_MODE == 0
+    float4 x = __ldg(reinterpret_cast<const float4*>(p));
+#else
+    float4 x;
+    // non-volatile: the compiler may still batch these ahead of their uses
+    asm(MGG_LD_INSN " {%0,%1,%2,%3}, [%4];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(p));
+#endif
     if (RELU) x = f4relu(x);
     return x;
   }
