@@ -174,13 +174,13 @@ def agg_bytes(edges: int, parts: int, rows: int, dim: int) -> int:
     return edges * (4 * pitch + 4) + 8 * parts + 2 * rows * 4 * pitch
 
 
-def _traffic(args):
+def _traffic(args, parts):
     """DRAM bytes per K1 launch from the committed ncu capture of this config."""
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
             for t in json.load(f):
                 if t.get("workload") == args.workload and t.get("config") == [
-                        args.ps, args.dist, args.wpb]:
+                        args.ps, args.dist, args.wpb] and t.get("parts", 1) == parts:
                     return t["dram_bytes_per_launch"]
     except Exception:  # noqa: BLE001
         pass
@@ -418,7 +418,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": f"K1 aggregation, width {w0}",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": _traffic(args),
+                         "traffic": _traffic(args, n),
                          "algorithmic_bytes_per_launch": algo,
                          "avg_launch_ms": round(agg_ms_per_launch, 4),
                          "share_of_step": round(share, 4), "peak_source": peak_kind,

@@ -111,8 +111,9 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+// 16 accumulator columns of this warp's 32 TMEM lanes; no wait (callers
+// batch several loads behind one tmem_wait).
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
       "%14,%15}, [%16];"
@@ -120,9 +121,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 #ifndef MGG_TC_WRITE_HI
@@ -134,12 +135,15 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
+// Accumulator = [Xh·Wh + Xl·Wh | Xh·Wl]: 2·NP fp32 columns, so Xh feeds one
+// N=2NP MMA against [Wh; Wl] and is read from smem once per k-step; the
+// epilogue adds the halves. (Accumulating all three products into one NP-wide
+// accumulator measured no faster and loses low-order bits of the small terms
+// against the large one: softmax error crossed 1e-4.)
 template <int NP>
 __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
                    const __grid_constant__ CUtensorMap map_w, TcArgs a) {
-  // Accumulator = [Xh·Wh + Xl·Wh | Xh·Wl]: 2·NP fp32 columns, so Xh feeds one
-  // N=2NP MMA against [Wh; Wl] and is read from smem once per k-step.
   constexpr uint32_t kAccCols = 2 * NP;
   constexpr uint32_t kTmemCols = (2 * kAccCols <= 32) ? 32 : (2 * kAccCols <= 64) ? 64
                                  : (2 * kAccCols <= 128) ? 128 : (2 * kAccCols <= 256) ? 256 : 512;
@@ -301,14 +305,19 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       float y[NP];
+      {
+        uint32_t r[NP];
+        const uint32_t ta = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16);
 #pragma unroll
-      for (int c = 0; c < NP; c += 16) {
-        float y2[16];
-        const uint32_t ta = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16) + c;
-        tmem_ld16(ta, y + c);
-        tmem_ld16(ta + NP, y2);
+        for (int c = 0; c < NP; c += 16) tmem_ld16_nowait(ta + c, r + c);
+        tmem_wait();
 #pragma unroll
-        for (int q = 0; q < 16; ++q) y[c + q] += y2[q];
+        for (int c = 0; c < NP; ++c) y[c] = __uint_as_float(r[c]);
+#pragma unroll
+        for (int c = 0; c < NP; c += 16) tmem_ld16_nowait(ta + NP + c, r + c);
+        tmem_wait();
+#pragma unroll
+        for (int c = 0; c < NP; ++c) y[c] += __uint_as_float(r[c]);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -446,7 +455,8 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   if (smem > 227 * 1024) throw Status{MGG_E_CONFIG, "gemm_tc: W too large for smem"};
   const CUtensorMap mx = make_map(in, a.k, a.rows, size_t(in_pitch) * 4, BK, BM);
   const CUtensorMap mw = make_map(wt, kpad, 2 * NP, size_t(kpad) * 4, BK, NP);
-  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   int dev = 0, sms = 0;
   MGG_CUDA(cudaGetDevice(&dev));
