@@ -63,6 +63,14 @@ WORKLOADS = {
                      ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 16, 4)),
     "orkut-gcn": ("GCN-2L com-Orkut-shaped (BASELINE configs[3])",
                   ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 4)),
+    # locality-bearing (skewed, ids not shuffled) variants of the same shapes
+    # (report both an id-random and an RMAT variant per graph)
+    "reddit-rmat-gcn": ("GCN-2L Reddit-shaped RMAT variant",
+                        ("rmat", 232_965, 114_615_892), ("gcn", 602, 16, 41, 2), (32, 16, 2)),
+    "products-rmat-gin": ("GIN-5L hidden 64 ogbn-products-shaped RMAT variant",
+                          ("rmat", 2_449_029, 61_859_140), ("gin", 100, 64, 47, 5), (16, 16, 4)),
+    "orkut-rmat-gcn": ("GCN-2L com-Orkut-shaped RMAT variant",
+                       ("rmat", 3_072_441, 117_185_083), ("gcn", 128, 16, 32, 2), (32, 16, 4)),
 }
 
 
