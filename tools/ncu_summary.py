@@ -14,6 +14,9 @@ SECTIONS = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Comput
             "Scheduler Statistics", "Warp State Statistics", "Occupancy", "Launch Statistics")
 RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
        "lts__t_bytes.sum", "l1tex__t_bytes.sum", "sm__pipe_tensor_cycles_active",
+       "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+       "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+       "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
        "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_wait",
        "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
@@ -45,7 +48,7 @@ def report(path):
         hdr, unit = raw[0], raw[1]
         for row in raw[2:]:
             for i, n in enumerate(hdr):
-                if n in RAW or (n.startswith("smsp__pcsamp") and n in RAW):
+                if n in RAW or any(n.endswith("." + r) for r in RAW):
                     print(f"  {n:60s} {unit[i]:>10s} {row[i]}")
 
 
