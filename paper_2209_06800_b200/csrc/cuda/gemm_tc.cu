@@ -339,7 +339,11 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
                           c + 2 < (int)a.m ? y[c + 2] * scale : 0.f,
                           c + 3 < (int)a.m ? y[c + 3] * scale : 0.f);
         __syncwarp();
-        for (int i = lane; i < 32 * kF4; i += 32) {
+        // fixed trip count, unrolled by 4: four smem reads issue before the
+        // first global store needs its data (full unroll spills at NP=48)
+#pragma unroll 4
+        for (int j = 0; j < kF4; ++j) {
+          const int i = lane + 32 * j;
           const int r = i / kF4, c4 = i % kF4;
           if (r < nrows && c4 < out_f4)
             *reinterpret_cast<float4*>(dst + (row0 + r) * a.out_pitch + 4 * c4) =
