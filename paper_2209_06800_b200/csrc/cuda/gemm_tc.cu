@@ -86,6 +86,25 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
       "l"(map), "r"(su32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// Bulk tensor store smem -> global (the epilogue): 32 rows x 128 B,
+// 128-B swizzled, clipped by the tensor map at the tensor edges.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x,
+                                             int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+      "r"(su32(src)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // UMMA shared-memory descriptor, K-major, 128-B swizzle: rows of 128 B,
 // 8-row core groups 1024 B apart (SBO), LBO unused (1), version 1.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
@@ -140,10 +159,20 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // epilogue adds the halves. (Accumulating all three products into one NP-wide
 // accumulator measured no faster and loses low-order bits of the small terms
 // against the large one: softmax error crossed 1e-4.)
+// Epilogue staging per warp: NB column blocks of 32 rows x 128 B (one TMA
+// store box each), 128-B swizzled so the row-per-lane float4 writes are
+// bank-conflict free.
+template <int NP>
+constexpr int kStoreBlocks = (NP + 31) / 32;
+template <int NP>
+constexpr uint32_t kEpBytes = kEpiGroups<NP> * 4 * kStoreBlocks<NP> * 4096;
+
 template <int NP>
 __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
-                   const __grid_constant__ CUtensorMap map_w, TcArgs a) {
+                   const __grid_constant__ CUtensorMap map_w,
+                   const __grid_constant__ CUtensorMap map_out,
+                   const __grid_constant__ CUtensorMap map_out2, TcArgs a) {
   constexpr uint32_t kAccCols = 2 * NP;
   constexpr uint32_t kTmemCols = (2 * kAccCols <= 32) ? 32 : (2 * kAccCols <= 64) ? 64
                                  : (2 * kAccCols <= 128) ? 128 : (2 * kAccCols <= 256) ? 256 : 512;
@@ -159,9 +188,8 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   uint8_t* w_s = smem;                          // [kb][hi|lo][NP][128 B]
   uint8_t* x_s = smem + wbytes;                 // [stage][16 KB] raw X -> Xh in place
   uint8_t* lo_s = x_s + a.stages * kTileBytes;  // [kLoSlots][16 KB] Xl
-  constexpr uint32_t kEpLd = NP + 4;  // padded row (floats): conflict-free float4 rows
-  float* ep_s = reinterpret_cast<float*>(lo_s + kLoSlots * kTileBytes);  // [groups][128][kEpLd]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpiGroups<NP> * BM * kEpLd);
+  uint8_t* ep_s = lo_s + kLoSlots * kTileBytes;  // [groups][4 warps][NB][4 KB], 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpBytes<NP>);
   uint64_t* full = bars;
   uint64_t* split = bars + a.stages;
   uint64_t* empty = bars + 2 * a.stages;
@@ -321,35 +349,31 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      // Each thread holds its row; stage the warp's 32 rows in padded smem and
-      // store them cooperatively (consecutive lanes -> consecutive float4 of a
-      // row: coalesced, full sectors) instead of 32 scattered row writes.
-      float* ep = ep_s + (eg * BM + 32 * g) * kEpLd;
-      const uint64_t row0 = static_cast<uint64_t>(t) * BM + 32 * g;
-      const uint64_t left = a.rows > row0 ? a.rows - row0 : 0;
-      const int nrows = left < 32 ? static_cast<int>(left) : 32;
-      constexpr int kF4 = NP / 4;  // float4 per staged row
-      const int out_f4 = static_cast<int>(a.out_pitch / 4);
-      auto stage_and_store = [&](float* dst, float scale) {
+      // Each thread holds its row: write it into the warp's swizzled staging
+      // blocks, then one lane hands the 32 x NP tile to the TMA engine (bulk
+      // tensor store, clipped at the last row / the pitch) — no per-lane
+      // global stores, no smem read-back by the warp.
+      uint8_t* ep = ep_s + ((eg * 4 + g) * kStoreBlocks<NP>) * 4096;
+      const int row0 = static_cast<int>(t * BM + 32 * g);
+      auto stage_and_store = [&](const CUtensorMap* map, float scale) {
+        if (lane == 0) bulk_wait_read0();  // the previous store has left the staging
+        __syncwarp();
 #pragma unroll
-        for (int c = 0; c < NP; c += 4)
-          *reinterpret_cast<float4*>(ep + lane * kEpLd + c) =
+        for (int c = 0; c < NP; c += 4) {
+          const int b = c / 32, c4 = (c % 32) / 4;
+          *reinterpret_cast<float4*>(ep + b * 4096 + lane * 128 + ((c4 ^ (lane & 7)) << 4)) =
               make_float4(c + 0 < (int)a.m ? y[c + 0] * scale : 0.f,
                           c + 1 < (int)a.m ? y[c + 1] * scale : 0.f,
                           c + 2 < (int)a.m ? y[c + 2] * scale : 0.f,
                           c + 3 < (int)a.m ? y[c + 3] * scale : 0.f);
-        __syncwarp();
-        // fixed trip count, unrolled by 4: four smem reads issue before the
-        // first global store needs its data (full unroll spills at NP=48)
-#pragma unroll 4
-        for (int j = 0; j < kF4; ++j) {
-          const int i = lane + 32 * j;
-          const int r = i / kF4, c4 = i % kF4;
-          if (r < nrows && c4 < out_f4)
-            *reinterpret_cast<float4*>(dst + (row0 + r) * a.out_pitch + 4 * c4) =
-                *reinterpret_cast<const float4*>(ep + r * kEpLd + 4 * c4);
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int b = 0; b < kStoreBlocks<NP>; ++b) tma_store_2d(map, ep + b * 4096, 32 * b, row0);
+          bulk_commit();
+        }
       };
       if (a.bias) {
 #pragma unroll
@@ -361,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
           y[c + 3] += b4.w;
         }
       }
-      if (a.out2) stage_and_store(a.out2, a.out2_scale);
+      if (a.out2) stage_and_store(&map_out2, a.out2_scale);
       if (a.act == 1) {
 #pragma unroll
         for (int c = 0; c < NP; ++c) y[c] = fmaxf(y[c], 0.f);
@@ -380,8 +404,9 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
 #pragma unroll
         for (int c = 0; c < NP; ++c) y[c] *= inv;
       }
-      stage_and_store(a.out, 1.f);
+      stage_and_store(&map_out, 1.f);
     }
+    if (lane == 0) bulk_wait0();  // stores complete before the CTA's smem goes away
   }
   tc_fence_before();
   __syncthreads();
@@ -444,9 +469,8 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   TcArgs b = a;
   b.stages = kMaxStages;
   auto smem_for = [&](uint32_t stages) {
-    return 1024 + wbytes + (stages + kLoSlots) * kTileBytes +
-           kEpiGroups<NP> * BM * (NP + 4) * 4 + (3 * stages + 5 + kLoSlots) * 8 + 16 +
-           16 + 4 * (NP + a.n_kb * BK);
+    return 1024 + wbytes + (stages + kLoSlots) * kTileBytes + kEpBytes<NP> +
+           (3 * stages + 5 + kLoSlots) * 8 + 16 + 16 + 4 * (NP + a.n_kb * BK);
   };
   static const uint32_t cap_env = [] {
     const char* e = std::getenv("MGG_TC_STAGES");
@@ -459,6 +483,10 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   if (smem > 227 * 1024) throw Status{MGG_E_CONFIG, "gemm_tc: W too large for smem"};
   const CUtensorMap mx = make_map(in, a.k, a.rows, size_t(in_pitch) * 4, BK, BM);
   const CUtensorMap mw = make_map(wt, kpad, 2 * NP, size_t(kpad) * 4, BK, NP);
+  const CUtensorMap mo = make_map(a.out, a.out_pitch, a.rows, size_t(a.out_pitch) * 4, 32, 32);
+  const CUtensorMap mo2 = a.out2 ? make_map(a.out2, a.out_pitch, a.rows,
+                                            size_t(a.out_pitch) * 4, 32, 32)
+                                 : mo;
   MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
@@ -467,7 +495,7 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const uint64_t tiles = (a.rows + BM - 1) / BM;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, sms));
-  gemm_tc_kernel<NP><<<grid, kThreadsFor<NP>, smem, st>>>(mx, mw, b);
+  gemm_tc_kernel<NP><<<grid, kThreadsFor<NP>, smem, st>>>(mx, mw, mo, mo2, b);
   MGG_CUDA(cudaGetLastError());
 }
 
@@ -482,8 +510,8 @@ bool gemm_tc_supported(uint32_t k, uint32_t m) {
   const uint32_t np = (m + 15) / 16 * 16;
   const size_t wbytes = size_t((k + BK - 1) / BK) * 2 * np * 128;
   const size_t kpad = size_t((k + BK - 1) / BK) * BK;
-  return 1024 + wbytes + (2 + kLoSlots) * kTileBytes + 2 * BM * (np + 4) * 4 + 128 + 16 +
-             4 * (np + kpad) <=
+  const size_t ep = size_t(np <= 48 ? 2 : 1) * 4 * ((np + 31) / 32) * 4096;
+  return 1024 + wbytes + (2 + kLoSlots) * kTileBytes + ep + 128 + 16 + 4 * (np + kpad) <=
          227 * 1024;
 }
 
