@@ -118,6 +118,28 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// A operand from TMEM (lanes = rows, 32-bit columns = k): the Xl term.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+// 32 consecutive 32-bit TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
+      "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
+      "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -144,6 +166,14 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 __device__ __forceinline__ void tmem_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+
+// Xl (the low TF32 part of X) staged in TMEM by the split warpgroup and fed
+// to the MMA as a TMEM A operand: no smem write + read of the Xl tile, so the
+// mainloop's smem traffic per X byte drops from ~5.4 to ~3.4 bytes.
+#ifndef MGG_TC_LO_TMEM
+#define MGG_TC_LO_TMEM 1
+#endif
+constexpr bool kLoTmem = MGG_TC_LO_TMEM != 0;
 
 #ifndef MGG_TC_WRITE_HI
 #define MGG_TC_WRITE_HI 0
@@ -174,8 +204,11 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ CUtensorMap map_out2, TcArgs a) {
   constexpr uint32_t kAccCols = 2 * NP;
-  constexpr uint32_t kTmemCols = (2 * kAccCols <= 32) ? 32 : (2 * kAccCols <= 64) ? 64
-                                 : (2 * kAccCols <= 128) ? 128 : (2 * kAccCols <= 256) ? 256 : 512;
+  constexpr uint32_t kLoCol = 2 * kAccCols;  // TMEM Xl slots [kLoCol + BK*l, +BK)
+  constexpr uint32_t kCols = kLoCol + (kLoTmem ? kLoSlots * BK : 0);
+  constexpr uint32_t kTmemCols = (kCols <= 32) ? 32 : (kCols <= 64) ? 64
+                                 : (kCols <= 128) ? 128 : (kCols <= 256) ? 256 : 512;
+  static_assert(kCols <= 512, "TMEM holds 512 columns");
   constexpr uint32_t kIdescBase = (1u << 4) | (2u << 7) | (2u << 10) | ((BM >> 4) << 24);
   constexpr uint32_t kIdesc2 = kIdescBase | (static_cast<uint32_t>((2 * NP) >> 3) << 17);
   constexpr uint32_t kIdesc1 = kIdescBase | (static_cast<uint32_t>(NP >> 3) << 17);
@@ -187,8 +220,8 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   const uint32_t wbytes = a.n_kb * 2 * NP * 128;
   uint8_t* w_s = smem;                          // [kb][hi|lo][NP][128 B]
   uint8_t* x_s = smem + wbytes;                 // [stage][16 KB] raw X -> Xh in place
-  uint8_t* lo_s = x_s + a.stages * kTileBytes;  // [kLoSlots][16 KB] Xl
-  uint8_t* ep_s = lo_s + kLoSlots * kTileBytes;  // [groups][4 warps][NB][4 KB], 1024-aligned
+  uint8_t* lo_s = x_s + a.stages * kTileBytes;  // [kLoSlots][16 KB] Xl (smem variant)
+  uint8_t* ep_s = lo_s + (kLoTmem ? 0 : kLoSlots * kTileBytes);  // [groups][4 warps][NB][4 KB]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpBytes<NP>);
   uint64_t* full = bars;
   uint64_t* split = bars + a.stages;
@@ -268,13 +301,23 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
           mbar_wait(&split[s], ph);
           tc_fence_after();
           const uint64_t xh = umma_desc(su32(x_s + s * kTileBytes));
-          const uint64_t xl = umma_desc(su32(lo_s + l * kTileBytes));
           const uint64_t wh = umma_desc(su32(w_s + kb * 2 * NP * 128));  // [Wh; Wl]
+          if (kLoTmem) {
+            const uint32_t xl = tmem + kLoCol + BK * l;
 #pragma unroll
-          for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B
-            const uint64_t o = 2 * k;
-            mma_tf32(d, xh + o, wh + o, kIdesc2, (kb | k) != 0);  // [Xh·Wh | Xh·Wl]
-            mma_tf32(d, xl + o, wh + o, kIdesc1, 1);              // += Xl·Wh
+            for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B / +8 cols
+              const uint64_t o = 2 * k;
+              mma_tf32(d, xh + o, wh + o, kIdesc2, (kb | k) != 0);  // [Xh·Wh | Xh·Wl]
+              mma_tf32_ts(d, xl + 8 * k, wh + o, kIdesc1, 1);       // += Xl·Wh (A in TMEM)
+            }
+          } else {
+            const uint64_t xl = umma_desc(su32(lo_s + l * kTileBytes));
+#pragma unroll
+            for (uint32_t k = 0; k < BK / 8; ++k) {
+              const uint64_t o = 2 * k;
+              mma_tf32(d, xh + o, wh + o, kIdesc2, (kb | k) != 0);
+              mma_tf32(d, xl + o, wh + o, kIdesc1, 1);
+            }
           }
           mma_commit(&empty[s]);   // X stage free once these MMAs retire
           mma_commit(&lofree[l]);  // and the Xl slot
@@ -293,6 +336,40 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
         mbar_wait(&full[s], ph);
         mbar_wait(&lofree[l], ((kcount / kLoSlots) & 1) ^ 1);
         float4* hi = reinterpret_cast<float4*>(x_s + s * kTileBytes);
+        if (kLoTmem) {
+          // thread = tile row = TMEM lane: its 8 (swizzled) float4 chunks in,
+          // Xl out to the lane's 32 columns of slot l
+          const int row = tid;
+          float lov[BK];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int i = row * 8 + (c ^ (row & 7));
+            float4 v = hi[i];
+            if (a.pre) {
+              const uint32_t k0 = kb * BK + c * 4;
+              float* e = &v.x;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float x = e[q];
+                if (a.pre == 2) x += pb_s[k0 + q];
+                e[q] = fmaxf(x, 0.f);
+              }
+            }
+            const float4 h =
+                make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+            if (a.pre || kWriteHi) hi[i] = h;
+            lov[4 * c] = v.x - h.x;
+            lov[4 * c + 1] = v.y - h.y;
+            lov[4 * c + 2] = v.z - h.z;
+            lov[4 * c + 3] = v.w - h.w;
+          }
+          tmem_st32(tmem + kLoCol + BK * l + (static_cast<uint32_t>(32 * (warp % 4)) << 16), lov);
+          tc_fence_before();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&split[s]);
+          if (++s == a.stages) s = 0, ph ^= 1;
+          continue;
+        }
         float4* lo = reinterpret_cast<float4*>(lo_s + l * kTileBytes);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -469,7 +546,7 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   TcArgs b = a;
   b.stages = kMaxStages;
   auto smem_for = [&](uint32_t stages) {
-    return 1024 + wbytes + (stages + kLoSlots) * kTileBytes + kEpBytes<NP> +
+    return 1024 + wbytes + (stages + (kLoTmem ? 0 : kLoSlots)) * kTileBytes + kEpBytes<NP> +
            (3 * stages + 5 + kLoSlots) * 8 + 16 + 16 + 4 * (NP + a.n_kb * BK);
   };
   static const uint32_t cap_env = [] {
