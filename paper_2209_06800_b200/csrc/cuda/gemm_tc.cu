@@ -174,6 +174,12 @@ __device__ __forceinline__ void tmem_wait() {
 #define MGG_TC_LO_TMEM 1
 #endif
 constexpr bool kLoTmem = MGG_TC_LO_TMEM != 0;
+// Xh staged in TMEM too: the MMA reads no X from smem at all, and the split
+// warpgroup (the last reader of the smem stage) releases it to the TMA.
+#ifndef MGG_TC_HI_TMEM
+#define MGG_TC_HI_TMEM 1
+#endif
+constexpr bool kHiTmem = kLoTmem && MGG_TC_HI_TMEM != 0;
 
 #ifndef MGG_TC_WRITE_HI
 #define MGG_TC_WRITE_HI 0
@@ -205,7 +211,8 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
                    const __grid_constant__ CUtensorMap map_out2, TcArgs a) {
   constexpr uint32_t kAccCols = 2 * NP;
   constexpr uint32_t kLoCol = 2 * kAccCols;  // TMEM Xl slots [kLoCol + BK*l, +BK)
-  constexpr uint32_t kCols = kLoCol + (kLoTmem ? kLoSlots * BK : 0);
+  constexpr uint32_t kHiCol = kLoCol + kLoSlots * BK;  // TMEM Xh slots (kHiTmem)
+  constexpr uint32_t kCols = kLoCol + (kLoTmem ? kLoSlots * BK : 0) + (kHiTmem ? kLoSlots * BK : 0);
   constexpr uint32_t kTmemCols = (kCols <= 32) ? 32 : (kCols <= 64) ? 64
                                  : (kCols <= 128) ? 128 : (kCols <= 256) ? 256 : 512;
   static_assert(kCols <= 512, "TMEM holds 512 columns");
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     for (uint32_t s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&split[s], 128);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kHiTmem ? 128 : 1);  // released by the split / the MMA
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -302,7 +309,15 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
           tc_fence_after();
           const uint64_t xh = umma_desc(su32(x_s + s * kTileBytes));
           const uint64_t wh = umma_desc(su32(w_s + kb * 2 * NP * 128));  // [Wh; Wl]
-          if (kLoTmem) {
+          if (kHiTmem) {
+            const uint32_t xlt = tmem + kLoCol + BK * l, xht = tmem + kHiCol + BK * l;
+#pragma unroll
+            for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +8 TMEM cols
+              const uint64_t o = 2 * k;
+              mma_tf32_ts(d, xht + 8 * k, wh + o, kIdesc2, (kb | k) != 0);  // [Xh·Wh | Xh·Wl]
+              mma_tf32_ts(d, xlt + 8 * k, wh + o, kIdesc1, 1);              // += Xl·Wh
+            }
+          } else if (kLoTmem) {
             const uint32_t xl = tmem + kLoCol + BK * l;
 #pragma unroll
             for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B / +8 cols
@@ -319,7 +334,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
               mma_tf32(d, xl + o, wh + o, kIdesc1, 1);
             }
           }
-          mma_commit(&empty[s]);   // X stage free once these MMAs retire
+          if (!kHiTmem) mma_commit(&empty[s]);  // X stage free once these MMAs retire
           mma_commit(&lofree[l]);  // and the Xl slot
           if (++s == a.stages) s = 0, ph ^= 1;
         }
@@ -341,6 +356,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
           // Xl out to the lane's 32 columns of slot l
           const int row = tid;
           float lov[BK];
+          float hiv[kHiTmem ? BK : 1];
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const int i = row * 8 + (c ^ (row & 7));
@@ -357,13 +373,25 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
             }
             const float4 h =
                 make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-            if (a.pre || kWriteHi) hi[i] = h;
+            if (kHiTmem) {
+              hiv[4 * c] = h.x;
+              hiv[4 * c + 1] = h.y;
+              hiv[4 * c + 2] = h.z;
+              hiv[4 * c + 3] = h.w;
+            } else if (a.pre || kWriteHi) {
+              hi[i] = h;
+            }
             lov[4 * c] = v.x - h.x;
             lov[4 * c + 1] = v.y - h.y;
             lov[4 * c + 2] = v.z - h.z;
             lov[4 * c + 3] = v.w - h.w;
           }
-          tmem_st32(tmem + kLoCol + BK * l + (static_cast<uint32_t>(32 * (warp % 4)) << 16), lov);
+          const uint32_t lane_base = static_cast<uint32_t>(32 * (warp % 4)) << 16;
+          tmem_st32(tmem + kLoCol + BK * l + lane_base, lov);
+          if (kHiTmem) {
+            tmem_st32(tmem + kHiCol + BK * l + lane_base, hiv);
+            mbar_arrive(&empty[s]);  // smem stage consumed: back to the TMA
+          }
           tc_fence_before();
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_arrive(&split[s]);
