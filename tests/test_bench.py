@@ -1,0 +1,77 @@
+"""bench.py contract on CPU: the reference arm's JSON line (the only arm that
+runs without a GPU), the algorithmic-byte formula of the roofline, the
+aggregation widths of the layer programs, and the product arm's loud failure
+without a device (no CPU fallback)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_agg_bytes_formula():
+    # E*(4*pitch + 4) + 8*P + 8*rows*pitch, pitch = round4(dim)
+    assert bench.agg_bytes(10, 3, 5, 16) == 10 * (64 + 4) + 24 + 8 * 5 * 16
+    assert bench.agg_bytes(7, 1, 2, 41) == 7 * (4 * 44 + 4) + 8 + 8 * 2 * 44
+    assert bench.agg_bytes(0, 0, 0, 1) == 0
+
+
+def test_agg_widths(mgg):
+    assert bench.agg_widths(mgg.make_gcn(602, 16, 41)) == [16, 16]
+    assert bench.agg_widths(mgg.make_gcn(16, 16, 16)) == [16, 16]
+    assert bench.agg_widths(mgg.make_gcn(8, 32, 4)) == [8, 4]
+    assert bench.agg_widths(mgg.make_gin(100, 64, 47, layers=5)) == [64] * 5
+
+
+def test_workload_table_matches_baseline():
+    # configs[0..3] of BASELINE.json + the RMAT variants; tuned configs valid
+    labels = " ".join(w[0] for w in bench.WORKLOADS.values())
+    for key in ("configs[0]", "configs[1]", "configs[2]", "configs[3]"):
+        assert key in labels
+    for name, (_, g, m, tuned) in bench.WORKLOADS.items():
+        ps, dist, wpb = tuned
+        assert 1 <= ps <= 32 and 1 <= dist <= 16 and 1 <= wpb <= 16, name
+        assert g[0] in ("powerlaw", "rmat") and m[0] in ("gcn", "gin"), name
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+         "--workload", "config1", "--steps", "1", "--warmup", "0"],
+        capture_output=True, text=True, timeout=600, cwd=ROOT,
+        env={**os.environ, "RANK": "0"})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["value"] > 0 and line["unit"] == "GEdges/s"
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+         "--workload", "config1", "--steps", "1", "--warmup", "0"],
+        capture_output=True, text=True, timeout=300, cwd=ROOT,
+        env={**os.environ, "RANK": "1"})
+    assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_product_arm_fails_loudly_without_gpu(mgg):
+    if mgg.cuda_available():
+        pytest.skip("a GPU is visible: the product arm would run")
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "config1", "--steps",
+         "1", "--warmup", "3", "--no-cpu", "--no-e2e"],
+        capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode != 0
+    assert "no CUDA device" in (out.stderr + out.stdout)
