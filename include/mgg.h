@@ -234,6 +234,15 @@ typedef struct {
 } mgg_dense_desc;
 int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
               const mgg_dense_desc* d, mgg_store* out, mgg_store* out2);
+/* Chained Update (the GIN layer boundary, Linear2 -> ReLU -> next Linear1):
+ *   O    = ReLU(pre(in)·W1 + b1)            (m1 columns, kept in TMEM)
+ *   out  = O·W2,  out2 = out2_scale·O·W2    (d2: W2, no bias, pre = 1)
+ * one tcgen05 kernel; O never touches HBM. d1->act must be 0. */
+int mgg_dense_chain(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
+                    const mgg_dense_desc* d1, uint32_t m1, const mgg_dense_desc* d2,
+                    mgg_store* out, mgg_store* out2);
+/* 1 when mgg_dense_chain handles in-width k -> m1 -> m. */
+int mgg_dense_chain_supported(uint32_t k, uint32_t m1, uint32_t m);
 
 /* K3 — cross-GPU layer barrier (R:PAPER.md:258 "result synchronization at
  * the end"; barrier_cycles, R:proj/src/sim.cpp:620): device-side flags in
@@ -446,7 +455,7 @@ mgg_ctx* mgg_engine_ctx(mgg_engine* e);
  * layer program on the first local part's stream; no host sync added). */
 int mgg_engine_set_profiling(mgg_engine* e, int on);
 /* Program size / per-op accumulated ms, op kind (0 dense, 1 init,
- * 2 aggregate, 3 barrier, 4 softmax), op width (output columns) and the
+ * 2 aggregate, 3 barrier, 4 softmax, 5 dense_chain), op width (output columns) and the
  * number of profiled forwards. Arrays hold `cap` entries. */
 int mgg_engine_profile(mgg_engine* e, double* op_ms, uint32_t* op_kind,
                        uint32_t* op_width, size_t cap, size_t* n_ops,

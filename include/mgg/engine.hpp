@@ -97,7 +97,7 @@ class Engine {
   void set_profiling(bool on);
   struct OpProfile {
     double ms = 0;           // accumulated over profiled forwards
-    std::uint32_t kind = 0;  // 0 dense 1 init 2 aggregate 3 barrier 4 softmax
+    std::uint32_t kind = 0;  // 0 dense 1 init 2 aggregate 3 barrier 4 softmax 5 dense_chain
     std::uint32_t width = 0; // output columns
   };
   std::vector<OpProfile> profile(std::uint64_t* forwards);
@@ -110,7 +110,7 @@ class Engine {
   Stats stats() const;
 
  private:
-  enum class OpKind { dense, init, aggregate, barrier, softmax };
+  enum class OpKind { dense, init, aggregate, barrier, softmax, dense_chain };
   struct Op {
     OpKind kind;
     int in = -1, out = -1, out2 = -1;  // store indices
@@ -118,6 +118,8 @@ class Engine {
     std::uint32_t pre = 0, act = 0;
     float scale = 1.f;
     int relu = 0;
+    int w2 = -1;  // dense_chain: second weight (O·W2), O = `mid` store's width
+    int mid = -1;
   };
 
   int add_store(std::uint32_t dim);
@@ -129,6 +131,7 @@ class Engine {
   void run(const Op& op);
   void forward_ops(bool streamed);
   void find_io_points();
+  void fuse_chains();
   static constexpr std::uint64_t kMaxInFlight = 32, kMarkSlots = 64;
   int in_last_use_ = -1, out_first_write_ = -1;
   std::uint64_t submitted_ = 0, completed_ = 0;

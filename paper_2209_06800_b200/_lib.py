@@ -99,6 +99,8 @@ _sig("mgg_rows_init", I, vp, U32, vp, vp, C.c_float, I)
 _sig("mgg_rows_init_copy", I, vp, U32, vp, vp, C.c_float, I, vp)
 _sig("mgg_rows_softmax", I, vp, U32, vp, vp)
 _sig("mgg_dense", I, vp, U32, vp, C.POINTER(DenseDesc), vp, vp)
+_sig("mgg_dense_chain", I, vp, U32, vp, C.POINTER(DenseDesc), U32, C.POINTER(DenseDesc), vp, vp)
+_sig("mgg_dense_chain_supported", I, U32, U32, U32)
 _sig("mgg_barrier", I, vp, vp)
 _sig("mgg_time_aggregate", I, vp, vp, vp, vp, C.POINTER(AggOpts), U32, u64p)
 # --- layer B

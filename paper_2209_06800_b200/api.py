@@ -494,7 +494,7 @@ class Engine:
     def set_profiling(self, on: bool) -> None:
         check(lib.mgg_engine_set_profiling(self._h, int(on)))
 
-    OP_KINDS = ("dense", "init", "aggregate", "barrier", "softmax")
+    OP_KINDS = ("dense", "init", "aggregate", "barrier", "softmax", "dense_chain")
 
     def profile(self):
         """[(kind, width, accumulated ms)] per program op, and #forwards."""

@@ -124,6 +124,12 @@ void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
 void launch_softmax(const float* in, float* out, uint64_t rows, uint32_t pitch,
                     uint32_t m, cudaStream_t st);
 bool gemm_tc_supported(uint32_t k, uint32_t m);
+bool gemm_tc_chain_supported(uint32_t k, uint32_t m1, uint32_t m);
+void launch_dense_tc_chain(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
+                           const float* wt1, const float* bias1, uint32_t m1,
+                           const float* pre_bias, uint32_t pre, const float* wt2,
+                           uint32_t m, float* out, uint32_t out_pitch, float* out2,
+                           float out2_scale, cudaStream_t st);
 const float* gemm_tc_prepare(mgg_dbuf* w, uint32_t k, uint32_t m, cudaStream_t st);
 void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                      const float* wt, const float* bias, const float* pre_bias, uint32_t m,

@@ -52,6 +52,8 @@ struct TcArgs {
   float* out;
   float* out2;
   float out2_scale;
+  const float* bias1;  // CHAIN: bias of the first product (m1 = NP columns)
+  uint32_t m1;
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -167,34 +169,34 @@ __device__ __forceinline__ void tmem_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Xl (the low TF32 part of X) staged in TMEM by the split warpgroup and fed
-// to the MMA as a TMEM A operand: no smem write + read of the Xl tile, so the
-// mainloop's smem traffic per X byte drops from ~5.4 to ~3.4 bytes.
-#ifndef MGG_TC_LO_TMEM
-#define MGG_TC_LO_TMEM 1
-#endif
-constexpr bool kLoTmem = MGG_TC_LO_TMEM != 0;
-// Xh staged in TMEM too: the MMA reads no X from smem at all, and the split
-// warpgroup (the last reader of the smem stage) releases it to the TMA.
-#ifndef MGG_TC_HI_TMEM
-#define MGG_TC_HI_TMEM 1
-#endif
-constexpr bool kHiTmem = kLoTmem && MGG_TC_HI_TMEM != 0;
-
-#ifndef MGG_TC_WRITE_HI
-#define MGG_TC_WRITE_HI 0
-#endif
-constexpr bool kWriteHi = MGG_TC_WRITE_HI != 0;
-
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
-// Accumulator = [Xh·Wh + Xl·Wh | Xh·Wl]: 2·NP fp32 columns, so Xh feeds one
-// N=2NP MMA against [Wh; Wl] and is read from smem once per k-step; the
-// epilogue adds the halves. (Accumulating all three products into one NP-wide
-// accumulator measured no faster and loses low-order bits of the small terms
-// against the large one: softmax error crossed 1e-4.)
+// TMEM column map (NP = padded output width; accumulators are
+// [Xh·Wh + Xl·Wh | Xh·Wl], 2·NP columns, double-buffered):
+//   [0, 4NP)                 accumulators 0 and 1
+//   kXlCol + BK·l, l < 2     Xl k-block slots   } written by the split
+//   kXhCol + BK·l            Xh k-block slots   } warpgroup, read by the MMA
+//   kOlCol / kOhCol          CHAIN: the intermediate O = act1(X·W + b1) split
+//                            into lo/hi, the A operand of the second GEMM
+// Xh and Xl live in TMEM so the MMA reads no X from shared memory (the smem
+// stage is released by the split itself); accumulating all three products
+// into one NP-wide accumulator instead was measured no faster and loses the
+// small terms' low bits (softmax error crossed 1e-4).
+template <int NP, bool CHAIN>
+struct TmemMap {
+  static constexpr uint32_t kAccCols = 2 * NP;
+  static constexpr uint32_t kXlCol = 2 * kAccCols;
+  static constexpr uint32_t kXhCol = kXlCol + kLoSlots * BK;
+  static constexpr uint32_t kOlCol = kXhCol + kLoSlots * BK;  // CHAIN: NP columns each
+  static constexpr uint32_t kOhCol = kOlCol + NP;
+  static constexpr uint32_t kCols = CHAIN ? kOhCol + NP : kOlCol;
+  static constexpr uint32_t kAlloc = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128
+                                     : kCols <= 256 ? 256 : 512;
+  static_assert(kCols <= 512, "TMEM holds 512 columns");
+};
+
 // Epilogue staging per warp: NB column blocks of 32 rows x 128 B (one TMA
 // store box each), 128-B swizzled so the row-per-lane float4 writes are
 // bank-conflict free.
@@ -203,22 +205,24 @@ constexpr int kStoreBlocks = (NP + 31) / 32;
 template <int NP>
 constexpr uint32_t kEpBytes = kEpiGroups<NP> * 4 * kStoreBlocks<NP> * 4096;
 
-template <int NP>
+// out = act(pre(X)·W + b) [+ out2 = out2_scale·(pre(X)·W + b)]; with CHAIN
+// the product goes through a second GEMM first:
+//   O = ReLU(pre(X)·W + b1)          (kept in TMEM, never written)
+//   out = O·W2 (+ out2 = out2_scale·O·W2)
+// — the GIN layer boundary Linear2 -> ReLU -> next layer's Linear1 + seed.
+template <int NP, bool CHAIN>
 __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
                    const __grid_constant__ CUtensorMap map_w,
+                   const __grid_constant__ CUtensorMap map_w2,
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ CUtensorMap map_out2, TcArgs a) {
-  constexpr uint32_t kAccCols = 2 * NP;
-  constexpr uint32_t kLoCol = 2 * kAccCols;  // TMEM Xl slots [kLoCol + BK*l, +BK)
-  constexpr uint32_t kHiCol = kLoCol + kLoSlots * BK;  // TMEM Xh slots (kHiTmem)
-  constexpr uint32_t kCols = kLoCol + (kLoTmem ? kLoSlots * BK : 0) + (kHiTmem ? kLoSlots * BK : 0);
-  constexpr uint32_t kTmemCols = (kCols <= 32) ? 32 : (kCols <= 64) ? 64
-                                 : (kCols <= 128) ? 128 : (kCols <= 256) ? 256 : 512;
-  static_assert(kCols <= 512, "TMEM holds 512 columns");
+  using TM = TmemMap<NP, CHAIN>;
+  constexpr uint32_t kAccCols = TM::kAccCols;
   constexpr uint32_t kIdescBase = (1u << 4) | (2u << 7) | (2u << 10) | ((BM >> 4) << 24);
   constexpr uint32_t kIdesc2 = kIdescBase | (static_cast<uint32_t>((2 * NP) >> 3) << 17);
   constexpr uint32_t kIdesc1 = kIdescBase | (static_cast<uint32_t>(NP >> 3) << 17);
+  constexpr uint32_t kW2Bytes = CHAIN ? (NP / BK) * 2 * NP * 128 : 0;  // W2: K = NP
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle, by offsetting the shared array
   // itself (a round trip through uintptr_t would lose the address space and
@@ -226,25 +230,31 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const uint32_t wbytes = a.n_kb * 2 * NP * 128;
   uint8_t* w_s = smem;                          // [kb][hi|lo][NP][128 B]
-  uint8_t* x_s = smem + wbytes;                 // [stage][16 KB] raw X -> Xh in place
-  uint8_t* lo_s = x_s + a.stages * kTileBytes;  // [kLoSlots][16 KB] Xl (smem variant)
-  uint8_t* ep_s = lo_s + (kLoTmem ? 0 : kLoSlots * kTileBytes);  // [groups][4 warps][NB][4 KB]
+  uint8_t* w2_s = smem + wbytes;                // CHAIN: [NP/BK][hi|lo][NP][128 B]
+  uint8_t* x_s = w2_s + kW2Bytes;               // [stage][16 KB] raw X
+  uint8_t* ep_s = x_s + a.stages * kTileBytes;  // [groups][4 warps][NB][4 KB]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpBytes<NP>);
-  uint64_t* full = bars;
-  uint64_t* split = bars + a.stages;
-  uint64_t* empty = bars + 2 * a.stages;
-  uint64_t* tfull = bars + 3 * a.stages;      // [2]
-  uint64_t* tempty = tfull + 2;               // [2]
-  uint64_t* lofree = tempty + 2;              // [kLoSlots]
-  uint64_t* wfull = lofree + kLoSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
+  uint64_t* full = bars;                        // [stages] TMA -> split
+  uint64_t* split = bars + a.stages;            // [stages] split -> MMA (X slots filled)
+  uint64_t* empty = bars + 2 * a.stages;        // [stages] split -> TMA
+  uint64_t* tfull = bars + 3 * a.stages;        // [2] final accumulator -> epilogue
+  uint64_t* tempty = tfull + 2;                 // [2] epilogue -> MMA
+  uint64_t* lofree = tempty + 2;                // [kLoSlots] MMA -> split (X slots)
+  uint64_t* wfull = lofree + kLoSlots;          // W (and W2) resident
+  uint64_t* t1full = wfull + 1;                 // CHAIN [2]: first product -> split
+  uint64_t* ofull = t1full + 2;                 // CHAIN: O slots filled -> MMA
+  uint64_t* ofree = ofull + 1;                  // CHAIN: O slots consumed -> split
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofree + 1);
   // bias (NP) and pre-bias (n_kb*BK) staged once: the epilogue and split read
   // them as shared-memory broadcasts instead of per-element global loads
-  uint8_t* tail = reinterpret_cast<uint8_t*>(wfull + 2);
+  uint8_t* tail = reinterpret_cast<uint8_t*>(ofree + 2);
   float* bias_s = reinterpret_cast<float*>(tail + ((16u - (su32(tail) & 15u)) & 15u));
   float* pb_s = bias_s + NP;
-  for (uint32_t i = threadIdx.x; i < NP; i += blockDim.x)
+  float* b1_s = pb_s + a.n_kb * BK;  // CHAIN: bias of the first product
+  for (uint32_t i = threadIdx.x; i < NP; i += blockDim.x) {
     bias_s[i] = (a.bias && i < a.m) ? __ldg(a.bias + i) : 0.f;
+    if (CHAIN) b1_s[i] = (a.bias1 && i < a.m1) ? __ldg(a.bias1 + i) : 0.f;
+  }
   if (a.pre == 2)
     for (uint32_t i = threadIdx.x; i < a.n_kb * BK; i += blockDim.x)
       pb_s[i] = i < a.k ? __ldg(a.pre_bias + i) : 0.f;
@@ -256,20 +266,23 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     for (uint32_t s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&split[s], 128);
-      mbar_init(&empty[s], kHiTmem ? 128 : 1);  // released by the split / the MMA
+      mbar_init(&empty[s], 128);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 128);
+      mbar_init(&t1full[i], 1);
     }
     for (uint32_t i = 0; i < kLoSlots; ++i) mbar_init(&lofree[i], 1);
     mbar_init(wfull, 1);
+    mbar_init(ofull, 128);
+    mbar_init(ofree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(kTmemCols));
+                 "r"(TM::kAlloc));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -280,11 +293,16 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
-      mbar_expect_tx(wfull, wbytes);
+      mbar_expect_tx(wfull, wbytes + kW2Bytes);
       for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
         tma_2d(w_s + kb * 2 * NP * 128, &map_w, wfull, kb * BK, 0);
         tma_2d(w_s + kb * 2 * NP * 128 + NP * 128, &map_w, wfull, kb * BK, NP);
       }
+      if (CHAIN)
+        for (uint32_t kb = 0; kb < NP / BK; ++kb) {
+          tma_2d(w2_s + kb * 2 * NP * 128, &map_w2, wfull, kb * BK, 0);
+          tma_2d(w2_s + kb * 2 * NP * 128 + NP * 128, &map_w2, wfull, kb * BK, NP);
+        }
       uint32_t s = 0, ph = 0;
       for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
         for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
@@ -297,7 +315,32 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       mbar_wait(wfull, 0);
-      uint32_t s = 0, ph = 0, it = 0, kcount = 0;
+      uint32_t s = 0, ph = 0, kcount = 0;
+      // [Ah·Wh | Ah·Wl] + Al·Wh over `nk` k-blocks whose A slots are TMEM
+      // columns al/ah + BK·kb
+      auto gemm = [&](uint32_t d, uint32_t al, uint32_t ah, const uint8_t* wsm, uint32_t kb,
+                      bool first) {
+        const uint64_t wh = umma_desc(su32(wsm + kb * 2 * NP * 128));  // [Wh; Wl]
+#pragma unroll
+        for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B / +8 cols
+          const uint64_t o = 2 * k;
+          mma_tf32_ts(d, ah + 8 * k, wh + o, kIdesc2, !(first && k == 0));  // [Ah·Wh | Ah·Wl]
+          mma_tf32_ts(d, al + 8 * k, wh + o, kIdesc1, 1);                   // += Al·Wh
+        }
+      };
+      // CHAIN: the second product of tile j reuses tile j's accumulator once
+      // the split warpgroup has turned it into O
+      auto second = [&](uint32_t j) {
+        const uint32_t acc = j & 1;
+        mbar_wait(ofull, j & 1);
+        tc_fence_after();
+        for (uint32_t kb = 0; kb < NP / BK; ++kb)
+          gemm(tmem + acc * kAccCols, tmem + TM::kOlCol + BK * kb, tmem + TM::kOhCol + BK * kb,
+               w2_s, kb, kb == 0);
+        mma_commit(ofree);
+        mma_commit(&tfull[acc]);
+      };
+      uint32_t it = 0;
       for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
         const uint32_t acc = it & 1, aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
@@ -307,125 +350,89 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
           const uint32_t l = kcount % kLoSlots;
           mbar_wait(&split[s], ph);
           tc_fence_after();
-          const uint64_t xh = umma_desc(su32(x_s + s * kTileBytes));
-          const uint64_t wh = umma_desc(su32(w_s + kb * 2 * NP * 128));  // [Wh; Wl]
-          if (kHiTmem) {
-            const uint32_t xlt = tmem + kLoCol + BK * l, xht = tmem + kHiCol + BK * l;
-#pragma unroll
-            for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +8 TMEM cols
-              const uint64_t o = 2 * k;
-              mma_tf32_ts(d, xht + 8 * k, wh + o, kIdesc2, (kb | k) != 0);  // [Xh·Wh | Xh·Wl]
-              mma_tf32_ts(d, xlt + 8 * k, wh + o, kIdesc1, 1);              // += Xl·Wh
-            }
-          } else if (kLoTmem) {
-            const uint32_t xl = tmem + kLoCol + BK * l;
-#pragma unroll
-            for (uint32_t k = 0; k < BK / 8; ++k) {  // K=8 per tf32 MMA: +32 B / +8 cols
-              const uint64_t o = 2 * k;
-              mma_tf32(d, xh + o, wh + o, kIdesc2, (kb | k) != 0);  // [Xh·Wh | Xh·Wl]
-              mma_tf32_ts(d, xl + 8 * k, wh + o, kIdesc1, 1);       // += Xl·Wh (A in TMEM)
-            }
-          } else {
-            const uint64_t xl = umma_desc(su32(lo_s + l * kTileBytes));
-#pragma unroll
-            for (uint32_t k = 0; k < BK / 8; ++k) {
-              const uint64_t o = 2 * k;
-              mma_tf32(d, xh + o, wh + o, kIdesc2, (kb | k) != 0);
-              mma_tf32(d, xl + o, wh + o, kIdesc1, 1);
-            }
-          }
-          if (!kHiTmem) mma_commit(&empty[s]);  // X stage free once these MMAs retire
-          mma_commit(&lofree[l]);  // and the Xl slot
+          gemm(d, tmem + TM::kXlCol + BK * l, tmem + TM::kXhCol + BK * l, w_s, kb, kb == 0);
+          mma_commit(&lofree[l]);  // X slot l free once these MMAs retire
           if (++s == a.stages) s = 0, ph ^= 1;
         }
-        mma_commit(&tfull[acc]);
+        if (CHAIN) {
+          mma_commit(&t1full[acc]);
+          if (it > 0) second(it - 1);
+        } else {
+          mma_commit(&tfull[acc]);
+        }
       }
+      if (CHAIN && it > 0) second(it - 1);
     }
   } else if (warp >= 4 && warp < 8) {
-    // ---------------- split warpgroup
-    const int tid = threadIdx.x - 128;  // 0..127
+    // ---------------- split warpgroup: thread = tile row = TMEM lane
+    const int row = threadIdx.x - 128;  // 0..127
+    const uint32_t lane_base = static_cast<uint32_t>(32 * (warp % 4)) << 16;
     uint32_t s = 0, ph = 0, kcount = 0;
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    // 32 values -> TMEM Xh/Xl style slots (hi = TF32-truncated, lo = rest)
+    auto split_store = [&](float* v, uint32_t lo_col, uint32_t hi_col) {
+      float lov[BK];
+#pragma unroll
+      for (int q = 0; q < BK; ++q) {
+        const float h = tf32_hi(v[q]);
+        lov[q] = v[q] - h;
+        v[q] = h;
+      }
+      tmem_st32(tmem + lo_col + lane_base, lov);
+      tmem_st32(tmem + hi_col + lane_base, v);
+    };
+    // CHAIN: O(j) = ReLU(first product + b1) from accumulator j&1 into the O slots
+    auto make_o = [&](uint32_t j) {
+      const uint32_t acc = j & 1;
+      mbar_wait(&t1full[acc], (j >> 1) & 1);
+      if (j > 0) mbar_wait(ofree, (j - 1) & 1);  // O(j-1) consumed by the second GEMM
+      tc_fence_after();
+      const uint32_t ta = tmem + acc * kAccCols + lane_base;
+#pragma unroll
+      for (int c0 = 0; c0 < NP; c0 += BK) {
+        uint32_t h[BK], l[BK];
+        tmem_ld16_nowait(ta + c0, h);
+        tmem_ld16_nowait(ta + c0 + 16, h + 16);
+        tmem_ld16_nowait(ta + NP + c0, l);
+        tmem_ld16_nowait(ta + NP + c0 + 16, l + 16);
+        tmem_wait();
+        float v[BK];
+#pragma unroll
+        for (int q = 0; q < BK; ++q)
+          v[q] = fmaxf(__uint_as_float(h[q]) + __uint_as_float(l[q]) + b1_s[c0 + q], 0.f);
+        split_store(v, TM::kOlCol + c0, TM::kOhCol + c0);
+      }
+      tc_fence_before();
+      mbar_arrive(ofull);
+    };
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       for (uint32_t kb = 0; kb < a.n_kb; ++kb, ++kcount) {
         const uint32_t l = kcount % kLoSlots;
         mbar_wait(&full[s], ph);
         mbar_wait(&lofree[l], ((kcount / kLoSlots) & 1) ^ 1);
-        float4* hi = reinterpret_cast<float4*>(x_s + s * kTileBytes);
-        if (kLoTmem) {
-          // thread = tile row = TMEM lane: its 8 (swizzled) float4 chunks in,
-          // Xl out to the lane's 32 columns of slot l
-          const int row = tid;
-          float lov[BK];
-          float hiv[kHiTmem ? BK : 1];
+        const float4* xt = reinterpret_cast<const float4*>(x_s + s * kTileBytes);
+        float v[BK];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int i = row * 8 + (c ^ (row & 7));
-            float4 v = hi[i];
-            if (a.pre) {
-              const uint32_t k0 = kb * BK + c * 4;
-              float* e = &v.x;
+        for (int c = 0; c < 8; ++c) {  // this row's 8 (swizzled) float4 chunks
+          float4 x4 = xt[row * 8 + (c ^ (row & 7))];
+          float* e = &x4.x;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                float x = e[q];
-                if (a.pre == 2) x += pb_s[k0 + q];
-                e[q] = fmaxf(x, 0.f);
-              }
-            }
-            const float4 h =
-                make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-            if (kHiTmem) {
-              hiv[4 * c] = h.x;
-              hiv[4 * c + 1] = h.y;
-              hiv[4 * c + 2] = h.z;
-              hiv[4 * c + 3] = h.w;
-            } else if (a.pre || kWriteHi) {
-              hi[i] = h;
-            }
-            lov[4 * c] = v.x - h.x;
-            lov[4 * c + 1] = v.y - h.y;
-            lov[4 * c + 2] = v.z - h.z;
-            lov[4 * c + 3] = v.w - h.w;
+          for (int q = 0; q < 4; ++q) {
+            float x = e[q];
+            if (a.pre == 2) x += pb_s[kb * BK + c * 4 + q];
+            if (a.pre) x = fmaxf(x, 0.f);
+            v[c * 4 + q] = x;
           }
-          const uint32_t lane_base = static_cast<uint32_t>(32 * (warp % 4)) << 16;
-          tmem_st32(tmem + kLoCol + BK * l + lane_base, lov);
-          if (kHiTmem) {
-            tmem_st32(tmem + kHiCol + BK * l + lane_base, hiv);
-            mbar_arrive(&empty[s]);  // smem stage consumed: back to the TMA
-          }
-          tc_fence_before();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&split[s]);
-          if (++s == a.stages) s = 0, ph ^= 1;
-          continue;
         }
-        float4* lo = reinterpret_cast<float4*>(lo_s + l * kTileBytes);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int i = tid + 128 * j;  // float4 slot in the 16 KB tile
-          float4 v = hi[i];
-          if (a.pre) {
-            const int row = i >> 3;
-            const int chunk = (i & 7) ^ (row & 7);  // undo the 128-B swizzle
-            const uint32_t k0 = kb * BK + chunk * 4;
-            float* e = &v.x;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float x = e[q];
-              if (a.pre == 2) x += pb_s[k0 + q];
-              e[q] = fmaxf(x, 0.f);
-            }
-          }
-          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          // The tf32 MMA reads only the top 19 bits of each fp32 operand, so
-          // the raw tile already is Xh; it is rewritten only when pre() changed it.
-          if (a.pre || kWriteHi) hi[i] = h;
-          lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&empty[s]);  // smem stage consumed: back to the TMA
+        split_store(v, TM::kXlCol + BK * l, TM::kXhCol + BK * l);
+        tc_fence_before();
         mbar_arrive(&split[s]);
         if (++s == a.stages) s = 0, ph ^= 1;
       }
+      if (CHAIN && it > 0) make_o(it - 1);
     }
+    if (CHAIN && it > 0) make_o(it - 1);
   } else if (warp >= 8) {
     // ---------------- epilogue warpgroup(s) (overlap the next tiles' split);
     // with two groups, group e drains accumulator e (tiles it % 2 == e)
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
+                 "r"(TM::kAlloc));
   }
 }
 
@@ -567,15 +574,16 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
-template <int NP>
+template <int NP, bool CHAIN>
 void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
-            const TcArgs& a, cudaStream_t st) {
+            const float* wt2, const TcArgs& a, cudaStream_t st) {
   const size_t wbytes = static_cast<size_t>(a.n_kb) * 2 * NP * 128;
+  const size_t w2bytes = CHAIN ? static_cast<size_t>(NP / BK) * 2 * NP * 128 : 0;
   TcArgs b = a;
   b.stages = kMaxStages;
   auto smem_for = [&](uint32_t stages) {
-    return 1024 + wbytes + (stages + (kLoTmem ? 0 : kLoSlots)) * kTileBytes + kEpBytes<NP> +
-           (3 * stages + 5 + kLoSlots) * 8 + 16 + 16 + 4 * (NP + a.n_kb * BK);
+    return 1024 + wbytes + w2bytes + stages * kTileBytes + kEpBytes<NP> +
+           (3 * stages + 11 + kLoSlots) * 8 + 16 + 16 + 4 * (2 * NP + a.n_kb * BK);
   };
   static const uint32_t cap_env = [] {
     const char* e = std::getenv("MGG_TC_STAGES");
@@ -588,11 +596,12 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   if (smem > 227 * 1024) throw Status{MGG_E_CONFIG, "gemm_tc: W too large for smem"};
   const CUtensorMap mx = make_map(in, a.k, a.rows, size_t(in_pitch) * 4, BK, BM);
   const CUtensorMap mw = make_map(wt, kpad, 2 * NP, size_t(kpad) * 4, BK, NP);
+  const CUtensorMap mw2 = CHAIN ? make_map(wt2, NP, 2 * NP, size_t(NP) * 4, BK, NP) : mw;
   const CUtensorMap mo = make_map(a.out, a.out_pitch, a.rows, size_t(a.out_pitch) * 4, 32, 32);
   const CUtensorMap mo2 = a.out2 ? make_map(a.out2, a.out_pitch, a.rows,
                                             size_t(a.out_pitch) * 4, 32, 32)
                                  : mo;
-  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP>,
+  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP, CHAIN>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   int dev = 0, sms = 0;
@@ -600,7 +609,7 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const uint64_t tiles = (a.rows + BM - 1) / BM;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, sms));
-  gemm_tc_kernel<NP><<<grid, kThreadsFor<NP>, smem, st>>>(mx, mw, mo, mo2, b);
+  gemm_tc_kernel<NP, CHAIN><<<grid, kThreadsFor<NP>, smem, st>>>(mx, mw, mw2, mo, mo2, b);
   MGG_CUDA(cudaGetLastError());
 }
 
@@ -616,8 +625,7 @@ bool gemm_tc_supported(uint32_t k, uint32_t m) {
   const size_t wbytes = size_t((k + BK - 1) / BK) * 2 * np * 128;
   const size_t kpad = size_t((k + BK - 1) / BK) * BK;
   const size_t ep = size_t(np <= 48 ? 2 : 1) * 4 * ((np + 31) / 32) * 4096;
-  return 1024 + wbytes + (2 + kLoSlots) * kTileBytes + ep + 128 + 16 + 4 * (np + kpad) <=
-         227 * 1024;
+  return 1024 + wbytes + 2 * kTileBytes + ep + 160 + 16 + 4 * (2 * np + kpad) <= 227 * 1024;
 }
 
 // Returns the cached device W^T hi/lo block for `w`, building it on first use.
@@ -657,11 +665,47 @@ void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t ro
   const uint32_t kpad = a.n_kb * BK;
   const uint32_t np = (m + 15) / 16 * 16;
   switch (np) {
-    case 16: run_tc<16>(in, in_pitch, wt, kpad, a, st); break;
-    case 32: run_tc<32>(in, in_pitch, wt, kpad, a, st); break;
-    case 48: run_tc<48>(in, in_pitch, wt, kpad, a, st); break;
-    case 64: run_tc<64>(in, in_pitch, wt, kpad, a, st); break;
+    case 16: run_tc<16, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
+    case 32: run_tc<32, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
+    case 48: run_tc<48, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
+    case 64: run_tc<64, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
     default: throw Status{MGG_E_CONFIG, "gemm_tc: unsupported width"};
+  }
+}
+
+bool gemm_tc_chain_supported(uint32_t k, uint32_t m1, uint32_t m) {
+  // O = m1 columns must be exactly the second GEMM's padded K (whole 32-wide
+  // k-blocks in TMEM), and both products share NP
+  const uint32_t np = (m + 15) / 16 * 16;
+  return gemm_tc_supported(k, m) && m1 == np && np % BK == 0 && m1 <= 64;
+}
+
+void launch_dense_tc_chain(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
+                           const float* wt1, const float* bias1, uint32_t m1,
+                           const float* pre_bias, uint32_t pre, const float* wt2,
+                           uint32_t m, float* out, uint32_t out_pitch, float* out2,
+                           float out2_scale, cudaStream_t st) {
+  if (rows == 0) return;
+  TcArgs a{};
+  a.rows = rows;
+  a.k = k;
+  a.n_kb = (k + BK - 1) / BK;
+  a.m = m;
+  a.m1 = m1;
+  a.out_pitch = out_pitch;
+  a.pre = pre;
+  a.act = 0;
+  a.bias = nullptr;
+  a.bias1 = bias1;
+  a.pre_bias = pre_bias;
+  a.out = out;
+  a.out2 = out2;
+  a.out2_scale = out2_scale;
+  const uint32_t kpad = a.n_kb * BK;
+  switch ((m + 15) / 16 * 16) {
+    case 32: run_tc<32, true>(in, in_pitch, wt1, kpad, wt2, a, st); break;
+    case 64: run_tc<64, true>(in, in_pitch, wt1, kpad, wt2, a, st); break;
+    default: throw Status{MGG_E_CONFIG, "gemm_tc chain: unsupported width"};
   }
 }
 

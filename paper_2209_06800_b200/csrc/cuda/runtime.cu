@@ -832,6 +832,32 @@ int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in, const mgg_dense_
   });
 }
 
+int mgg_dense_chain_supported(uint32_t k, uint32_t m1, uint32_t m) {
+  return gemm_tc_chain_supported(k, m1, m) ? 1 : 0;
+}
+
+int mgg_dense_chain(mgg_ctx* ctx, uint32_t part, const mgg_store* in, const mgg_dense_desc* d1,
+                    uint32_t m1, const mgg_dense_desc* d2, mgg_store* out, mgg_store* out2) {
+  return guard([&] {
+    if (!in || !d1 || !d2 || !out || !d1->w || !d2->w)
+      throw Status{MGG_E_INPUT, "dense_chain: null argument"};
+    if (out2 && out2->pitch != out->pitch) throw Status{MGG_E_INPUT, "dense_chain: out2 width differs"};
+    if (!gemm_tc_chain_supported(in->dim, m1, out->dim))
+      throw Status{MGG_E_CONFIG, "dense_chain: unsupported widths"};
+    if (d2->bias || d2->pre != 1 || d2->act != 0 || d1->act != 0)
+      throw Status{MGG_E_CONFIG, "dense_chain: second GEMM must be ReLU-in, no bias, no act"};
+    cudaStream_t st = enter(ctx, part);
+    const float* w1 = gemm_tc_prepare(const_cast<mgg_dbuf*>(d1->w), in->dim, m1, st);
+    const float* w2 = gemm_tc_prepare(const_cast<mgg_dbuf*>(d2->w), m1, out->dim, st);
+    const float* b1 = d1->bias ? static_cast<const float*>(d1->bias->ptr) : nullptr;
+    const float* pb = d1->pre_bias ? static_cast<const float*>(d1->pre_bias->ptr) : nullptr;
+    launch_dense_tc_chain(in->shard[part], in->pitch, in->dim, in->rows(part), w1, b1, m1, pb,
+                          d1->pre, w2, out->dim, out->shard[part], out->pitch,
+                          out2 ? out2->shard[part] : nullptr, d2->out2_scale, st);
+    count_launch(ctx);
+  });
+}
+
 int mgg_rows_softmax(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out) {
   return guard([&] {
     if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "rows_softmax: in/out width differ"};
