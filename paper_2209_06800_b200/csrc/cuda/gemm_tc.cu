@@ -36,12 +36,14 @@ constexpr int BK = 32;             // fp32 per 128-B swizzle row
 constexpr int kTileBytes = BM * BK * 4;  // 16 KB
 constexpr uint32_t kMaxStages = 8;
 constexpr uint32_t kLoSlots = 2;  // Xl twin tiles (decoupled from the TMA ring)
-// Epilogue warpgroups: two (alternating accumulators) while a thread's row of
-// NP fp32 fits the 128-register budget of a 512-thread CTA, else one.
-template <int NP>
-constexpr int kEpiGroups = NP <= 48 ? 2 : 1;
-template <int NP>
-constexpr int kThreadsFor = 256 + 128 * kEpiGroups<NP>;
+// EG epilogue warpgroups drain max(EG, 2) TMEM accumulators round-robin:
+// four for the short-K heads (epilogue-bound: softmax over a row per thread),
+// two while a thread's row of NP fp32 fits the 128-register budget of a
+// 512-thread CTA, else one.
+template <int EG>
+constexpr int kThreadsFor = 256 + 128 * EG;
+template <int EG>
+constexpr uint32_t kNAcc = EG < 2 ? 2 : EG;
 
 struct TcArgs {
   uint64_t rows;
@@ -128,6 +130,16 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
+// 16 consecutive 32-bit TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15])
+      : "memory");
+}
 // 32 consecutive 32-bit TMEM columns of this thread's lane.
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
   asm volatile(
@@ -184,10 +196,10 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // stage is released by the split itself); accumulating all three products
 // into one NP-wide accumulator instead was measured no faster and loses the
 // small terms' low bits (softmax error crossed 1e-4).
-template <int NP, bool CHAIN>
+template <int NP, bool CHAIN, uint32_t NACC>
 struct TmemMap {
   static constexpr uint32_t kAccCols = 2 * NP;
-  static constexpr uint32_t kXlCol = 2 * kAccCols;
+  static constexpr uint32_t kXlCol = NACC * kAccCols;
   static constexpr uint32_t kXhCol = kXlCol + kLoSlots * BK;
   static constexpr uint32_t kOlCol = kXhCol + kLoSlots * BK;  // CHAIN: NP columns each
   static constexpr uint32_t kOhCol = kOlCol + NP;
@@ -202,22 +214,24 @@ struct TmemMap {
 // bank-conflict free.
 template <int NP>
 constexpr int kStoreBlocks = (NP + 31) / 32;
-template <int NP>
-constexpr uint32_t kEpBytes = kEpiGroups<NP> * 4 * kStoreBlocks<NP> * 4096;
+template <int NP, int EG>
+constexpr uint32_t kEpBytes = EG * 4 * kStoreBlocks<NP> * 4096;
 
 // out = act(pre(X)·W + b) [+ out2 = out2_scale·(pre(X)·W + b)]; with CHAIN
 // the product goes through a second GEMM first:
 //   O = ReLU(pre(X)·W + b1)          (kept in TMEM, never written)
 //   out = O·W2 (+ out2 = out2_scale·O·W2)
 // — the GIN layer boundary Linear2 -> ReLU -> next layer's Linear1 + seed.
-template <int NP, bool CHAIN>
-__global__ void __launch_bounds__(kThreadsFor<NP>, 1)
+template <int NP, bool CHAIN, int EG>
+__global__ void __launch_bounds__(kThreadsFor<EG>, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
                    const __grid_constant__ CUtensorMap map_w,
                    const __grid_constant__ CUtensorMap map_w2,
                    const __grid_constant__ CUtensorMap map_out,
                    const __grid_constant__ CUtensorMap map_out2, TcArgs a) {
-  using TM = TmemMap<NP, CHAIN>;
+  static_assert(!CHAIN || EG <= 2, "the chain reuses accumulators j & 1");
+  constexpr uint32_t NACC = kNAcc<EG>;
+  using TM = TmemMap<NP, CHAIN, NACC>;
   constexpr uint32_t kAccCols = TM::kAccCols;
   constexpr uint32_t kIdescBase = (1u << 4) | (2u << 7) | (2u << 10) | ((BM >> 4) << 24);
   constexpr uint32_t kIdesc2 = kIdescBase | (static_cast<uint32_t>((2 * NP) >> 3) << 17);
@@ -233,13 +247,13 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
   uint8_t* w2_s = smem + wbytes;                // CHAIN: [NP/BK][hi|lo][NP][128 B]
   uint8_t* x_s = w2_s + kW2Bytes;               // [stage][16 KB] raw X
   uint8_t* ep_s = x_s + a.stages * kTileBytes;  // [groups][4 warps][NB][4 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpBytes<NP>);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ep_s + kEpBytes<NP, EG>);
   uint64_t* full = bars;                        // [stages] TMA -> split
   uint64_t* split = bars + a.stages;            // [stages] split -> MMA (X slots filled)
   uint64_t* empty = bars + 2 * a.stages;        // [stages] split -> TMA
-  uint64_t* tfull = bars + 3 * a.stages;        // [2] final accumulator -> epilogue
-  uint64_t* tempty = tfull + 2;                 // [2] epilogue -> MMA
-  uint64_t* lofree = tempty + 2;                // [kLoSlots] MMA -> split (X slots)
+  uint64_t* tfull = bars + 3 * a.stages;        // [NACC] final accumulator -> epilogue
+  uint64_t* tempty = tfull + NACC;              // [NACC] epilogue -> MMA
+  uint64_t* lofree = tempty + NACC;             // [kLoSlots] MMA -> split (X slots)
   uint64_t* wfull = lofree + kLoSlots;          // W (and W2) resident
   uint64_t* t1full = wfull + 1;                 // CHAIN [2]: first product -> split
   uint64_t* ofull = t1full + 2;                 // CHAIN: O slots filled -> MMA
@@ -268,11 +282,11 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
       mbar_init(&split[s], 128);
       mbar_init(&empty[s], 128);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (uint32_t i = 0; i < NACC; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 128);
-      mbar_init(&t1full[i], 1);
     }
+    for (int i = 0; i < 2; ++i) mbar_init(&t1full[i], 1);
     for (uint32_t i = 0; i < kLoSlots; ++i) mbar_init(&lofree[i], 1);
     mbar_init(wfull, 1);
     mbar_init(ofull, 128);
@@ -342,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
       };
       uint32_t it = 0;
       for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+        const uint32_t acc = it % NACC, aph = (it / NACC) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * kAccCols;
@@ -368,18 +382,20 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     const int row = threadIdx.x - 128;  // 0..127
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp % 4)) << 16;
     uint32_t s = 0, ph = 0, kcount = 0;
-    // 32 values -> TMEM Xh/Xl style slots (hi = TF32-truncated, lo = rest)
+    // 16 values -> TMEM Xh/Xl style slots (hi = TF32-truncated, lo = rest);
+    // the stores complete (wait::st) before the caller signals the MMA
     auto split_store = [&](float* v, uint32_t lo_col, uint32_t hi_col) {
-      float lov[BK];
+      float lov[16];
 #pragma unroll
-      for (int q = 0; q < BK; ++q) {
+      for (int q = 0; q < 16; ++q) {
         const float h = tf32_hi(v[q]);
         lov[q] = v[q] - h;
         v[q] = h;
       }
-      tmem_st32(tmem + lo_col + lane_base, lov);
-      tmem_st32(tmem + hi_col + lane_base, v);
+      tmem_st16(tmem + lo_col + lane_base, lov);
+      tmem_st16(tmem + hi_col + lane_base, v);
     };
+    auto st_wait = [] { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); };
     // CHAIN: O(j) = ReLU(first product + b1) from accumulator j&1 into the O slots
     auto make_o = [&](uint32_t j) {
       const uint32_t acc = j & 1;
@@ -388,19 +404,18 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
       tc_fence_after();
       const uint32_t ta = tmem + acc * kAccCols + lane_base;
 #pragma unroll
-      for (int c0 = 0; c0 < NP; c0 += BK) {
-        uint32_t h[BK], l[BK];
+      for (int c0 = 0; c0 < NP; c0 += 16) {
+        uint32_t h[16], l[16];
         tmem_ld16_nowait(ta + c0, h);
-        tmem_ld16_nowait(ta + c0 + 16, h + 16);
         tmem_ld16_nowait(ta + NP + c0, l);
-        tmem_ld16_nowait(ta + NP + c0 + 16, l + 16);
         tmem_wait();
-        float v[BK];
+        float v[16];
 #pragma unroll
-        for (int q = 0; q < BK; ++q)
+        for (int q = 0; q < 16; ++q)
           v[q] = fmaxf(__uint_as_float(h[q]) + __uint_as_float(l[q]) + b1_s[c0 + q], 0.f);
         split_store(v, TM::kOlCol + c0, TM::kOhCol + c0);
       }
+      st_wait();
       tc_fence_before();
       mbar_arrive(ofull);
     };
@@ -411,21 +426,26 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
         mbar_wait(&full[s], ph);
         mbar_wait(&lofree[l], ((kcount / kLoSlots) & 1) ^ 1);
         const float4* xt = reinterpret_cast<const float4*>(x_s + s * kTileBytes);
-        float v[BK];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // this row's 8 (swizzled) float4 chunks
-          float4 x4 = xt[row * 8 + (c ^ (row & 7))];
-          float* e = &x4.x;
+        for (int half = 0; half < 2; ++half) {  // 16 columns at a time
+          float v[16];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float x = e[q];
-            if (a.pre == 2) x += pb_s[kb * BK + c * 4 + q];
-            if (a.pre) x = fmaxf(x, 0.f);
-            v[c * 4 + q] = x;
+          for (int c = 0; c < 4; ++c) {  // this row's (swizzled) float4 chunks
+            const int cc = half * 4 + c;
+            float4 x4 = xt[row * 8 + (cc ^ (row & 7))];
+            float* e = &x4.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float x = e[q];
+              if (a.pre == 2) x += pb_s[kb * BK + cc * 4 + q];
+              if (a.pre) x = fmaxf(x, 0.f);
+              v[c * 4 + q] = x;
+            }
           }
+          split_store(v, TM::kXlCol + BK * l + 16 * half, TM::kXhCol + BK * l + 16 * half);
         }
         mbar_arrive(&empty[s]);  // smem stage consumed: back to the TMA
-        split_store(v, TM::kXlCol + BK * l, TM::kXhCol + BK * l);
+        st_wait();
         tc_fence_before();
         mbar_arrive(&split[s]);
         if (++s == a.stages) s = 0, ph ^= 1;
@@ -440,14 +460,27 @@ __global__ void __launch_bounds__(kThreadsFor<NP>, 1)
     const int g = warp % 4;  // TMEM lane quarter
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      if (kEpiGroups<NP> == 2 && static_cast<int>(it & 1) != eg) continue;
-      const uint32_t acc = it & 1, aph = (it >> 1) & 1;
+      if (EG > 1 && static_cast<int>(it % EG) != eg) continue;
+      const uint32_t acc = it % NACC, aph = (it / NACC) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       float y[NP];
-      {
+      const uint32_t ta = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16);
+      if (EG >= 3) {  // register-lean: 16 columns in flight
+#pragma unroll
+        for (int c = 0; c < NP; c += 16) {
+          uint32_t r[16];
+          tmem_ld16_nowait(ta + c, r);
+          tmem_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) y[c + q] = __uint_as_float(r[q]);
+          tmem_ld16_nowait(ta + NP + c, r);
+          tmem_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) y[c + q] += __uint_as_float(r[q]);
+        }
+      } else {
         uint32_t r[NP];
-        const uint32_t ta = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * g) << 16);
 #pragma unroll
         for (int c = 0; c < NP; c += 16) tmem_ld16_nowait(ta + c, r + c);
         tmem_wait();
@@ -574,7 +607,7 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
-template <int NP, bool CHAIN>
+template <int NP, bool CHAIN, int EG>
 void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
             const float* wt2, const TcArgs& a, cudaStream_t st) {
   const size_t wbytes = static_cast<size_t>(a.n_kb) * 2 * NP * 128;
@@ -582,8 +615,8 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   TcArgs b = a;
   b.stages = kMaxStages;
   auto smem_for = [&](uint32_t stages) {
-    return 1024 + wbytes + w2bytes + stages * kTileBytes + kEpBytes<NP> +
-           (3 * stages + 11 + kLoSlots) * 8 + 16 + 16 + 4 * (2 * NP + a.n_kb * BK);
+    return 1024 + wbytes + w2bytes + stages * kTileBytes + kEpBytes<NP, EG> +
+           (3 * stages + 2 * kNAcc<EG> + 7 + kLoSlots) * 8 + 16 + 16 + 4 * (2 * NP + a.n_kb * BK);
   };
   static const uint32_t cap_env = [] {
     const char* e = std::getenv("MGG_TC_STAGES");
@@ -601,7 +634,7 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   const CUtensorMap mo2 = a.out2 ? make_map(a.out2, a.out_pitch, a.rows,
                                             size_t(a.out_pitch) * 4, 32, 32)
                                  : mo;
-  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP, CHAIN>,
+  MGG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<NP, CHAIN, EG>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   int dev = 0, sms = 0;
@@ -609,7 +642,7 @@ void run_tc(const float* in, uint32_t in_pitch, const float* wt, uint32_t kpad,
   MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const uint64_t tiles = (a.rows + BM - 1) / BM;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, sms));
-  gemm_tc_kernel<NP, CHAIN><<<grid, kThreadsFor<NP>, smem, st>>>(mx, mw, mw2, mo, mo2, b);
+  gemm_tc_kernel<NP, CHAIN, EG><<<grid, kThreadsFor<EG>, smem, st>>>(mx, mw, mw2, mo, mo2, b);
   MGG_CUDA(cudaGetLastError());
 }
 
@@ -624,7 +657,7 @@ bool gemm_tc_supported(uint32_t k, uint32_t m) {
   const uint32_t np = (m + 15) / 16 * 16;
   const size_t wbytes = size_t((k + BK - 1) / BK) * 2 * np * 128;
   const size_t kpad = size_t((k + BK - 1) / BK) * BK;
-  const size_t ep = size_t(np <= 48 ? 2 : 1) * 4 * ((np + 31) / 32) * 4096;
+  const size_t ep = size_t(np <= 48 ? 4 : 1) * 4 * ((np + 31) / 32) * 4096;
   return 1024 + wbytes + 2 * kTileBytes + ep + 160 + 16 + 4 * (2 * np + kpad) <= 227 * 1024;
 }
 
@@ -664,11 +697,29 @@ void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t ro
   a.out2_scale = out2_scale;
   const uint32_t kpad = a.n_kb * BK;
   const uint32_t np = (m + 15) / 16 * 16;
+  // four epilogue groups for short-K GEMMs (the heads: the epilogue binds),
+  // two (NP <= 48) or one otherwise
+  static const uint32_t g4_kb = [] {
+    const char* e = std::getenv("MGG_TC_G4_KB");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;
+  }();
+  const bool g4 = a.n_kb <= g4_kb;
   switch (np) {
-    case 16: run_tc<16, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
-    case 32: run_tc<32, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
-    case 48: run_tc<48, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
-    case 64: run_tc<64, false>(in, in_pitch, wt, kpad, nullptr, a, st); break;
+    case 16: g4 ? run_tc<16, false, 4>(in, in_pitch, wt, kpad, nullptr, a, st)
+                : run_tc<16, false, 2>(in, in_pitch, wt, kpad, nullptr, a, st); break;
+    case 32: g4 ? run_tc<32, false, 4>(in, in_pitch, wt, kpad, nullptr, a, st)
+                : run_tc<32, false, 2>(in, in_pitch, wt, kpad, nullptr, a, st); break;
+    case 48: {
+      static const int eg48 = [] {
+        const char* e = std::getenv("MGG_TC_EG48");
+        return e ? std::atoi(e) : 3;
+      }();
+      if (!g4) run_tc<48, false, 2>(in, in_pitch, wt, kpad, nullptr, a, st);
+      else if (eg48 == 4) run_tc<48, false, 4>(in, in_pitch, wt, kpad, nullptr, a, st);
+      else run_tc<48, false, 3>(in, in_pitch, wt, kpad, nullptr, a, st);
+      break;
+    }
+    case 64: run_tc<64, false, 1>(in, in_pitch, wt, kpad, nullptr, a, st); break;
     default: throw Status{MGG_E_CONFIG, "gemm_tc: unsupported width"};
   }
 }
@@ -703,8 +754,8 @@ void launch_dense_tc_chain(const float* in, uint32_t in_pitch, uint32_t k, uint6
   a.out2_scale = out2_scale;
   const uint32_t kpad = a.n_kb * BK;
   switch ((m + 15) / 16 * 16) {
-    case 32: run_tc<32, true>(in, in_pitch, wt1, kpad, wt2, a, st); break;
-    case 64: run_tc<64, true>(in, in_pitch, wt1, kpad, wt2, a, st); break;
+    case 32: run_tc<32, true, 2>(in, in_pitch, wt1, kpad, wt2, a, st); break;
+    case 64: run_tc<64, true, 1>(in, in_pitch, wt1, kpad, wt2, a, st); break;
     default: throw Status{MGG_E_CONFIG, "gemm_tc chain: unsupported width"};
   }
 }
