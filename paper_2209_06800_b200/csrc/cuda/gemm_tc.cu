@@ -8,16 +8,19 @@
 // the 3x tensor work is free; what matters is streaming X at HBM rate.
 //
 // Persistent CTA per SM, warp-specialised:
-//   warp 0  : TMA producer — X tiles (128 rows x 32 fp32 = one 128-B swizzle
-//             row per tile row) into a 4-deep smem ring; W^T hi/lo resident.
-//   warp 1  : MMA issuer — one elected thread, 3 x 4 tcgen05.mma (M=128,
-//             N=NP, K=8) per 32-wide k-block into a TMEM accumulator
-//             (double-buffered across row tiles).
-//   warp 2  : TMEM allocator.
-//   warps 4-7: split (pre-transform, Xh in place, Xl to a twin tile; the
-//             async-proxy fence hands the tile to the tensor core) and the
-//             epilogue (tcgen05.ld 32x32b -> bias / ReLU / row softmax /
-//             scaled accumulator seed -> global).
+//   warp 0   : TMA producer — X tiles (128 rows x 32 fp32, 128-B swizzle)
+//              into a smem ring; W^T hi/lo (and the chain's W2) resident.
+//   warp 1   : MMA issuer — one thread; A operands from TMEM:
+//              [Xh·Wh | Xh·Wl] (N = 2NP) + Xl·Wh per K=8 step into a TMEM
+//              accumulator ring.
+//   warp 2   : TMEM allocator.
+//   warps 4-7: split — thread = tile row = TMEM lane: pre-transform, Xh/Xl
+//              into TMEM (tcgen05.st), releases the smem stage; in the chain
+//              variant also turns the first product into the second GEMM's
+//              A operand (O never leaves TMEM).
+//   warps 8+ : 1-4 epilogue warpgroups — tcgen05.ld, bias / ReLU / row
+//              softmax / scaled accumulator seed, 128-B swizzled staging and
+//              TMA bulk tensor stores.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -115,13 +118,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) |
          (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
 // A operand from TMEM (lanes = rows, 32-bit columns = k): the Xl term.
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
                                             uint32_t idesc, uint32_t acc) {
@@ -139,20 +135,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
       "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
       "f"(v[15])
       : "memory");
-}
-// 32 consecutive 32-bit TMEM columns of this thread's lane.
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-          taddr),
-      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
-      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
-      "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
-      "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
-      "f"(v[29]), "f"(v[30]), "f"(v[31])
-      : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
