@@ -30,6 +30,7 @@ struct mgg_ctx;
 struct mgg_store;
 struct mgg_dplan;
 struct mgg_dbuf;
+struct mgg_exec;
 
 namespace mgg {
 
@@ -72,6 +73,9 @@ class Engine {
   void set_remote_fetch(RemoteFetch mode);
   void set_input(const float* x);            // N x in_dim host rows
   void forward();                            // async, device resident
+  /// Replay forward() from a captured CUDA graph when the context allows it
+  /// (one device, all parts local, not profiling); on by default there.
+  void set_graphs(bool on);
   void synchronize();
   void get_output(float* z);                 // N x out_dim host rows
   void forward_host(const float* x, float* z);  // submit_host + wait
@@ -166,6 +170,10 @@ class Engine {
   std::vector<int> hidden_;           // post-aggregation stores per layer
   mgg_store* scratch_[2] = {nullptr, nullptr};
   bool profiling_ = false;
+  bool graphs_ = true;
+  mgg_exec* exec_ = nullptr;          // captured forward()
+  mgg_store* exec_input_ = nullptr;   // input store the capture read
+  void drop_exec();
   std::uint32_t prof_part_ = 0, next_slot_ = 0;
   std::vector<std::uint32_t> prof_starts_;  // first slot of each profiled forward
   Stats stats_;

@@ -146,6 +146,7 @@ _sig("mgg_dplan_halo_len", I, vp, u64p)
 _sig("mgg_remote_partition_bytes", U64, U64, U64, I, U64)
 _sig("mgg_engine_set_input", I, vp, f32p)
 _sig("mgg_engine_forward", I, vp)
+_sig("mgg_engine_set_graphs", I, vp, I)
 _sig("mgg_engine_get_output", I, vp, f32p)
 _sig("mgg_engine_forward_host", I, vp, f32p, f32p)
 _sig("mgg_engine_submit_host", I, vp, f32p, f32p, u64p)
@@ -169,6 +170,10 @@ _sig("mgg_engine_ctx", vp, vp)
 _sig("mgg_engine_set_profiling", I, vp, I)
 _sig("mgg_engine_profile", I, vp, C.POINTER(C.c_double), u32p, u32p, SZ, C.POINTER(SZ), u64p)
 _sig("mgg_event_record", I, vp, U32, U32)
+_sig("mgg_capture_begin", I, vp)
+_sig("mgg_capture_end", I, vp, PP)
+_sig("mgg_exec_launch", I, vp, vp)
+_sig("mgg_exec_destroy", I, vp)
 _sig("mgg_event_elapsed", I, vp, U32, U32, U32, f32p)
 
 # every exported symbol the header declares (checked by the CPU test suite)

@@ -436,6 +436,10 @@ class Engine:
     def forward(self) -> None:
         check(lib.mgg_engine_forward(self._h))
 
+    def set_graphs(self, on: bool) -> None:
+        """CUDA-graph replay of forward() on single-device contexts (default on)."""
+        check(lib.mgg_engine_set_graphs(self._h, int(on)))
+
     def synchronize(self) -> None:
         check(lib.mgg_ctx_synchronize(lib.mgg_engine_ctx(self._h)))
 

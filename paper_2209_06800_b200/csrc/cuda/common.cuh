@@ -40,6 +40,8 @@ struct mgg_ctx {
   std::vector<std::vector<cudaEvent_t>> lane_ev;  // per part: [from*3+to] fences
   std::vector<std::vector<cudaEvent_t>> marks;    // per part: host-waitable slots
   uint64_t launches = 0;
+  uint64_t capture_base = 0;           // launch count at mgg_capture_begin
+  bool capturing = false;
   uint32_t epoch = 0;                  // barrier generation
   bool all_local = true;
   bool single_device = true;
@@ -68,6 +70,12 @@ struct mgg_dbuf {
   size_t bytes = 0;
   void* tc_cache = nullptr;  // W^T hi/lo split for the tcgen05 GEMM
   uint32_t tc_k = 0, tc_m = 0;
+};
+
+struct mgg_exec {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;  // library launches captured (replays count them)
+  int device = 0;
 };
 
 struct mgg_trace {

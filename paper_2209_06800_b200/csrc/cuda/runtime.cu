@@ -328,6 +328,65 @@ int mgg_lane_wait_host(mgg_ctx* ctx, uint32_t part, uint32_t slot) {
 
 uint64_t mgg_ctx_launch_count(const mgg_ctx* c) { return c ? c->launches : 0; }
 
+static uint32_t first_local(mgg_ctx* ctx) {
+  for (uint32_t p = 0; p < ctx->num_parts; ++p)
+    if (ctx->device[p] >= 0) return p;
+  throw Status{MGG_E_INPUT, "context has no local part"};
+}
+
+int mgg_capture_begin(mgg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) throw Status{MGG_E_INPUT, "capture_begin: null context"};
+    if (!ctx->all_local || !ctx->single_device)
+      throw Status{MGG_E_CONFIG, "capture: needs one device and all parts local"};
+    if (ctx->capturing) throw Status{MGG_E_INPUT, "capture_begin: already capturing"};
+    cudaStream_t st = enter(ctx, first_local(ctx));
+    MGG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    ctx->capturing = true;
+    ctx->capture_base = ctx->launches;
+  });
+}
+
+int mgg_capture_end(mgg_ctx* ctx, mgg_exec** out) {
+  return guard([&] {
+    if (!ctx || !out) throw Status{MGG_E_INPUT, "capture_end: null argument"};
+    if (!ctx->capturing) throw Status{MGG_E_INPUT, "capture_end: not capturing"};
+    const uint32_t p = first_local(ctx);
+    cudaStream_t st = enter(ctx, p);
+    ctx->capturing = false;
+    cudaGraph_t g = nullptr;
+    MGG_CUDA(cudaStreamEndCapture(st, &g));
+    auto* e = new mgg_exec();
+    e->device = ctx->device[p];
+    e->kernels = ctx->launches - ctx->capture_base;
+    ctx->launches = ctx->capture_base;  // captured, not launched
+    const cudaError_t r = cudaGraphInstantiate(&e->exec, g, 0);
+    cudaGraphDestroy(g);
+    if (r != cudaSuccess) {
+      delete e;
+      check(r, "cudaGraphInstantiate");
+    }
+    *out = e;
+  });
+}
+
+int mgg_exec_launch(mgg_ctx* ctx, const mgg_exec* g) {
+  return guard([&] {
+    if (!ctx || !g) throw Status{MGG_E_INPUT, "exec_launch: null argument"};
+    cudaStream_t st = enter(ctx, first_local(ctx));
+    MGG_CUDA(cudaGraphLaunch(g->exec, st));
+    ctx->launches += g->kernels;
+  });
+}
+
+int mgg_exec_destroy(mgg_exec* g) {
+  if (!g) return MGG_OK;
+  // at process teardown the runtime may already be gone: leak, don't crash
+  if (cudaSetDevice(g->device) == cudaSuccess) cudaGraphExecDestroy(g->exec);
+  delete g;
+  return MGG_OK;
+}
+
 int mgg_event_record(mgg_ctx* ctx, uint32_t part, uint32_t slot) {
   return guard([&] {
     cudaStream_t st = enter(ctx, part);

@@ -479,6 +479,9 @@ int mgg_engine_get_output(mgg_engine* e, float* z) {
 int mgg_engine_forward_host(mgg_engine* e, const float* x, float* z) {
   return guard([&] { e->e->forward_host(x, z); });
 }
+int mgg_engine_set_graphs(mgg_engine* e, int on) {
+  return guard([&] { e->e->set_graphs(on != 0); });
+}
 int mgg_engine_submit_host(mgg_engine* e, const float* x, float* z, uint64_t* ticket) {
   return guard([&] {
     if (!ticket) throw mgg::InputError("submit_host: null ticket");

@@ -63,6 +63,8 @@ Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
 
 Engine::~Engine() {
   if (ctx_) mgg_ctx_synchronize(ctx_);
+  mgg_exec_destroy(exec_);
+  exec_ = nullptr;
   free_plans();
   for (auto* s : in_bufs_)  // the one not currently installed as the input
     if (s && s != stores_[input_]) mgg_store_destroy(s);
@@ -193,6 +195,12 @@ void Engine::build_program() {
 }
 
 void Engine::free_plans() {
+  if (exec_) {  // the captured forward references these plans
+    mgg_ctx_synchronize(ctx_);
+    mgg_exec_destroy(exec_);
+    exec_ = nullptr;
+    exec_input_ = nullptr;
+  }
   for (auto*& p : plans_) {
     mgg_dplan_destroy(p);
     p = nullptr;
@@ -365,7 +373,43 @@ void Engine::set_input(const float* x) {
   ok(mgg_store_upload(stores_[input_], x, 0, g_.num_nodes, spec_.in_dim));
 }
 
-void Engine::forward() { forward_ops(false); }
+void Engine::forward() {
+  bool graphable = graphs_ && !profiling_;
+  for (std::uint32_t p = 0; p < num_parts_ && graphable; ++p)
+    graphable = dev_[p] >= 0 && dev_[p] == dev_[0];
+  if (!graphable) {
+    forward_ops(false);
+    return;
+  }
+  if (exec_ && exec_input_ != stores_[input_]) drop_exec();  // streamed double buffer swapped
+  if (!exec_) {
+    ok(mgg_capture_begin(ctx_));
+    try {
+      forward_ops(false);
+    } catch (...) {
+      mgg_exec* junk = nullptr;
+      mgg_capture_end(ctx_, &junk);
+      mgg_exec_destroy(junk);
+      throw;
+    }
+    ok(mgg_capture_end(ctx_, &exec_));
+    exec_input_ = stores_[input_];
+  }
+  ok(mgg_exec_launch(ctx_, exec_));
+}
+
+void Engine::set_graphs(bool on) {
+  graphs_ = on;
+  if (!on) drop_exec();
+}
+
+void Engine::drop_exec() {
+  if (!exec_) return;
+  ok(mgg_ctx_synchronize(ctx_));
+  mgg_exec_destroy(exec_);
+  exec_ = nullptr;
+  exec_input_ = nullptr;
+}
 
 // `streamed`: the forward of submit_host — its input arrives on the H2D lane
 // and its output leaves on the D2H lane, fenced so that the next forward's

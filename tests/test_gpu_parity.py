@@ -358,3 +358,32 @@ def test_device_trace_schema_and_counts(mgg, parts, cfg):
     short = eng.trace_csv(16, capacity=10).strip().split("\n")
     assert len(short) - 2 <= 10 * parts
     eng.close()
+
+
+@pytest.mark.parametrize("parts", [1, 2])
+def test_graph_replay_matches_eager(mgg, oracle_mod, parts):
+    # forward() is captured into a CUDA graph once and replayed; a re-plan
+    # (set_config) must re-capture, results must equal the eager path's
+    g = mgg.gen_rmat(3000, 40000, seed=19)
+    model = mgg.make_gcn(48, 16, 12, seed=5)
+    x = mgg.random_features(g.num_nodes, 48, seed=6)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=16, dist=2, wpb=4)
+    try:
+        eng.set_input(x)
+        eng.set_graphs(False)
+        eng.forward()
+        z_eager = eng.get_output().copy()
+        eng.set_graphs(True)
+        l0 = eng.stats()["launches"]
+        for _ in range(3):
+            eng.forward()
+        eng.synchronize()
+        assert eng.stats()["launches"] > l0, "graph replays must count their kernels"
+        # K1's vector reductions commute only up to fp32 rounding
+        assert np.abs(eng.get_output() - z_eager).max() <= 1e-5
+        eng.set_config(32, 4, 2)
+        eng.forward()
+        _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+        assert np.abs(eng.get_output() - zr).max() <= TOL
+    finally:
+        eng.close()
