@@ -87,6 +87,9 @@ def _args():
     ap.add_argument("--wpb", type=int, default=None)
     ap.add_argument("--parts", type=int, default=None,
                     help="logical partitions on one GPU (single process)")
+    ap.add_argument("--fetch", default="auto", choices=["auto", "fine", "halo"],
+                    help="remote rows: per-edge peer reads in K1 (fine, the paper's design) or "
+                         "one deduplicated pull per layer (halo); auto picks by bytes moved")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
@@ -331,6 +334,8 @@ def main():
     t0 = time.perf_counter()
     eng = mgg.Engine(g, n, part_device, model, ps=args.ps, dist=args.dist, wpb=args.wpb)
     setup_s = time.perf_counter() - t0
+    if args.fetch != "auto":
+        eng.set_remote_fetch(args.fetch)
     if world > 1:
         mdist.exchange_ipc(eng, rank, world)
         dist.barrier()
@@ -465,6 +470,7 @@ def main():
                        "nodes": N, "edges": E, "dim": model.in_dim, "hidden": model.hidden,
                        "classes": model.out_dim, "layers": layers, "agg_widths": widths,
                        "ps": args.ps, "dist": args.dist, "wpb": args.wpb, "parts": n,
+                       "remote_fetch": args.fetch,
                        "l2": "inputs larger than L2 (X + CSR >= 1 GB), no flush",
                        "layer_forward_ms": round(ms_step, 4)},
             "roofline": {"bound": "hbm", "kernel": f"K1 aggregation, width {w0}",
