@@ -387,3 +387,21 @@ def test_graph_replay_matches_eager(mgg, oracle_mod, parts):
         assert np.abs(eng.get_output() - zr).max() <= TOL
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("hidden,eps", [(32, 0.0), (48, 0.1), (64, 0.5), (16, 0.0)])
+def test_gin_chain_widths(mgg, oracle_mod, hidden, eps):
+    # GIN layer boundaries run as one chained tcgen05 kernel when the hidden
+    # width is a whole number of 32-column k-blocks (32, 64); other widths
+    # (16, 48) fall back to two GEMMs — all must match the oracle
+    g = mgg.gen_synthetic(mgg.POWERLAW, 2500, 9, 7)
+    model = mgg.make_gin(40, hidden, 11, layers=4, seed=hidden, eps=eps)
+    x = mgg.random_features(g.num_nodes, 40, seed=3)
+    eng = mgg.Engine(g, 1, [0], model, ps=16, dist=4, wpb=4)
+    try:
+        z = np.zeros((g.num_nodes, 11), np.float32)
+        eng.forward_host(x, z)
+        _, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
+        assert np.abs(z - zr).max() <= TOL, np.abs(z - zr).max()
+    finally:
+        eng.close()
