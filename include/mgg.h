@@ -71,6 +71,11 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
 int mgg_ctx_destroy(mgg_ctx* ctx);
 /* Waits for all work this process queued on every local part. */
 int mgg_ctx_synchronize(mgg_ctx* ctx);
+/* Parts sharing a device each have their own stream (logical partitions run
+ * concurrently; MGG_PART_STREAMS=0 reverts to one stream per device). This
+ * orders every part's stream after every other's current tail; a no-op when
+ * the parts of a device share a stream. */
+int mgg_ctx_join(mgg_ctx* ctx);
 
 /* Symmetric embedding store — the paper's NVSHMEM "shared" NE space
  * (R:PAPER.md:333-345) as per-part shards: part p holds global rows

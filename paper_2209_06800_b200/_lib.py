@@ -170,6 +170,7 @@ _sig("mgg_engine_ctx", vp, vp)
 _sig("mgg_engine_set_profiling", I, vp, I)
 _sig("mgg_engine_profile", I, vp, C.POINTER(C.c_double), u32p, u32p, SZ, C.POINTER(SZ), u64p)
 _sig("mgg_event_record", I, vp, U32, U32)
+_sig("mgg_ctx_join", I, vp)
 _sig("mgg_capture_begin", I, vp)
 _sig("mgg_capture_end", I, vp, PP)
 _sig("mgg_exec_launch", I, vp, vp)

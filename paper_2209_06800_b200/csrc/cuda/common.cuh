@@ -45,6 +45,10 @@ struct mgg_ctx {
   uint32_t epoch = 0;                  // barrier generation
   bool all_local = true;
   bool single_device = true;
+  // parts sharing a device get their own compute/aux streams (concurrent
+  // logical partitions); the K3 barrier becomes a cross-stream event join
+  bool part_streams = false;
+  std::vector<cudaEvent_t> bar_ev;     // per part: barrier join events
 };
 
 struct mgg_store {

@@ -169,6 +169,11 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
       c->fork.assign(num_parts, nullptr);
       c->join.assign(num_parts, nullptr);
       c->evpool.assign(num_parts, {});
+      c->bar_ev.assign(num_parts, nullptr);
+      {
+        const char* e = std::getenv("MGG_PART_STREAMS");
+        c->part_streams = !(e && std::string(e) == "0");
+      }
       c->h2d.assign(num_parts, nullptr);
       c->d2h.assign(num_parts, nullptr);
       c->rp.assign(num_parts, nullptr);
@@ -185,15 +190,17 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
         if (first < 0) first = d;
         if (d != first) c->single_device = false;
         MGG_CUDA(cudaSetDevice(d));
-        // parts on one device share one stream: launches then order phases
-        // across logical partitions without a barrier
-        for (uint32_t q = 0; q < p; ++q)
+        // one compute/aux stream per part, also for logical partitions sharing
+        // a device: they run concurrently and join at barriers with events
+        // (MGG_PART_STREAMS=0: one stream per device, stream order instead)
+        for (uint32_t q = 0; q < p && !c->part_streams; ++q)
           if (c->device[q] == d) c->stream[p] = c->stream[q];
         if (!c->stream[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->stream[p], cudaStreamNonBlocking));
         MGG_CUDA(cudaEventCreate(&c->ev0[p]));
         MGG_CUDA(cudaEventCreate(&c->ev1[p]));
-        for (uint32_t q = 0; q < p; ++q)
+        for (uint32_t q = 0; q < p && !c->part_streams; ++q)
           if (c->device[q] == d) c->aux[p] = c->aux[q];
+        MGG_CUDA(cudaEventCreateWithFlags(&c->bar_ev[p], cudaEventDisableTiming));
         if (!c->aux[p]) MGG_CUDA(cudaStreamCreateWithFlags(&c->aux[p], cudaStreamNonBlocking));
         for (uint32_t q = 0; q < p; ++q)
           if (c->device[q] == d) {
@@ -259,6 +266,7 @@ int mgg_ctx_destroy(mgg_ctx* c) {
     }
     for (cudaEvent_t e : c->lane_ev[p])
       if (e) cudaEventDestroy(e);
+    if (c->bar_ev[p]) cudaEventDestroy(c->bar_ev[p]);
     for (cudaEvent_t e : c->marks[p])
       if (e) cudaEventDestroy(e);
   }
@@ -334,16 +342,39 @@ static uint32_t first_local(mgg_ctx* ctx) {
   throw Status{MGG_E_INPUT, "context has no local part"};
 }
 
+int mgg_ctx_join(mgg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx || !ctx->part_streams) return;
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      if (ctx->device[p] >= 0) {
+        enter(ctx, p);
+        MGG_CUDA(cudaEventRecord(ctx->bar_ev[p], ctx->stream[p]));
+      }
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      for (uint32_t q = 0; q < ctx->num_parts; ++q)
+        if (q != p && ctx->device[p] >= 0 && ctx->device[q] == ctx->device[p]) {
+          enter(ctx, p);
+          MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[q], 0));
+        }
+  });
+}
+
 int mgg_capture_begin(mgg_ctx* ctx) {
   return guard([&] {
     if (!ctx) throw Status{MGG_E_INPUT, "capture_begin: null context"};
     if (!ctx->all_local || !ctx->single_device)
       throw Status{MGG_E_CONFIG, "capture: needs one device and all parts local"};
     if (ctx->capturing) throw Status{MGG_E_INPUT, "capture_begin: already capturing"};
-    cudaStream_t st = enter(ctx, first_local(ctx));
+    const uint32_t p0 = first_local(ctx);
+    cudaStream_t st = enter(ctx, p0);
     MGG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
     ctx->capturing = true;
     ctx->capture_base = ctx->launches;
+    if (ctx->part_streams) {  // pull the other parts' streams into the capture
+      MGG_CUDA(cudaEventRecord(ctx->bar_ev[p0], st));
+      for (uint32_t p = 0; p < ctx->num_parts; ++p)
+        if (p != p0) MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[p0], 0));
+    }
   });
 }
 
@@ -354,6 +385,12 @@ int mgg_capture_end(mgg_ctx* ctx, mgg_exec** out) {
     const uint32_t p = first_local(ctx);
     cudaStream_t st = enter(ctx, p);
     ctx->capturing = false;
+    if (ctx->part_streams)  // join the other parts' streams back
+      for (uint32_t q = 0; q < ctx->num_parts; ++q)
+        if (q != p) {
+          MGG_CUDA(cudaEventRecord(ctx->bar_ev[q], ctx->stream[q]));
+          MGG_CUDA(cudaStreamWaitEvent(st, ctx->bar_ev[q], 0));
+        }
     cudaGraph_t g = nullptr;
     MGG_CUDA(cudaStreamEndCapture(st, &g));
     auto* e = new mgg_exec();
@@ -928,7 +965,16 @@ int mgg_rows_softmax(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store
 
 int mgg_barrier(mgg_ctx* ctx, mgg_store* flags) {
   return guard([&] {
-    if (ctx->all_local && ctx->single_device) return;  // stream order suffices
+    if (ctx->all_local && ctx->single_device) {
+      if (!ctx->part_streams) return;  // one stream per device: stream order suffices
+      // one stream per part: every part waits for every other part's work
+      for (uint32_t p = 0; p < ctx->num_parts; ++p)
+        MGG_CUDA(cudaEventRecord(ctx->bar_ev[p], ctx->stream[p]));
+      for (uint32_t p = 0; p < ctx->num_parts; ++p)
+        for (uint32_t q = 0; q < ctx->num_parts; ++q)
+          if (q != p) MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[q], 0));
+      return;
+    }
     if (!flags) throw Status{MGG_E_INPUT, "barrier: flags store required"};
     ++ctx->epoch;
     if (ctx->all_local) {  // one process, several devices: host-side join

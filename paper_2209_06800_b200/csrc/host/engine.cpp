@@ -429,6 +429,7 @@ void Engine::forward_ops(bool streamed) {
     if (streamed && static_cast<int>(i) == out_first_write_)
       fence_all(MGG_LANE_D2H, MGG_LANE_COMPUTE);  // previous z has left the device
     run(program_[i]);
+    if (i + 1 == program_.size()) ok(mgg_ctx_join(ctx_));  // concurrent parts: end together
     if (profiling_) ok(mgg_event_record(ctx_, prof_part_, next_slot_++));
     if (streamed && static_cast<int>(i) == in_last_use_) {
       if (in_bufs_[1]) {  // this buffer is free for the submission after next
