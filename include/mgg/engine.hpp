@@ -171,6 +171,7 @@ class Engine {
   mgg_store* scratch_[2] = {nullptr, nullptr};
   bool profiling_ = false;
   bool graphs_ = true;
+  bool eager_warm_ = false;           // one eager forward before the first capture
   mgg_exec* exec_ = nullptr;          // captured forward()
   mgg_store* exec_input_ = nullptr;   // input store the capture read
   void drop_exec();

@@ -195,6 +195,7 @@ void Engine::build_program() {
 }
 
 void Engine::free_plans() {
+  eager_warm_ = false;  // new plans: halo buffers are re-created by an eager pass
   if (exec_) {  // the captured forward references these plans
     mgg_ctx_synchronize(ctx_);
     mgg_exec_destroy(exec_);
@@ -382,6 +383,13 @@ void Engine::forward() {
     return;
   }
   if (exec_ && exec_input_ != stores_[input_]) drop_exec();  // streamed double buffer swapped
+  if (!eager_warm_) {
+    // first forward runs eagerly: one-time work (tcgen05 weight splits,
+    // halo buffers) must not become nodes of the captured graph
+    forward_ops(false);
+    eager_warm_ = true;
+    return;
+  }
   if (!exec_) {
     ok(mgg_capture_begin(ctx_));
     try {
