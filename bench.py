@@ -61,7 +61,7 @@ WORKLOADS = {
     "products-gcn": ("GCN-2L ogbn-products-shaped (north_star target shape)",
                      ("powerlaw", 2_449_029, 25.259), ("gcn", 100, 16, 47, 2), (32, 16, 2)),
     "products-gin": ("GIN-5L hidden 64 ogbn-products-shaped (BASELINE configs[2])",
-                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 16, 16)),
+                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 16, 2)),
     "orkut-gcn": ("GCN-2L com-Orkut-shaped (BASELINE configs[3])",
                   ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 2)),
     # locality-bearing (skewed, ids not shuffled) variants of the same shapes
@@ -69,7 +69,7 @@ WORKLOADS = {
     "reddit-rmat-gcn": ("GCN-2L Reddit-shaped RMAT variant",
                         ("rmat", 232_965, 114_615_892), ("gcn", 602, 16, 41, 2), (32, 16, 2)),
     "products-rmat-gin": ("GIN-5L hidden 64 ogbn-products-shaped RMAT variant",
-                          ("rmat", 2_449_029, 61_859_140), ("gin", 100, 64, 47, 5), (16, 16, 4)),
+                          ("rmat", 2_449_029, 61_859_140), ("gin", 100, 64, 47, 5), (16, 16, 2)),
     "orkut-rmat-gcn": ("GCN-2L com-Orkut-shaped RMAT variant",
                        ("rmat", 3_072_441, 117_185_083), ("gcn", 128, 16, 32, 2), (32, 16, 4)),
 }

@@ -489,8 +489,8 @@ int reg_cap_mode() {
 // partition / warp / CTA geometry without the pairing machinery, so the
 // register footprint — hence resident warps, hence row loads in flight —
 // is set by the gather alone.
-template <int VEC, bool RELU, int MINB>
-__global__ void __launch_bounds__(512, MINB) agg_local(AggArgs a) {
+template <int VEC, bool RELU>
+__device__ __forceinline__ void agg_local_body(const AggArgs& a) {
   using L = Lanes<VEC, RELU>;
   const L ln(a);
   const int lane = ln.lane;
@@ -530,6 +530,27 @@ __global__ void __launch_bounds__(512, MINB) agg_local(AggArgs a) {
   if (cur >= 0) ln.flush(a, acc, cur);
 }
 
+// The register budget is the occupancy knob of this latency-bound gather:
+// MINB resident 512-thread CTAs (64 / 42 / 32 registers), or an explicit cap.
+template <int VEC, bool RELU, int MINB>
+__global__ void __launch_bounds__(512, MINB) agg_local(AggArgs a) {
+  agg_local_body<VEC, RELU>(a);
+}
+template <int VEC, bool RELU, int REGS>
+__global__ void __maxnreg__(REGS) agg_local_r(AggArgs a) {
+  agg_local_body<VEC, RELU>(a);
+}
+template <bool RELU, int REGS>
+KernelFn pick_local_r(uint32_t v) {
+  if (v <= 1) return agg_local_r<1, RELU, REGS>;
+  if (v <= 2) return agg_local_r<2, RELU, REGS>;
+  if (v <= 4) return agg_local_r<4, RELU, REGS>;
+  if (v <= 8) return agg_local_r<8, RELU, REGS>;
+  if (v <= 16) return agg_local_r<16, RELU, REGS>;
+  if (v <= 32) return agg_local_r<32, RELU, REGS>;
+  return agg_wide<RELU>;
+}
+
 template <bool RELU, int MINB>
 KernelFn pick_local(uint32_t v) {
   if (v <= 1) return agg_local<1, RELU, MINB>;
@@ -556,10 +577,13 @@ KernelFn pick(uint32_t v) {
       case 3: return pick_local<RELU, 3>(v);
       case 4: return pick_local<RELU, 4>(v);
       case 5: return pick_local<RELU, 2>(v);
-      // measured (profiles/r01_k1_experiments.md): narrow rows (<= 16 floats,
-      // L2-resident tables) want 64 regs/36 warps; wider rows want 40 regs/48
-      // warps despite a few spilled bytes
-      default: return v <= 4 ? pick_local<RELU, 2>(v) : pick_local<RELU, 3>(v);
+      case 10: return pick_local_r<RELU, 48>(v);
+      case 11: return pick_local_r<RELU, 56>(v);
+      case 12: return pick_local_r<RELU, 48>(v);
+      // measured (profiles/r01_k1_experiments.md): narrow rows (<= 16 floats)
+      // want the 64-register cap; wider rows an explicit 48 (products-gin
+      // K1 2.68 -> 2.48 ms vs the spilling 42-register MINB=3 cap)
+      default: return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
     }
   }
   // measured on B200 (profiles/): local-only is best at a 64-register cap
