@@ -227,6 +227,87 @@ __global__ void __launch_bounds__(512) k_hybrid(const __grid_constant__ CUtensor
   out[static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x] = acc.x + acc.y + acc.z + acc.w;
 }
 
+// 64-B rows, K1-like mapping, 128-bit (4 lanes per row, 8 rows per warp
+// step) vs 256-bit loads (2 lanes per row, 16 rows per step): is the L1TEX
+// cost per row or per load instruction?
+template <int W>  // bytes per lane load: 16 or 32
+__global__ void __launch_bounds__(512) k_vec(const float* __restrict__ x,
+                                             const int* __restrict__ idx, long n_idx,
+                                             float* __restrict__ out) {
+  constexpr int D = 16, L = 64 / W, R = 32 / L;  // lanes per row, rows per step
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long gw = static_cast<long>(blockIdx.x) * 16 + warp;
+  const long tw = static_cast<long>(gridDim.x) * 16;
+  const long nwin = n_idx / 32;
+  const long per = (nwin + tw - 1) / tw;
+  const long w0 = gw * per, w1 = min(w0 + per, nwin);
+  const int sub = lane / L, v = lane % L;
+  float acc[W / 4] = {};
+  for (long j = w0; j < w1; ++j) {
+    const int id = __ldg(idx + j * 32 + lane);
+#pragma unroll
+    for (int q = 0; q < 32 / R; ++q) {
+      const int row = __shfl_sync(0xffffffffu, id, q * R + sub);
+      const float* p = x + static_cast<long>(row) * D + v * (W / 4);
+      if (W == 16) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
+      } else {
+        float r[8];
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                       "=f"(r[6]), "=f"(r[7])
+                     : "l"(p));
+#pragma unroll
+        for (int i = 0; i < W / 4; ++i) acc[i] += r[i % 8];
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < W / 4; ++i) s += acc[i];
+  out[static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x] = s;
+}
+
+void run_vec(long rows, long n_idx) {
+  std::vector<int> h(n_idx);
+  std::mt19937_64 g(42);
+  for (auto& v : h) v = static_cast<int>(g() % rows);
+  float *x, *out;
+  int* idx;
+  CK(cudaMalloc(&x, rows * 16 * 4));
+  CK(cudaMemset(x, 0, rows * 16 * 4));
+  CK(cudaMalloc(&idx, n_idx * 4));
+  CK(cudaMemcpy(idx, h.data(), n_idx * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&out, static_cast<size_t>(148) * 4 * 512 * 4));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  const double bytes = static_cast<double>(n_idx) * 64;
+  for (int per_sm : {2, 3, 4}) {
+    float best[2] = {1e30f, 1e30f};
+    for (int impl = 0; impl < 2; ++impl)
+      for (int it = 0; it < 6; ++it) {
+        CK(cudaEventRecord(a));
+        if (impl == 0)
+          k_vec<16><<<148 * per_sm, 512>>>(x, idx, n_idx, out);
+        else
+          k_vec<32><<<148 * per_sm, 512>>>(x, idx, n_idx, out);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        CK(cudaGetLastError());
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (it > 0 && ms < best[impl]) best[impl] = ms;
+      }
+    std::printf("vec rows=%ld ctas/sm=%d  128-bit: %.3f ms %.0f GB/s | 256-bit: %.3f ms %.0f GB/s\n",
+                rows, per_sm, best[0], bytes / best[0] / 1e6, best[1], bytes / best[1] / 1e6);
+  }
+  CK(cudaFree(x));
+  CK(cudaFree(idx));
+  CK(cudaFree(out));
+}
+
 static PFN_cuTensorMapEncodeTiled encode_fn() {
   void* p = nullptr;
   cudaDriverEntryPointQueryResult q{};
@@ -357,6 +438,11 @@ void run_hybrid(long rows, long n_idx) {
 }
 
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "vec") {
+    run_vec(232965, 1L << 27);
+    run_vec(2449029, 1L << 27);
+    return 0;
+  }
   if (argc > 1 && std::string(argv[1]) == "hybrid") {
     run_hybrid(232965, 1L << 27);
     run_hybrid(2449029, 1L << 27);
