@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, fetch="auto", kind="gcn"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0")
     try:
@@ -31,19 +31,32 @@ def _worker(rank, world, port, q):
         from paper_2209_06800_b200 import dist as mdist
         dist.init_process_group("gloo", rank=rank, world_size=world)
         g = mgg.gen_rmat(4000, 60000, seed=3)
-        model = mgg.make_gcn(64, 16, 24, seed=4)
+        if kind == "gin":  # chained GIN boundaries across processes
+            model = mgg.make_gin(64, 32, 24, layers=3, seed=4, eps=0.2)
+        else:
+            model = mgg.make_gcn(64, 16, 24, seed=4)
         x = mgg.random_features(g.num_nodes, 64, seed=5)
         eng = mgg.Engine(g, world, mdist.part_devices(world, rank, 0), model, ps=16, dist=2,
                          wpb=4)
+        if fetch != "auto":
+            eng.set_remote_fetch(fetch)  # before the IPC exchange: halo buffers are per part
         mdist.exchange_ipc(eng, rank, world)
         dist.barrier()
         z = np.zeros((g.num_nodes, 24), np.float32)
         for _ in range(2):
             eng.forward_host(x, z)
+        # the device-resident path too (set_input + forward + get_output)
+        eng.set_input(x)
+        eng.forward()
+        z2 = eng.get_output()
         st = eng.stats()
-        _, _, zr = oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+        if kind == "gin":
+            _, zr = oracle.gin_forward(g.row_ptr, g.col_idx, x, model)
+        else:
+            _, _, zr = oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model)
         lo, hi = (int(v) for v in mgg.chunk_ranges(g, world)[rank])
-        err = float(np.abs(z[lo:hi] - zr[lo:hi]).max()) if hi > lo else 0.0
+        err = float(max(np.abs(z[lo:hi] - zr[lo:hi]).max(),
+                        np.abs(z2[lo:hi] - zr[lo:hi]).max())) if hi > lo else 0.0
         dist.barrier()
         eng.close()
         dist.destroy_process_group()
@@ -53,14 +66,16 @@ def _worker(rank, world, port, q):
         q.put((rank, None, None, traceback.format_exc()))
 
 
-def test_two_processes_ipc_forward():
+@pytest.mark.parametrize("fetch,kind", [("auto", "gcn"), ("fine", "gcn"), ("halo", "gin")])
+def test_two_processes_ipc_forward(fetch, kind):
     import paper_2209_06800_b200 as mgg
     assert mgg.cuda_available()
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fetch, kind))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
