@@ -235,7 +235,17 @@ def _traffic(args, parts):
     return None
 
 
-def cpu_forward_time(g, x, model, threads=0):
+def host_threads() -> int:
+    """All host threads of the box (torchrun exports OMP_NUM_THREADS=1 to every
+    rank; the CPU baseline must not inherit that)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def cpu_forward_time(g, x, model, threads=None):
+    threads = host_threads() if threads is None else threads
     import oracle
     t0 = time.perf_counter()
     if model.kind == 0:
@@ -255,7 +265,7 @@ def run_reference(args):
     e = g.num_edges
     layers = model.layers
     x = mgg.random_features(g.num_nodes, model.in_dim, seed=1)
-    cores = os.cpu_count() or 1
+    cores = host_threads()
     for _ in range(max(args.warmup, 0)):
         cpu_forward_time(g, x, model)
     times = [cpu_forward_time(g, x, model) for _ in range(max(args.steps, 1))]
@@ -450,7 +460,7 @@ def main():
         try:
             tc = cpu_forward_time(g, np.asarray(x), model)
             cpu = {"value": round(layers * E / tc / 1e9, 4), "unit": "GEdges/s",
-                   "cores": os.cpu_count(), "kind": "port",
+                   "cores": host_threads(), "kind": "port",
                    "sample": "one full forward of the same workload (oracle.c, fp32 "
                              "accumulate, OpenMP all host threads)",
                    "seconds": round(tc, 3)}
