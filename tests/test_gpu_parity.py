@@ -6,6 +6,8 @@ accumulate. "Relative" is per output row: |gpu - ref| <= 1e-4 * max|ref_row|
 cancellation; the row scale is the magnitude the terms carry). Softmax rows
 are compared absolutely (they are already normalised).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -453,3 +455,49 @@ def test_full_size_forward_matches_oracle(mgg, oracle_mod, workload):
     print(f"\n{workload}: logits row-relative {lerr:.2e}, softmax {err:.2e} "
           f"(fp32 oracle floor {floor:.2e}, max |logit| {np.abs(lg).max():.1f})")
     assert err <= max(TOL, 2 * floor), f"{workload}: softmax {err:.3e}, fp32 oracle floor {floor:.3e}"
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MGG_FUZZ_N", "12"))))
+def test_fuzz_forward(mgg, oracle_mod, seed):
+    # random graph kind / size, model kind and widths, part count, (ps,
+    # dist, wpb), remote-fetch mode and graph replay on/off — every output
+    # against the fp64 oracle (logits-scale-aware softmax check as above)
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(200, 4000))
+    kind = ("rmat", "powerlaw", "uniform")[seed % 3]
+    if kind == "rmat":
+        g = mgg.gen_rmat(n, int(n * rng.integers(2, 20)), seed=seed)
+    else:
+        g = mgg.gen_synthetic(mgg.POWERLAW if kind == "powerlaw" else mgg.UNIFORM, n,
+                              float(rng.uniform(1.5, 20)), seed)
+    din = int(rng.choice([5, 16, 33, 64, 100, 130]))
+    hid = int(rng.choice([8, 16, 32, 48, 64]))
+    cls = int(rng.choice([3, 16, 41, 47, 64]))
+    if seed % 2:
+        model = mgg.make_gin(din, hid, cls, layers=int(rng.integers(2, 5)), seed=seed,
+                             eps=float(rng.uniform(0, 0.5)))
+    else:
+        model = mgg.make_gcn(din, hid, cls, seed=seed)
+    parts = int(rng.integers(1, 5))
+    cfg = (int(rng.choice([1, 2, 4, 8, 16, 32])), int(rng.choice([1, 2, 4, 8, 16])),
+           int(rng.choice([1, 2, 4, 8, 16])))
+    x = mgg.random_features(g.num_nodes, din, seed=seed + 7)
+    eng = mgg.Engine(g, parts, [0] * parts, model, *cfg)
+    try:
+        eng.set_remote_fetch(("auto", "fine", "halo")[seed % 3])
+        eng.set_graphs(bool(seed % 4))
+        eng.set_input(x)
+        eng.forward()
+        eng.forward()
+        z = eng.get_output()
+    finally:
+        eng.close()
+    if model.kind == 0:
+        _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+        _, _, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+    else:
+        _, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
+        _, z32 = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+    floor = float(np.abs(z32 - zr).max())
+    err = float(np.abs(z - zr).max())
+    assert err <= max(TOL, 2 * floor), (seed, kind, n, din, hid, cls, parts, cfg, err, floor)
