@@ -294,8 +294,8 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
         tma_2d(w_s + kb * 2 * NP * 128, &map_w, wfull, kb * BK, 0);
         tma_2d(w_s + kb * 2 * NP * 128 + NP * 128, &map_w, wfull, kb * BK, NP);
       }
-      if (CHAIN)
-        for (uint32_t kb = 0; kb < NP / BK; ++kb) {
+      if constexpr (CHAIN)
+        for (uint32_t kb = 0; kb < static_cast<uint32_t>(NP / BK); ++kb) {
           tma_2d(w2_s + kb * 2 * NP * 128, &map_w2, wfull, kb * BK, 0);
           tma_2d(w2_s + kb * 2 * NP * 128 + NP * 128, &map_w2, wfull, kb * BK, NP);
         }
@@ -330,9 +330,10 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
         const uint32_t acc = j & 1;
         mbar_wait(ofull, j & 1);
         tc_fence_after();
-        for (uint32_t kb = 0; kb < NP / BK; ++kb)
-          gemm(tmem + acc * kAccCols, tmem + TM::kOlCol + BK * kb, tmem + TM::kOhCol + BK * kb,
-               w2_s, kb, kb == 0);
+        if constexpr (CHAIN)
+          for (uint32_t kb = 0; kb < static_cast<uint32_t>(NP / BK); ++kb)
+            gemm(tmem + acc * kAccCols, tmem + TM::kOlCol + BK * kb,
+                 tmem + TM::kOhCol + BK * kb, w2_s, kb, kb == 0);
         mma_commit(ofree);
         mma_commit(&tfull[acc]);
       };
