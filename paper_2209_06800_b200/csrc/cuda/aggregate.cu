@@ -50,6 +50,10 @@
 #define MGG_LD_INSN "ld.global.nc.L1::evict_first.v4.f32"
 #endif
 
+#ifndef MGG_AGG_PF
+#define MGG_AGG_PF 4
+#endif
+
 #ifndef MGG_AGG_UNROLL
 #define MGG_AGG_UNROLL 4
 #endif
@@ -177,7 +181,7 @@ __device__ __forceinline__ void cta_chunk(uint32_t total, uint32_t& b0, uint32_t
 template <int VEC, bool RELU>
 struct Lanes {
   static constexpr int RPW = 32 / VEC;  // rows per warp step
-  static constexpr int PF = 4;          // remote steps staged ahead
+  static constexpr int PF = MGG_AGG_PF;  // remote steps staged ahead
   int lane, sub, v;
   bool vlane;
   uint32_t voff;       // byte offset of this lane's float4 in a row
