@@ -64,6 +64,9 @@ WORKLOADS = {
                      ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 16, 2)),
     "orkut-gcn": ("GCN-2L com-Orkut-shaped (BASELINE configs[3])",
                   ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 2)),
+    # the symmetric-normalised GCN (D^-1/2 (A+I) D^-1/2) on the configs[1] graph
+    "reddit-gcn-norm": ("GCN-2L normalised, Reddit-shaped (configs[1] graph)",
+                        ("powerlaw", 232_965, 492), ("gcn-norm", 602, 16, 41, 2), (32, 16, 2)),
     # locality-bearing (skewed, ids not shuffled) variants of the same shapes
     # (report both an id-random and an RMAT variant per graph)
     "reddit-rmat-gcn": ("GCN-2L Reddit-shaped RMAT variant",
@@ -202,8 +205,10 @@ def build(mgg, name):
         g = mgg.gen_synthetic(mgg.POWERLAW, n, avg, 0)
     gen_s = time.perf_counter() - t0
     mk, din, hid, out, layers = mspec
-    model = (mgg.make_gcn(din, hid, out, seed=2) if mk == "gcn"
-             else mgg.make_gin(din, hid, out, layers=layers, seed=2))
+    if mk in ("gcn", "gcn-norm"):
+        model = mgg.make_gcn(din, hid, out, seed=2, norm=mk == "gcn-norm")
+    else:
+        model = mgg.make_gin(din, hid, out, layers=layers, seed=2)
     return label, g, model, gen_s
 
 
@@ -249,7 +254,8 @@ def cpu_forward_time(g, x, model, threads=None):
     import oracle
     t0 = time.perf_counter()
     if model.kind == 0:
-        oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False, threads=threads)
+        oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model, norm=model.norm, acc64=False,
+                            threads=threads)
     else:
         oracle.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False, threads=threads)
     return time.perf_counter() - t0

@@ -216,6 +216,12 @@ int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
 /* mgg_rows_init that also writes copy[r] = f(in[r]) (same width; null = no
  * copy): the activated layer input, which the next mgg_aggregate then
  * gathers with relu_in = 0 instead of applying f once per edge. */
+/* rows_init_copy with an optional per-row multiplier (the part's rows). */
+int mgg_rows_init_rs(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
+                     float scale, int relu_in, mgg_store* copy, const mgg_dbuf* row_scale);
+/* rows_softmax of row_scale[r] * in[r]. */
+int mgg_rows_softmax_rs(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
+                        const mgg_dbuf* row_scale);
 int mgg_rows_init_copy(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
                        mgg_store* out, float scale, int relu_in, mgg_store* copy);
 
@@ -236,6 +242,8 @@ typedef struct {
   uint32_t pre;
   uint32_t act;
   float out2_scale;
+  const mgg_dbuf* row_scale; /* optional: per-row multiplier of the product
+                                (the part's rows; normalised GCN) */
 } mgg_dense_desc;
 int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
               const mgg_dense_desc* d, mgg_store* out, mgg_store* out2);
@@ -400,6 +408,9 @@ typedef struct {
   const float* b1;
   const float* w2;
   const float* b2;
+  uint32_t norm;       /* GCN: 1 = symmetric normalisation D^-1/2 (A+I) D^-1/2
+                          with d_v = |N(v)| + 1 (oracle norm=1); 0 = the
+                          paper's plain sum over N(v) ∪ {v} */
 } mgg_model_desc;
 
 /* Builds split (Alg. 1), follow_split placement, per-part plans, stores and

@@ -39,6 +39,7 @@ struct ModelSpec {
   std::uint32_t layers = 2;
   std::uint32_t in_dim = 0, hidden = 0, out_dim = 0;
   float eps = 0.f;
+  bool norm = false;  // GCN: D^-1/2 (A+I) D^-1/2, d_v = |N(v)| + 1
   // packed weights, layout of mgg_model_desc (include/mgg.h)
   std::vector<float> w1, b1, w2, b2;
 };
@@ -124,18 +125,21 @@ class Engine {
     int relu = 0;
     int w2 = -1;  // dense_chain: second weight (O·W2), O = `mid` store's width
     int mid = -1;
+    int rs = 0;   // normalised GCN: multiply the op's rows by D^-rs/2
   };
 
   int add_store(std::uint32_t dim);
   int add_weight(const float* src, std::size_t n);
   void build_program();
-  int activated(int h, std::uint32_t width, int relu, int a, float scale);
+  int activated(int h, std::uint32_t width, int relu, int a, float scale, int rs);
   void build_plans();
   void free_plans();
   void run(const Op& op);
   void forward_ops(bool streamed);
   void find_io_points();
   void fuse_chains();
+  void build_row_scales();
+  std::vector<mgg_dbuf*> rs_[3];  // [power][part]: D^-power/2 over the part's rows
   static constexpr std::uint64_t kMaxInFlight = 32, kMarkSlots = 64;
   int in_last_use_ = -1, out_first_write_ = -1;
   std::uint64_t submitted_ = 0, completed_ = 0;

@@ -33,7 +33,7 @@ MEASURE_FN = C.CFUNCTYPE(C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, vp,
 class ModelDesc(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("layers", C.c_uint32), ("in_dim", C.c_uint32),
                 ("hidden", C.c_uint32), ("out_dim", C.c_uint32), ("eps", C.c_float),
-                ("w1", f32p), ("b1", f32p), ("w2", f32p), ("b2", f32p)]
+                ("w1", f32p), ("b1", f32p), ("w2", f32p), ("b2", f32p), ("norm", C.c_uint32)]
 
 
 class PlanDesc(C.Structure):
@@ -51,7 +51,7 @@ class AggOpts(C.Structure):
 
 class DenseDesc(C.Structure):
     _fields_ = [("w", vp), ("bias", vp), ("pre_bias", vp), ("pre", C.c_uint32),
-                ("act", C.c_uint32), ("out2_scale", C.c_float)]
+                ("act", C.c_uint32), ("out2_scale", C.c_float), ("row_scale", vp)]
 
 
 def _sig(name, res, *args):
@@ -98,6 +98,8 @@ _sig("mgg_aggregate", I, vp, vp, vp, vp, C.POINTER(AggOpts))
 _sig("mgg_rows_init", I, vp, U32, vp, vp, C.c_float, I)
 _sig("mgg_rows_init_copy", I, vp, U32, vp, vp, C.c_float, I, vp)
 _sig("mgg_rows_softmax", I, vp, U32, vp, vp)
+_sig("mgg_rows_softmax_rs", I, vp, U32, vp, vp, vp)
+_sig("mgg_rows_init_rs", I, vp, U32, vp, vp, C.c_float, I, vp, vp)
 _sig("mgg_dense", I, vp, U32, vp, C.POINTER(DenseDesc), vp, vp)
 _sig("mgg_dense_chain", I, vp, U32, vp, C.POINTER(DenseDesc), U32, C.POINTER(DenseDesc), vp, vp)
 _sig("mgg_dense_chain_supported", I, U32, U32, U32)

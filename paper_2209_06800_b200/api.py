@@ -345,6 +345,7 @@ class Model:
     w2: np.ndarray | None = None
     b2: np.ndarray | None = None
     eps: float = 0.0
+    norm: int = 0  # GCN: 1 = D^-1/2 (A+I) D^-1/2 (oracle norm=1), 0 = the paper's plain sum
 
     def gin_dims(self) -> list[int]:
         return [self.in_dim] + [self.hidden] * (self.layers - 1) + [self.out_dim]
@@ -355,11 +356,11 @@ def _glorot(rng: np.random.Generator, fan_in: int, fan_out: int) -> np.ndarray:
     return rng.uniform(-lim, lim, size=(fan_in, fan_out)).astype(np.float32)
 
 
-def make_gcn(in_dim: int, hidden: int, classes: int, seed: int = 2) -> Model:
+def make_gcn(in_dim: int, hidden: int, classes: int, seed: int = 2, norm: bool = False) -> Model:
     rng = np.random.default_rng(seed)
     w = np.concatenate([_glorot(rng, in_dim, hidden).ravel(),
                         _glorot(rng, hidden, classes).ravel()])
-    return Model(0, 2, in_dim, hidden, classes, w.astype(np.float32))
+    return Model(0, 2, in_dim, hidden, classes, w.astype(np.float32), norm=int(norm))
 
 
 def make_gin(in_dim: int, hidden: int, classes: int, layers: int = 5, seed: int = 2,
@@ -394,7 +395,7 @@ class Engine:
         f = C.POINTER(C.c_float)
         arg = [x.ctypes.data_as(f) if x is not None else None for x in self._keep]
         desc = ModelDesc(model.kind, model.layers, model.in_dim, model.hidden,
-                         model.out_dim, model.eps, *arg)
+                         model.out_dim, model.eps, *arg, getattr(model, "norm", 0))
         dev = np.ascontiguousarray(part_device, np.int32)
         self._h = C.c_void_p()
         check(lib.mgg_engine_create(g.handle, num_parts, _p(dev, C.c_int32), ps, dist, wpb,

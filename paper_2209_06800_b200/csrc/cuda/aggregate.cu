@@ -624,11 +624,16 @@ unsigned resident_grid(KernelFn k, int threads) {
 // a per-edge ReLU)
 template <bool RELU>
 __global__ void rows_init_kernel(const float4* __restrict__ in, float4* __restrict__ out,
-                                 float4* __restrict__ copy, size_t n4, float scale) {
+                                 float4* __restrict__ copy, size_t n4, float scale,
+                                 const float* __restrict__ row_scale, uint32_t vec) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
        i += (size_t)gridDim.x * blockDim.x) {
     float4 x = __ldg(in + i);
     if (RELU) x = f4relu(x);
+    if (row_scale) {  // normalised GCN: the row's D^-1/2 power
+      const float r = __ldg(row_scale + i / vec);
+      x = make_float4(x.x * r, x.y * r, x.z * r, x.w * r);
+    }
     out[i] = make_float4(x.x * scale, x.y * scale, x.z * scale, x.w * scale);
     if (copy) copy[i] = x;
   }
@@ -753,7 +758,8 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
 }
 
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
-                      float scale, int relu_in, float* copy, cudaStream_t st) {
+                      float scale, int relu_in, float* copy, cudaStream_t st,
+                      const float* row_scale) {
   const size_t n4 = rows * (size_t)pitch / 4;
   if (n4 == 0) return;
   const unsigned blocks =
@@ -762,10 +768,10 @@ void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch
   auto* c = reinterpret_cast<float4*>(copy);
   if (relu_in)
     rows_init_kernel<true><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), o, c,
-                                                   n4, scale);
+                                                   n4, scale, row_scale, pitch / 4);
   else
     rows_init_kernel<false><<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in), o, c,
-                                                    n4, scale);
+                                                    n4, scale, row_scale, pitch / 4);
   MGG_CUDA(cudaGetLastError());
 }
 

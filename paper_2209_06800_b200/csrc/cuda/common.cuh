@@ -126,15 +126,17 @@ void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st);
 void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st);
 void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg_store* out,
                    const mgg_agg_opts* o, cudaStream_t st);
+// row_scale (optional): per-row multiplier of the part's rows (normalised GCN)
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,
-                      float scale, int relu_in, float* copy, cudaStream_t st);
+                      float scale, int relu_in, float* copy, cudaStream_t st,
+                      const float* row_scale = nullptr);
 void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                   const float* w, const float* bias, const float* pre_bias,
                   uint32_t m, uint32_t pre, uint32_t act, float* out,
                   uint32_t out_pitch, float* out2, float out2_scale,
-                  cudaStream_t st);
+                  cudaStream_t st, const float* row_scale = nullptr);
 void launch_softmax(const float* in, float* out, uint64_t rows, uint32_t pitch,
-                    uint32_t m, cudaStream_t st);
+                    uint32_t m, cudaStream_t st, const float* row_scale = nullptr);
 bool gemm_tc_supported(uint32_t k, uint32_t m);
 bool gemm_tc_chain_supported(uint32_t k, uint32_t m1, uint32_t m);
 void launch_dense_tc_chain(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
@@ -146,7 +148,7 @@ const float* gemm_tc_prepare(mgg_dbuf* w, uint32_t k, uint32_t m, cudaStream_t s
 void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                      const float* wt, const float* bias, const float* pre_bias, uint32_t m,
                      uint32_t pre, uint32_t act, float* out, uint32_t out_pitch, float* out2,
-                     float out2_scale, cudaStream_t st);
+                     float out2_scale, cudaStream_t st, const float* row_scale = nullptr);
 void launch_barrier(unsigned* const* flag_shards_dev, unsigned* own, uint32_t me,
                     uint32_t num_parts, uint32_t epoch, cudaStream_t st);
 

@@ -31,6 +31,7 @@ struct DenseArgs {
   uint32_t col0;  // first output column of this launch's column tile
   uint32_t pre, act;
   float out2_scale;
+  const float* row_scale;  // optional per-row multiplier of the product
 };
 
 // k-tile: 16 when the whole reduction is <= 16 (the GCN heads), else 32
@@ -123,7 +124,9 @@ __global__ void __launch_bounds__(256) dense_kernel(DenseArgs a) {
 #pragma unroll
     for (int i = 0; i < S::RPT; ++i) {
       const uint64_t row = row0 + rg + i * S::RG;
-      float y[4] = {acc[i].x + b[0], acc[i].y + b[1], acc[i].z + b[2], acc[i].w + b[3]};
+      const float rs = (a.row_scale && row < a.rows) ? __ldg(a.row_scale + row) : 1.f;
+      float y[4] = {acc[i].x * rs + b[0], acc[i].y * rs + b[1], acc[i].z * rs + b[2],
+                    acc[i].w * rs + b[3]};
       if (a.out2 && row < a.rows && c_base < (int)a.out_pitch) {
         float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
         float* po = &o2.x;
@@ -192,28 +195,29 @@ void run(const DenseArgs& a, cudaStream_t st) {
 
 // Row softmax over the first m columns (one warp per row), in place allowed.
 __global__ void softmax_rows_kernel(const float* in, float* out, uint64_t rows,
-                                    uint32_t pitch, uint32_t m) {
+                                    uint32_t pitch, uint32_t m, const float* row_scale) {
   const uint64_t row = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   const float* x = in + row * pitch;
+  const float rs = row_scale ? __ldg(row_scale + row) : 1.f;
   float mx = -FLT_MAX;
-  for (uint32_t j = lane; j < m; j += 32) mx = fmaxf(mx, x[j]);
+  for (uint32_t j = lane; j < m; j += 32) mx = fmaxf(mx, x[j] * rs);
   for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   float s = 0.f;
-  for (uint32_t j = lane; j < m; j += 32) s += __expf(x[j] - mx);
+  for (uint32_t j = lane; j < m; j += 32) s += __expf(x[j] * rs - mx);
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   const float inv = 1.f / s;
-  for (uint32_t j = lane; j < m; j += 32) out[row * pitch + j] = __expf(x[j] - mx) * inv;
+  for (uint32_t j = lane; j < m; j += 32) out[row * pitch + j] = __expf(x[j] * rs - mx) * inv;
 }
 
 }  // namespace
 
 void launch_softmax(const float* in, float* out, uint64_t rows, uint32_t pitch,
-                    uint32_t m, cudaStream_t st) {
+                    uint32_t m, cudaStream_t st, const float* row_scale) {
   if (rows == 0) return;
   softmax_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(in, out, rows,
-                                                                          pitch, m);
+                                                                          pitch, m, row_scale);
   MGG_CUDA(cudaGetLastError());
 }
 
@@ -221,11 +225,11 @@ void launch_dense(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                   const float* w, const float* bias, const float* pre_bias,
                   uint32_t m, uint32_t pre, uint32_t act, float* out,
                   uint32_t out_pitch, float* out2, float out2_scale,
-                  cudaStream_t st) {
+                  cudaStream_t st, const float* row_scale) {
   if (act == 2 && m > 64)
     throw Status{MGG_E_CONFIG, "dense: fused softmax supports m <= 64"};
   DenseArgs a{in, w, bias, pre_bias, out, out2, rows, in_pitch, k, m, out_pitch,
-              0, pre, act, out2_scale};
+              0, pre, act, out2_scale, row_scale};
   for (uint32_t c0 = 0; c0 < m; c0 += 64) {
     a.col0 = c0;
     const uint32_t cols = std::min<uint32_t>(64, m - c0);

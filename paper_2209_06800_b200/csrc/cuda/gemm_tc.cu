@@ -59,6 +59,7 @@ struct TcArgs {
   float out2_scale;
   const float* bias1;  // CHAIN: bias of the first product (m1 = NP columns)
   uint32_t m1;
+  const float* row_scale;  // optional per-row multiplier of the product (before bias)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -477,6 +478,12 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (a.row_scale) {  // normalised GCN: this row's D^-1/2 power
+        const uint64_t r = static_cast<uint64_t>(t) * BM + 32 * g + lane;
+        const float rs = r < a.rows ? __ldg(a.row_scale + r) : 1.f;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) y[c] *= rs;
+      }
       // Each thread holds its row: write it into the warp's swizzled staging
       // blocks, then one lane hands the 32 x NP tile to the TMA engine (bulk
       // tensor store, clipped at the last row / the pitch) — no per-lane
@@ -663,9 +670,10 @@ const float* gemm_tc_prepare(mgg_dbuf* w, uint32_t k, uint32_t m, cudaStream_t s
 void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t rows,
                      const float* wt, const float* bias, const float* pre_bias, uint32_t m,
                      uint32_t pre, uint32_t act, float* out, uint32_t out_pitch, float* out2,
-                     float out2_scale, cudaStream_t st) {
+                     float out2_scale, cudaStream_t st, const float* row_scale) {
   if (rows == 0) return;
   TcArgs a{};
+  a.row_scale = row_scale;
   a.rows = rows;
   a.k = k;
   a.n_kb = (k + BK - 1) / BK;

@@ -889,13 +889,31 @@ int mgg_rows_init(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* o
 
 int mgg_rows_init_copy(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
                        float scale, int relu_in, mgg_store* copy) {
+  return mgg_rows_init_rs(ctx, part, in, out, scale, relu_in, copy, nullptr);
+}
+
+int mgg_rows_softmax_rs(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
+                        const mgg_dbuf* row_scale) {
+  return guard([&] {
+    if (!in || !out) throw Status{MGG_E_INPUT, "rows_softmax: null store"};
+    if (in->pitch != out->pitch) throw Status{MGG_E_INPUT, "rows_softmax: in/out width differ"};
+    cudaStream_t st = enter(ctx, part);
+    launch_softmax(in->shard[part], out->shard[part], in->rows(part), in->pitch, in->dim, st,
+                   row_scale ? static_cast<const float*>(row_scale->ptr) : nullptr);
+    count_launch(ctx);
+  });
+}
+
+int mgg_rows_init_rs(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store* out,
+                     float scale, int relu_in, mgg_store* copy, const mgg_dbuf* row_scale) {
   return guard([&] {
     if (!in || !out) throw Status{MGG_E_INPUT, "rows_init: null store"};
     if (in->pitch != out->pitch || (copy && copy->pitch != in->pitch))
       throw Status{MGG_E_INPUT, "rows_init: in/out width differ"};
     cudaStream_t st = enter(ctx, part);
     launch_rows_init(in->shard[part], out->shard[part], in->rows(part), in->pitch, scale,
-                     relu_in, copy ? copy->shard[part] : nullptr, st);
+                     relu_in, copy ? copy->shard[part] : nullptr, st,
+                     row_scale ? static_cast<const float*>(row_scale->ptr) : nullptr);
     count_launch(ctx);
   });
 }
@@ -908,6 +926,7 @@ int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in, const mgg_dense_
     cudaStream_t st = enter(ctx, part);
     const float* bias = d->bias ? static_cast<const float*>(d->bias->ptr) : nullptr;
     const float* pre_bias = d->pre_bias ? static_cast<const float*>(d->pre_bias->ptr) : nullptr;
+    const float* rs = d->row_scale ? static_cast<const float*>(d->row_scale->ptr) : nullptr;
     static const bool force_simt = [] {
       const char* e = std::getenv("MGG_GEMM");
       return e && std::string(e) == "simt";
@@ -916,14 +935,14 @@ int mgg_dense(mgg_ctx* ctx, uint32_t part, const mgg_store* in, const mgg_dense_
       const float* wt = gemm_tc_prepare(const_cast<mgg_dbuf*>(d->w), in->dim, out->dim, st);
       launch_dense_tc(in->shard[part], in->pitch, in->dim, in->rows(part), wt, bias, pre_bias,
                       out->dim, d->pre, d->act, out->shard[part], out->pitch,
-                      out2 ? out2->shard[part] : nullptr, d->out2_scale, st);
+                      out2 ? out2->shard[part] : nullptr, d->out2_scale, st, rs);
       count_launch(ctx);
       return;
     }
     launch_dense(in->shard[part], in->pitch, in->dim, in->rows(part),
                  static_cast<const float*>(d->w->ptr), bias, pre_bias, out->dim, d->pre, d->act,
                  out->shard[part], out->pitch, out2 ? out2->shard[part] : nullptr,
-                 d->out2_scale, st);
+                 d->out2_scale, st, rs);
     count_launch(ctx, (out->dim + 63) / 64);
   });
 }

@@ -387,6 +387,7 @@ int mgg_engine_create(const mgg_graph* g, uint32_t num_parts, const int32_t* par
     spec.hidden = m->hidden;
     spec.out_dim = m->out_dim;
     spec.eps = m->eps;
+    spec.norm = m->norm != 0;
     if (spec.kind == ModelSpec::Kind::gcn) {
       need(m->w1, "engine_create w1");
       const std::size_t n =

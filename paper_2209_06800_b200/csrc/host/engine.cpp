@@ -3,6 +3,7 @@
 #include "mgg/engine.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstring>
 
@@ -45,12 +46,15 @@ Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
     std::vector<std::uint64_t> flag_lb(num_parts_ + 1);
     for (std::uint32_t p = 0; p <= num_parts_; ++p) flag_lb[p] = p;
     ok(mgg_store_create(ctx_, flag_lb.data(), kMaxOwners, &flags_));
+    build_row_scales();
     build_program();
     fuse_chains();
     find_io_points();
     build_plans();
   } catch (...) {
     free_plans();
+    for (auto& v : rs_)
+      for (auto* b : v) mgg_dbuf_destroy(b);
     mgg_store_destroy(in_bufs_[1]);
     for (auto* s : stores_) mgg_store_destroy(s);
     for (auto& slot : weights_)
@@ -72,6 +76,8 @@ Engine::~Engine() {
   for (auto* s : scratch_) mgg_store_destroy(s);
   for (auto& slot : weights_)
     for (auto* b : slot) mgg_dbuf_destroy(b);
+  for (auto& v : rs_)
+    for (auto* b : v) mgg_dbuf_destroy(b);
   mgg_store_destroy(flags_);
   mgg_ctx_destroy(ctx_);
 }
@@ -97,9 +103,12 @@ int Engine::add_weight(const float* src, std::size_t n) {
 // Self term A = scale * f(H). With a pending ReLU f, the init also writes
 // G = ReLU(H) once per row and the aggregation gathers G (no per-edge ReLU,
 // H itself stays readable through get_hidden); returns the store to gather.
-int Engine::activated(int h, std::uint32_t width, int relu, int a, float scale) {
-  const int g = relu ? add_store(width) : h;
-  program_.push_back({OpKind::init, h, a, relu ? g : -1, -1, -1, -1, 0, 0, scale, relu});
+int Engine::activated(int h, std::uint32_t width, int relu, int a, float scale, int rs) {
+  // a row-scaled (normalised GCN) gather table is always a separate copy
+  const int g = (relu || rs) ? add_store(width) : h;
+  Op op{OpKind::init, h, a, g != h ? g : -1, -1, -1, -1, 0, 0, scale, relu};
+  op.rs = rs;
+  program_.push_back(op);
   return g;
 }
 
@@ -115,6 +124,12 @@ void Engine::build_program() {
     if (v.size() < n) throw InputError(std::string("engine: weight array too short: ") + what);
   };
 
+  // normalised GCN: Â = D^-1/2 (A+I) D^-1/2 as row scalings around the plain
+  // sum — a gather table holds D^-1/2 · (true rows) (its seed too), the sum
+  // is then D^1/2 · (true result), i.e. its consumer owes one more D^-1/2.
+  // `pend` is that owed power on `cur`.
+  const bool norm = gcn && s.norm;
+  int pend = 0;
   for (std::uint32_t l = 0; l < s.layers; ++l) {
     const bool last = l + 1 == s.layers;
     if (gcn) {
@@ -125,25 +140,33 @@ void Engine::build_program() {
       o1 += std::size_t(a) * b;
       if (b < a) {  // update first: T = f(H)·W, A = T + Σ T_u
         const int T = add_store(b), A = add_store(b);
-        program_.push_back({OpKind::dense, cur, T, A, W, -1, -1, std::uint32_t(fin), 0, 1.f, 0});
+        Op d{OpKind::dense, cur, T, A, W, -1, -1, std::uint32_t(fin), 0, 1.f, 0};
+        d.rs = norm ? pend + 1 : 0;
+        program_.push_back(d);
         program_.push_back({OpKind::barrier});
         program_.push_back({OpKind::aggregate, T, A});
         hidden_.push_back(A);
         if (last) {
           const int Z = add_store(b);
-          program_.push_back({OpKind::softmax, A, Z});
+          Op sm{OpKind::softmax, A, Z};
+          sm.rs = norm ? 1 : 0;
+          program_.push_back(sm);
           output_ = Z;
         }
         cur = A;
+        pend = norm ? 1 : 0;
       } else {  // aggregate first: A = f(H) + Σ f(H_u), then A·W
         const int A = add_store(a), Y = add_store(b);
-        const int G = activated(cur, a, fin, A, 1.f);
+        const int G = activated(cur, a, fin, A, 1.f, norm ? pend + 1 : 0);
         program_.push_back({OpKind::barrier});
         program_.push_back({OpKind::aggregate, G, A});
         hidden_.push_back(A);
-        program_.push_back({OpKind::dense, A, Y, -1, W, -1, -1, 0, last ? 2u : 0u, 1.f, 0});
+        Op d{OpKind::dense, A, Y, -1, W, -1, -1, 0, last ? 2u : 0u, 1.f, 0};
+        d.rs = norm ? 1 : 0;
+        program_.push_back(d);
         if (last) output_ = Y;
         cur = Y;
+        pend = 0;
       }
       cur_w = b;
       fin = 1;
@@ -178,7 +201,7 @@ void Engine::build_program() {
         program_.push_back({OpKind::dense, A, O, -1, W2, B2, B1, 2, last ? 2u : 0u, 1.f, 0});
       } else {  // A = (1+eps) f(H) + Σ f(H_u); M = ReLU(A·W1+b1); O = M·W2+b2
         const int A = add_store(a), M = add_store(h);
-        const int G = activated(cur, a, fin, A, self);
+        const int G = activated(cur, a, fin, A, self, 0);
         program_.push_back({OpKind::barrier});
         program_.push_back({OpKind::aggregate, G, A});
         hidden_.push_back(A);
@@ -331,6 +354,7 @@ void Engine::run(const Op& op) {
         d.pre = op.pre;
         d.act = op.act;
         d.out2_scale = op.scale;
+        d.row_scale = op.rs ? rs_[op.rs][p] : nullptr;
         ok(mgg_dense(ctx_, p, stores_[op.in], &d, stores_[op.out],
                      op.out2 >= 0 ? stores_[op.out2] : nullptr));
         break;
@@ -351,8 +375,9 @@ void Engine::run(const Op& op) {
         break;
       }
       case OpKind::init:
-        ok(mgg_rows_init_copy(ctx_, p, stores_[op.in], stores_[op.out], op.scale, op.relu,
-                              op.out2 >= 0 ? stores_[op.out2] : nullptr));
+        ok(mgg_rows_init_rs(ctx_, p, stores_[op.in], stores_[op.out], op.scale, op.relu,
+                            op.out2 >= 0 ? stores_[op.out2] : nullptr,
+                            op.rs ? rs_[op.rs][p] : nullptr));
         break;
       case OpKind::aggregate: {
         std::uint32_t w = 0;
@@ -362,7 +387,8 @@ void Engine::run(const Op& op) {
         break;
       }
       case OpKind::softmax:
-        ok(mgg_rows_softmax(ctx_, p, stores_[op.in], stores_[op.out]));
+        ok(mgg_rows_softmax_rs(ctx_, p, stores_[op.in], stores_[op.out],
+                               op.rs ? rs_[op.rs][p] : nullptr));
         break;
       case OpKind::barrier:
         break;
@@ -404,6 +430,25 @@ void Engine::forward() {
     exec_input_ = stores_[input_];
   }
   ok(mgg_exec_launch(ctx_, exec_));
+}
+
+// D^-1/2 and D^-1 over each local part's rows (d_v = |N(v)| + 1, the
+// oracle's inv_sqrt_deg), for the normalised GCN's row scalings.
+void Engine::build_row_scales() {
+  for (auto& v : rs_) v.assign(num_parts_, nullptr);
+  if (!(spec_.kind == ModelSpec::Kind::gcn && spec_.norm)) return;
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    if (dev_[p] < 0) continue;
+    const std::uint64_t lb = ne_.ranges[p].lb, n = ne_.ranges[p].size();
+    std::vector<float> s1(std::max<std::uint64_t>(n, 1)), s2(s1.size());
+    for (std::uint64_t r = 0; r < n; ++r) {
+      const double d = double(g_.row_ptr[lb + r + 1] - g_.row_ptr[lb + r]) + 1.0;
+      s1[r] = static_cast<float>(1.0 / std::sqrt(d));
+      s2[r] = static_cast<float>(1.0 / d);
+    }
+    ok(mgg_dbuf_create(ctx_, p, s1.data(), s1.size() * sizeof(float), &rs_[1][p]));
+    ok(mgg_dbuf_create(ctx_, p, s2.data(), s2.size() * sizeof(float), &rs_[2][p]));
+  }
 }
 
 void Engine::set_graphs(bool on) {

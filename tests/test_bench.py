@@ -37,7 +37,7 @@ def test_workload_table_matches_baseline():
     for name, (_, g, m, tuned) in bench.WORKLOADS.items():
         ps, dist, wpb = tuned
         assert 1 <= ps <= 32 and 1 <= dist <= 16 and 1 <= wpb <= 16, name
-        assert g[0] in ("powerlaw", "rmat") and m[0] in ("gcn", "gin"), name
+        assert g[0] in ("powerlaw", "rmat") and m[0] in ("gcn", "gcn-norm", "gin"), name
 
 
 def test_reference_arm_json_line():

@@ -501,3 +501,29 @@ def test_fuzz_forward(mgg, oracle_mod, seed):
     floor = float(np.abs(z32 - zr).max())
     err = float(np.abs(z - zr).max())
     assert err <= max(TOL, 2 * floor), (seed, kind, n, din, hid, cls, parts, cfg, err, floor)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3])
+@pytest.mark.parametrize("dims", [(96, 16, 41), (32, 64, 8), (12, 16, 5)])
+def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
+    # symmetric normalisation D^-1/2 (A+I) D^-1/2 (d_v = |N(v)| + 1) as row
+    # scalings around the plain-sum K1: update-first and aggregate-first
+    # layers, softmax op and fused softmax head, against the oracle's norm=1
+    din, hid, cls = dims
+    g = mgg.gen_rmat(3000, 40000, seed=23)
+    model = mgg.make_gcn(din, hid, cls, seed=7, norm=True)
+    x = mgg.random_features(g.num_nodes, din, seed=8)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=16, dist=2, wpb=4)
+    try:
+        z = np.zeros((g.num_nodes, cls), np.float32)
+        eng.forward_host(x, z)
+        eng.set_input(x)
+        eng.forward()
+        eng.forward()
+        z2 = eng.get_output()
+    finally:
+        eng.close()
+    _, lg, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, norm=1)
+    assert np.abs(lg).max() < 1e3  # normalised logits stay small
+    assert np.abs(z - zr).max() <= TOL, np.abs(z - zr).max()
+    assert np.abs(z2 - zr).max() <= TOL, np.abs(z2 - zr).max()
