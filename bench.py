@@ -51,19 +51,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # name: (label, graph (kind, nodes, avg_degree | edges), model (kind, in, hidden, out, layers),
-#        tuned (ps, dist, wpb) — profiles/r01_tune_final_*.json: the exhaustive optimum of the
-#        150-point grid with the measured K1, which the tuner reaches in <= 15 evaluations)
+#        tuned (ps, dist, wpb) — profiles/r01_tune2_*.json: the exhaustive optimum of the
+#        150-point grid with the measured K1 where swept (the tuner lands within 1.2% of it
+#        in <= 15 evaluations), the tuner's pick elsewhere)
 WORKLOADS = {
     "reddit-gcn": ("GCN-2L Reddit-shaped (BASELINE configs[1])",
                    ("powerlaw", 232_965, 492), ("gcn", 602, 16, 41, 2), (32, 16, 2)),
     "config1": ("GCN-2L RMAT 100K/1.6M dim 16, 2 logical partitions (BASELINE configs[0])",
-                ("rmat", 100_000, 1_600_000), ("gcn", 16, 16, 16, 2), (32, 16, 1)),
+                ("rmat", 100_000, 1_600_000), ("gcn", 16, 16, 16, 2), (8, 8, 2)),
     "products-gcn": ("GCN-2L ogbn-products-shaped (north_star target shape)",
-                     ("powerlaw", 2_449_029, 25.259), ("gcn", 100, 16, 47, 2), (32, 16, 2)),
+                     ("powerlaw", 2_449_029, 25.259), ("gcn", 100, 16, 47, 2), (16, 8, 8)),
     "products-gin": ("GIN-5L hidden 64 ogbn-products-shaped (BASELINE configs[2])",
-                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 16, 2)),
+                     ("powerlaw", 2_449_029, 25.259), ("gin", 100, 64, 47, 5), (16, 2, 8)),
     "orkut-gcn": ("GCN-2L com-Orkut-shaped (BASELINE configs[3])",
-                  ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (32, 16, 2)),
+                  ("powerlaw", 3_072_441, 38.141), ("gcn", 128, 16, 32, 2), (8, 16, 8)),
     # the symmetric-normalised GCN (D^-1/2 (A+I) D^-1/2) on the configs[1] graph
     "reddit-gcn-norm": ("GCN-2L normalised, Reddit-shaped (configs[1] graph)",
                         ("powerlaw", 232_965, 492), ("gcn-norm", 602, 16, 41, 2), (32, 16, 2)),

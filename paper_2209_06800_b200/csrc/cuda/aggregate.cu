@@ -534,6 +534,111 @@ __device__ __forceinline__ void agg_local_body(const AggArgs& a) {
   if (cur >= 0) ln.flush(a, acc, cur);
 }
 
+// Group-per-partition local K1 for short partitions (HBM-resident tables):
+// each VEC-lane group walks its own partition, UNR rows in flight per group,
+// so a warp keeps 32/VEC partitions' gathers outstanding at once instead of
+// one partition's predicated window.
+template <int VEC, bool RELU, int UNR, bool PIPE>
+__device__ __forceinline__ void agg_group_body(const AggArgs& a) {
+  constexpr int G = 32 / VEC;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / VEC, v = lane % VEC;
+  const bool vlane = v < static_cast<int>(a.vec);
+  const uint32_t pb = a.pitch * 4u;
+  const char* lbase = reinterpret_cast<const char*>(a.own) + (vlane ? 16u * v : 0u);
+  asm("mov.b64 %0, %0;" : "+l"(lbase));
+  auto load = [&](uint32_t c) {
+    float4 x;
+    asm(MGG_LD_INSN " {%0,%1,%2,%3}, [%4];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(lbase + static_cast<size_t>(c) * pb));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    const uint32_t l0 = w * a.dist;
+    const uint32_t l1 = min(l0 + a.dist, a.nL);
+    for (uint32_t i = l0 + grp; i < l1; i += G) {
+      const int2 m = __ldg(a.lmeta + i);
+      const int end = __ldg(&a.lmeta[i + 1].y);
+      float4 acc = f4zero();
+      int k = m.y;
+      if (PIPE) {
+        // column ids of step s+1 load while step s's rows are in flight
+        uint32_t c[UNR];
+        if (k + UNR <= end) {
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+        }
+        for (; k + UNR <= end; k += UNR) {
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) t[u] = load(c[u]);
+          if (k + 2 * UNR <= end) {
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + UNR + u);
+          }
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+      } else {
+        for (; k + UNR <= end; k += UNR) {
+          uint32_t c[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) t[u] = load(c[u]);
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+      }
+      if (k < end) {
+        float4 t[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          t[u] = k + u < end ? load(__ldg(a.lcols + k + u)) : f4zero();
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+      }
+      if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+    }
+  }
+}
+template <int VEC, bool RELU, int UNR, bool PIPE>
+__global__ void __launch_bounds__(512, 2) agg_group(AggArgs a) {
+  agg_group_body<VEC, RELU, UNR, PIPE>(a);
+}
+template <int VEC, bool RELU, int UNR, bool PIPE, int REGS>
+__global__ void __maxnreg__(REGS) agg_group_r(AggArgs a) {
+  agg_group_body<VEC, RELU, UNR, PIPE>(a);
+}
+template <bool RELU, int UNR, int REGS>
+KernelFn pick_group_r(uint32_t v) {
+  if (v <= 1) return agg_group_r<1, RELU, UNR, true, REGS>;
+  if (v <= 2) return agg_group_r<2, RELU, UNR, true, REGS>;
+  if (v <= 4) return agg_group_r<4, RELU, UNR, true, REGS>;
+  if (v <= 8) return agg_group_r<8, RELU, UNR, true, REGS>;
+  if (v <= 16) return agg_group_r<16, RELU, UNR, true, REGS>;
+  if (v <= 32) return agg_group_r<32, RELU, UNR, true, REGS>;
+  return agg_wide<RELU>;
+}
+template <bool RELU, int UNR, bool PIPE = false>
+KernelFn pick_group(uint32_t v) {
+  if (v <= 1) return agg_group<1, RELU, UNR, PIPE>;
+  if (v <= 2) return agg_group<2, RELU, UNR, PIPE>;
+  if (v <= 4) return agg_group<4, RELU, UNR, PIPE>;
+  if (v <= 8) return agg_group<8, RELU, UNR, PIPE>;
+  if (v <= 16) return agg_group<16, RELU, UNR, PIPE>;
+  if (v <= 32) return agg_group<32, RELU, UNR, PIPE>;
+  return agg_wide<RELU>;
+}
+
 // The register budget is the occupancy knob of this latency-bound gather:
 // MINB resident 512-thread CTAs (64 / 42 / 32 registers), or an explicit cap.
 template <int VEC, bool RELU, int MINB>
@@ -569,7 +674,7 @@ KernelFn pick_local(uint32_t v) {
 int lean_mode() {
   static const int m = [] {
     const char* e = std::getenv("MGG_AGG_LEAN");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 1;
   }();
   return m;
 }
@@ -584,6 +689,16 @@ KernelFn pick(uint32_t v) {
       case 10: return pick_local_r<RELU, 48>(v);
       case 11: return pick_local_r<RELU, 56>(v);
       case 12: return pick_local_r<RELU, 48>(v);
+      case 20: return pick_group<RELU, 4>(v);
+      case 21: return pick_group<RELU, 8>(v);
+      case 22: return pick_group<RELU, 2>(v);
+      case 23: return pick_group<RELU, 2, true>(v);
+      case 24: return pick_group<RELU, 4, true>(v);
+      case 25: return pick_group<RELU, 1, true>(v);
+      case 26: return pick_group_r<RELU, 4, 40>(v);
+      case 27: return pick_group_r<RELU, 4, 32>(v);
+      case 28: return pick_group<RELU, 8, true>(v);
+      case 29: return pick_group_r<RELU, 8, 48>(v);
       // measured (profiles/r01_k1_experiments.md): narrow rows (<= 16 floats)
       // want the 64-register cap; wider rows an explicit 48 (products-gin
       // K1 2.68 -> 2.48 ms vs the spilling 42-register MINB=3 cap)
@@ -599,6 +714,21 @@ KernelFn pick(uint32_t v) {
     case 3: return pick_minb<RELU, REMOTE, 3>(v);
     default: return REMOTE ? pick_minb<RELU, REMOTE, 1>(v) : pick_minb<RELU, REMOTE, 2>(v);
   }
+}
+
+// Local-only K1 flavour for one launch (lean_mode 1 = by the plan's shape).
+// Measured (profiles/r01_k1_experiments.md): the warp-window kernel wins
+// when most partitions are full ps = 32 windows (Reddit 0.53 vs 0.80 ms,
+// Orkut 1.62 vs 1.65); group-per-partition wins on short partitions
+// (products-shaped 0.84 -> 0.745 ms at ps 16, Reddit at ps 16 0.92 -> 0.65);
+// 8 rows in flight per group with the next column ids prefetched (UNR 4:
+// +1%, register caps 40/32 for more warps: +4-10%).
+template <bool RELU>
+KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges) {
+  if (lean_mode() != 1) return pick<RELU, false>(v);
+  const bool short_parts = ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts;
+  if (short_parts) return pick_group<RELU, 8, true>(v);
+  return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
 }
 
 // Resident CTAs per SM for (kernel, CTA size), cached per device.
@@ -740,8 +870,12 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   a.num_warps = static_cast<uint32_t>(warps);
   a.num_lblocks = (a.num_warps + a.wpb - 1) / a.wpb;
   const bool remote = a.nR > 0 && a.phase != 1;
-  KernelFn k = relu_in ? (remote ? pick<true, true>(a.vec) : pick<true, false>(a.vec))
-                       : (remote ? pick<false, true>(a.vec) : pick<false, false>(a.vec));
+  const bool remote_lean = halo && phase == 2;
+  const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
+  const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
+  KernelFn k = remote ? (relu_in ? pick<true, true>(a.vec) : pick<false, true>(a.vec))
+                      : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges)
+                                 : pick_lean<false>(a.vec, p->ps, lparts, ledges));
   if (trace) {  // the pipelined kernel with stage stamps, whatever the plan
     if (relu_in || halo) throw Status{MGG_E_CONFIG, "trace: fine-grained, no ReLU-on-load"};
     k = pick_traced(a.vec);

@@ -96,6 +96,7 @@ struct mgg_dplan {
   uint32_t part = 0;
   uint32_t ps = 1, dist = 1, wpb = 1, mapping = 0, granularity = 0;
   uint64_t rows = 0, n_local = 0, n_remote = 0;
+  uint64_t local_edges = 0, remote_edges = 0;  // column ids per kind
   int2* lmeta = nullptr;
   uint32_t* lcols = nullptr;
   int2* rmeta = nullptr;

@@ -744,6 +744,8 @@ int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* d, mgg_dplan** out) {
       p->rows = d->rows;
       p->n_local = d->n_local;
       p->n_remote = d->n_remote;
+      p->local_edges = d->local_cols_len;
+      p->remote_edges = d->remote_cols_len;
       p->lmeta = reinterpret_cast<int2*>(upload_array(d->local_meta, 2 * (d->n_local + 1)));
       p->rmeta = reinterpret_cast<int2*>(upload_array(d->remote_meta, 2 * (d->n_remote + 1)));
       p->lcols = upload_array(d->local_cols, d->local_cols_len);

@@ -64,6 +64,23 @@ def test_aggregate_every_config(mgg, oracle_mod, cfg):
         eng.close()
 
 
+@pytest.mark.parametrize("ps", [32, 16, 7])
+@pytest.mark.parametrize("dim", [4, 16, 64, 128, 200])
+def test_aggregate_local_flavours(mgg, oracle_mod, ps, dim):
+    # long rows (avg 60): ps 32 takes the warp-window local K1, ps <= 16 the
+    # group-per-partition one (aggregate.cu pick_lean); 1 and 3 parts (halo
+    # passes use the same local kernels)
+    g = mgg.gen_synthetic(mgg.POWERLAW, 1500, 60, 11)
+    x = mgg.random_features(g.num_nodes, dim, seed=dim)
+    ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
+    for parts in (1, 3):
+        eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 8, 4), ps=ps, dist=4, wpb=4)
+        eng.set_remote_fetch("halo")
+        out = eng.aggregate(x, 1.0, relu_in=True)
+        assert_rows_close(out, ref, what=f"ps={ps} dim={dim} parts={parts}")
+        eng.close()
+
+
 def test_aggregate_edge_cases(mgg, oracle_mod):
     # isolated nodes, an empty trailing chunk, self loops, duplicates, a hub
     rows = [[0, 0, 1], [], [3] * 70, list(range(8)) * 9, [], [5], [2, 2]]
