@@ -628,6 +628,119 @@ KernelFn pick_group_r(uint32_t v) {
   if (v <= 32) return agg_group_r<32, RELU, UNR, true, REGS>;
   return agg_wide<RELU>;
 }
+// Group-per-partition form of the paired (fine-fetch) K1: group g of a
+// logical warp takes pairs i = g, g + 32/VEC, ... of the warp's local and
+// remote groups and keeps the reference's async discipline per pair
+// (R:proj/src/sim.cpp:102-125): issue the first PF peer rows of R_i, reduce
+// L_i, then consume R_i — per group instead of per warp.
+template <int VEC, bool RELU, int UNR, int PF>
+__device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
+  constexpr int G = 32 / VEC;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / VEC, v = lane % VEC;
+  const bool vlane = v < static_cast<int>(a.vec);
+  const uint32_t voff = vlane ? 16u * v : 0u;
+  const uint32_t pb = a.pitch * 4u;
+  const char* lbase = reinterpret_cast<const char*>(a.own) + voff;
+  asm("mov.b64 %0, %0;" : "+l"(lbase));
+  auto ld = [&](const char* p) {
+    float4 x;
+    asm(MGG_LD_INSN " {%0,%1,%2,%3}, [%4];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(p));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  auto raddr = [&](uint32_t c) {
+    const char* b =
+        a.halo ? reinterpret_cast<const char*>(a.halo)
+               : reinterpret_cast<const char*>(
+                     __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
+    return b + voff + static_cast<size_t>(c & kMask) * pb;
+  };
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    uint32_t l0, l1, r0, r1;
+    warp_groups(a, w, l0, l1, r0, r1);
+    const uint32_t nl = l1 - l0, nr = r1 - r0, n = max(nl, nr);
+    for (uint32_t i = grp; i < n; i += G) {
+      // (1) issue R_i's first PF peer rows
+      float4 pre[PF];
+      int rk = 0, rend = 0, rt = 0;
+      if (i < nr) {
+        const int2 m = __ldg(a.rmeta + r0 + i);
+        rend = __ldg(&a.rmeta[r0 + i + 1].y);
+        rt = m.x;
+        rk = m.y;
+#pragma unroll
+        for (int u = 0; u < PF; ++u)
+          pre[u] = rk + u < rend ? ld(raddr(__ldg(a.rcols + rk + u))) : f4zero();
+        rk = min(rk + PF, rend);
+      }
+      // (2) reduce L_i
+      if (i < nl) {
+        const int2 m = __ldg(a.lmeta + l0 + i);
+        const int end = __ldg(&a.lmeta[l0 + i + 1].y);
+        float4 acc = f4zero();
+        int k = m.y;
+        for (; k + UNR <= end; k += UNR) {
+          uint32_t c[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) t[u] = ld(lbase + static_cast<size_t>(c[u]) * pb);
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (k < end) {
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+            t[u] = k + u < end ? ld(lbase + static_cast<size_t>(__ldg(a.lcols + k + u)) * pb)
+                               : f4zero();
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+      }
+      // (3) consume R_i
+      if (i < nr) {
+        float4 acc = f4zero();
+#pragma unroll
+        for (int u = 0; u < PF; ++u) acc = f4add(acc, pre[u]);
+        for (; rk < rend; rk += UNR) {
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+            t[u] = rk + u < rend ? ld(raddr(__ldg(a.rcols + rk + u))) : f4zero();
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (vlane) red_add4(a.out + static_cast<size_t>(rt) * a.pitch + 4 * v, acc);
+      }
+    }
+  }
+}
+template <int VEC, bool RELU, int UNR, int PF>
+__global__ void __launch_bounds__(512, 2) agg_gpair(AggArgs a) {
+  agg_gpair_body<VEC, RELU, UNR, PF>(a);
+}
+template <bool RELU, int UNR, int PF>
+KernelFn pick_gpair(uint32_t v) {
+  if (v <= 1) return agg_gpair<1, RELU, UNR, PF>;
+  if (v <= 2) return agg_gpair<2, RELU, UNR, PF>;
+  if (v <= 4) return agg_gpair<4, RELU, UNR, PF>;
+  if (v <= 8) return agg_gpair<8, RELU, UNR, PF>;
+  if (v <= 16) return agg_gpair<16, RELU, UNR, PF>;
+  if (v <= 32) return agg_gpair<32, RELU, UNR, PF>;
+  return agg_wide<RELU>;
+}
+
 template <bool RELU, int UNR, bool PIPE = false>
 KernelFn pick_group(uint32_t v) {
   if (v <= 1) return agg_group<1, RELU, UNR, PIPE>;
@@ -724,11 +837,35 @@ KernelFn pick(uint32_t v) {
 // 8 rows in flight per group with the next column ids prefetched (UNR 4:
 // +1%, register caps 40/32 for more warps: +4-10%).
 template <bool RELU>
-KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges) {
+KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
+                   uint32_t granularity) {
   if (lean_mode() != 1) return pick<RELU, false>(v);
-  const bool short_parts = ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts;
+  const bool short_parts =
+      granularity == 0 && (ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts);
   if (short_parts) return pick_group<RELU, 8, true>(v);
   return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
+}
+
+int pair_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_PAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+
+// Paired (local + remote, fine fetch) K1 flavour. Measured (K1 ms per part,
+// profiles/r01_k1_experiments.md): the group-per-pair kernel beats the
+// warp-window pair loop on every shape and part count tried, full windows
+// included (Reddit 2 parts 0.494 -> 0.440, 8 parts 0.201 -> 0.160; products
+// at (16,8,8) 1.16 -> 0.50; Orkut at (8,16,8) 2.72 -> 0.91); UNR 8 or PF 8
+// spill at the 64-register cap and lose 5-20%, uncapped they lose occupancy.
+// MGG_AGG_PAIR=0 keeps the warp-window pair loop (ablations, A/B).
+// Whole-list plans (granularity 1, the no_np ablation) keep the warp per
+// list of the paper's baseline.
+template <bool RELU>
+KernelFn pick_pair(uint32_t v, uint32_t granularity) {
+  return pair_mode() == 0 || granularity == 1 ? pick<RELU, true>(v) : pick_gpair<RELU, 4, 4>(v);
 }
 
 // Resident CTAs per SM for (kernel, CTA size), cached per device.
@@ -873,9 +1010,10 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const bool remote_lean = halo && phase == 2;
   const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
-  KernelFn k = remote ? (relu_in ? pick<true, true>(a.vec) : pick<false, true>(a.vec))
-                      : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges)
-                                 : pick_lean<false>(a.vec, p->ps, lparts, ledges));
+  KernelFn k = remote ? (relu_in ? pick_pair<true>(a.vec, p->granularity)
+                                 : pick_pair<false>(a.vec, p->granularity))
+                      : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity)
+                                 : pick_lean<false>(a.vec, p->ps, lparts, ledges, p->granularity));
   if (trace) {  // the pipelined kernel with stage stamps, whatever the plan
     if (relu_in || halo) throw Status{MGG_E_CONFIG, "trace: fine-grained, no ReLU-on-load"};
     k = pick_traced(a.vec);
