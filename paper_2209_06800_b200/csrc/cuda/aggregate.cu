@@ -144,6 +144,19 @@ __device__ __forceinline__ void trace_emit(const AggArgs& a, uint32_t w, uint32_
                           (sm << 8) | (stage << 1) | (begin ? 1u : 0u), w);
 }
 
+// Group form (agg_gpair): the group's first lane records, id = w * groups + group.
+__device__ __forceinline__ void trace_emit_g(const AggArgs& a, uint32_t w, uint32_t id,
+                                             bool leader, uint32_t stage, bool begin,
+                                             uint64_t t) {
+  if (!leader || w >= a.trace_warps) return;
+  const unsigned long long i = atomicAdd(a.trace_n, 1ull);
+  if (i >= a.trace_cap) return;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  a.trace[i] = make_uint4(static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
+                          (sm << 8) | (stage << 1) | (begin ? 1u : 0u), id);
+}
+
 __device__ __forceinline__ const float* shfl_ptr(const float* p, int src) {
   const unsigned long long v = reinterpret_cast<unsigned long long>(p);
   return reinterpret_cast<const float*>(__shfl_sync(kFull, v, src));
@@ -633,7 +646,7 @@ KernelFn pick_group_r(uint32_t v) {
 // remote groups and keeps the reference's async discipline per pair
 // (R:proj/src/sim.cpp:102-125): issue the first PF peer rows of R_i, reduce
 // L_i, then consume R_i — per group instead of per warp.
-template <int VEC, bool RELU, int UNR, int PF>
+template <int VEC, bool RELU, int UNR, int PF, bool TRACE = false>
 __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -671,7 +684,9 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
       // (1) issue R_i's first PF peer rows
       float4 pre[PF];
       int rk = 0, rend = 0, rt = 0;
+      const uint32_t tid = w * G + grp;
       if (i < nr) {
+        if (TRACE) trace_emit_g(a, w, tid, v == 0, kLR, true, stamp_after(0.f));
         const int2 m = __ldg(a.rmeta + r0 + i);
         rend = __ldg(&a.rmeta[r0 + i + 1].y);
         rt = m.x;
@@ -686,6 +701,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
         const int2 m = __ldg(a.lmeta + l0 + i);
         const int end = __ldg(&a.lmeta[l0 + i + 1].y);
         float4 acc = f4zero();
+        if (TRACE) trace_emit_g(a, w, tid, v == 0, kLL, true, stamp_after(0.f));
         int k = m.y;
         for (; k + UNR <= end; k += UNR) {
           uint32_t c[UNR];
@@ -706,11 +722,17 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
 #pragma unroll
           for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
         }
+        if (TRACE) trace_emit_g(a, w, tid, v == 0, kLL, false, stamp_after(acc.x));
         if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
       // (3) consume R_i
       if (i < nr) {
         float4 acc = f4zero();
+        if (TRACE) {  // R_i's issued rows have landed: the get ends, AC starts
+          const uint64_t t = stamp_after(pre[PF - 1].x);
+          trace_emit_g(a, w, tid, v == 0, kLR, false, t);
+          trace_emit_g(a, w, tid, v == 0, kAC, true, t);
+        }
 #pragma unroll
         for (int u = 0; u < PF; ++u) acc = f4add(acc, pre[u]);
         for (; rk < rend; rk += UNR) {
@@ -721,10 +743,15 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
 #pragma unroll
           for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
         }
+        if (TRACE) trace_emit_g(a, w, tid, v == 0, kAC, false, stamp_after(acc.x));
         if (vlane) red_add4(a.out + static_cast<size_t>(rt) * a.pitch + 4 * v, acc);
       }
     }
   }
+}
+template <int VEC, int PF>
+__global__ void __launch_bounds__(512, 2) agg_gpair_traced(AggArgs a) {
+  agg_gpair_body<VEC, false, 4, PF, true>(a);
 }
 template <int VEC, bool RELU, int UNR, int PF>
 __global__ void __launch_bounds__(512, 2) agg_gpair(AggArgs a) {
@@ -953,6 +980,16 @@ void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st) {
   MGG_CUDA(cudaGetLastError());
 }
 
+KernelFn pick_traced_g(uint32_t v) {
+  if (v <= 1) return agg_gpair_traced<1, 4>;
+  if (v <= 2) return agg_gpair_traced<2, 4>;
+  if (v <= 4) return agg_gpair_traced<4, 4>;
+  if (v <= 8) return agg_gpair_traced<8, 4>;
+  if (v <= 16) return agg_gpair_traced<16, 4>;
+  if (v <= 32) return agg_gpair_traced<32, 4>;
+  throw Status{MGG_E_CONFIG, "trace: rows wider than 128 floats are not traced"};
+}
+
 KernelFn pick_traced(uint32_t v) {
   if (v <= 1) return agg_kernel<1, false, true, 1, true>;
   if (v <= 2) return agg_kernel<2, false, true, 1, true>;
@@ -1016,7 +1053,9 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                                  : pick_lean<false>(a.vec, p->ps, lparts, ledges, p->granularity));
   if (trace) {  // the pipelined kernel with stage stamps, whatever the plan
     if (relu_in || halo) throw Status{MGG_E_CONFIG, "trace: fine-grained, no ReLU-on-load"};
-    k = pick_traced(a.vec);
+    // the pair kernel that runs untraced: group-per-pair unless the
+    // warp-window loop is selected (MGG_AGG_PAIR=0) or the plan is whole-list
+    k = pair_mode() == 0 || p->granularity == 1 ? pick_traced(a.vec) : pick_traced_g(a.vec);
     a.trace = reinterpret_cast<uint4*>(trace->events);
     a.trace_n = reinterpret_cast<unsigned long long*>(trace->count);
     a.trace_cap = trace->capacity;
