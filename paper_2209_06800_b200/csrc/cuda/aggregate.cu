@@ -26,6 +26,12 @@
 // flight per lane. A target's partials fold across the RPW row groups with
 // xor-shuffles and land in `out` with one 128-bit vector reduction
 // (REDG.ADD.F32x4) per lane, only when the warp's target changes.
+//
+// Group-per-partition forms (agg_group local-only, agg_gpair paired): the
+// same plan geometry, but each VEC-lane group of a warp walks its own
+// partitions (pairs) with 4-8 rows in flight, so short partitions keep
+// 32/VEC gather streams per warp busy. The launcher picks the form per
+// launch from the plan's shape (pick_lean / pick_pair below).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
