@@ -493,14 +493,22 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
       auto stage_and_store = [&](const CUtensorMap* map, float scale) {
         if (lane == 0) bulk_wait_read0();  // the previous store has left the staging
         __syncwarp();
+        // columns >= m are exact zeros (W^T and bias zero-padded, softmax
+        // zeroes them), so they are staged as they are, no per-column select
+        if (scale == 1.f) {
 #pragma unroll
-        for (int c = 0; c < NP; c += 4) {
-          const int b = c / 32, c4 = (c % 32) / 4;
-          *reinterpret_cast<float4*>(ep + b * 4096 + lane * 128 + ((c4 ^ (lane & 7)) << 4)) =
-              make_float4(c + 0 < (int)a.m ? y[c + 0] * scale : 0.f,
-                          c + 1 < (int)a.m ? y[c + 1] * scale : 0.f,
-                          c + 2 < (int)a.m ? y[c + 2] * scale : 0.f,
-                          c + 3 < (int)a.m ? y[c + 3] * scale : 0.f);
+          for (int c = 0; c < NP; c += 4) {
+            const int b = c / 32, c4 = (c % 32) / 4;
+            *reinterpret_cast<float4*>(ep + b * 4096 + lane * 128 + ((c4 ^ (lane & 7)) << 4)) =
+                make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NP; c += 4) {
+            const int b = c / 32, c4 = (c % 32) / 4;
+            *reinterpret_cast<float4*>(ep + b * 4096 + lane * 128 + ((c4 ^ (lane & 7)) << 4)) =
+                make_float4(y[c] * scale, y[c + 1] * scale, y[c + 2] * scale, y[c + 3] * scale);
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -521,6 +529,7 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
         }
       }
       if (a.out2) stage_and_store(&map_out2, a.out2_scale);
+      float oscale = 1.f;  // softmax: 1/sum, applied while staging
       if (a.act == 1) {
 #pragma unroll
         for (int c = 0; c < NP; ++c) y[c] = fmaxf(y[c], 0.f);
@@ -535,11 +544,9 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
           y[c] = c < static_cast<int>(a.m) ? __expf(y[c] - mx) : 0.f;
           sum += y[c];
         }
-        const float inv = 1.f / sum;
-#pragma unroll
-        for (int c = 0; c < NP; ++c) y[c] *= inv;
+        oscale = 1.f / sum;
       }
-      stage_and_store(&map_out, 1.f);
+      stage_and_store(&map_out, oscale);
     }
     if (lane == 0) bulk_wait0();  // stores complete before the CTA's smem goes away
   }
