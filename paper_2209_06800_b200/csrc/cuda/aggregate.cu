@@ -554,10 +554,11 @@ __device__ __forceinline__ void agg_local_body(const AggArgs& a) {
 }
 
 // Group-per-partition local K1 for short partitions (HBM-resident tables):
-// each VEC-lane group walks its own partition, UNR rows in flight per group,
+// each VEC-lane group walks its own partition, UNR rows in flight per group
+// (the next UNR column ids prefetched),
 // so a warp keeps 32/VEC partitions' gathers outstanding at once instead of
 // one partition's predicated window.
-template <int VEC, bool RELU, int UNR, bool PIPE>
+template <int VEC, bool RELU, int UNR>
 __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -587,35 +588,22 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
       const int end = __ldg(&a.lmeta[i + 1].y);
       float4 acc = f4zero();
       int k = m.y;
-      if (PIPE) {
-        // column ids of step s+1 load while step s's rows are in flight
-        uint32_t c[UNR];
-        if (k + UNR <= end) {
+      // column ids of step s+1 load while step s's rows are in flight
+      uint32_t c[UNR];
+      if (k + UNR <= end) {
 #pragma unroll
-          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+        for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+      }
+      for (; k + UNR <= end; k += UNR) {
+        float4 t[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) t[u] = load(c[u]);
+        if (k + 2 * UNR <= end) {
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + UNR + u);
         }
-        for (; k + UNR <= end; k += UNR) {
-          float4 t[UNR];
 #pragma unroll
-          for (int u = 0; u < UNR; ++u) t[u] = load(c[u]);
-          if (k + 2 * UNR <= end) {
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + UNR + u);
-          }
-#pragma unroll
-          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
-        }
-      } else {
-        for (; k + UNR <= end; k += UNR) {
-          uint32_t c[UNR];
-#pragma unroll
-          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
-          float4 t[UNR];
-#pragma unroll
-          for (int u = 0; u < UNR; ++u) t[u] = load(c[u]);
-#pragma unroll
-          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
-        }
+        for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
       }
       if (k < end) {
         float4 t[UNR];
@@ -628,24 +616,6 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
       if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
     }
   }
-}
-template <int VEC, bool RELU, int UNR, bool PIPE>
-__global__ void __launch_bounds__(512, 2) agg_group(AggArgs a) {
-  agg_group_body<VEC, RELU, UNR, PIPE>(a);
-}
-template <int VEC, bool RELU, int UNR, bool PIPE, int REGS>
-__global__ void __maxnreg__(REGS) agg_group_r(AggArgs a) {
-  agg_group_body<VEC, RELU, UNR, PIPE>(a);
-}
-template <bool RELU, int UNR, int REGS>
-KernelFn pick_group_r(uint32_t v) {
-  if (v <= 1) return agg_group_r<1, RELU, UNR, true, REGS>;
-  if (v <= 2) return agg_group_r<2, RELU, UNR, true, REGS>;
-  if (v <= 4) return agg_group_r<4, RELU, UNR, true, REGS>;
-  if (v <= 8) return agg_group_r<8, RELU, UNR, true, REGS>;
-  if (v <= 16) return agg_group_r<16, RELU, UNR, true, REGS>;
-  if (v <= 32) return agg_group_r<32, RELU, UNR, true, REGS>;
-  return agg_wide<RELU>;
 }
 // Group-per-partition form of the paired (fine-fetch) K1: group g of a
 // logical warp takes pairs i = g, g + 32/VEC, ... of the warp's local and
@@ -774,14 +744,18 @@ KernelFn pick_gpair(uint32_t v) {
   return agg_wide<RELU>;
 }
 
-template <bool RELU, int UNR, bool PIPE = false>
+template <int VEC, bool RELU, int UNR>
+__global__ void __launch_bounds__(512, 2) agg_group(AggArgs a) {
+  agg_group_body<VEC, RELU, UNR>(a);
+}
+template <bool RELU, int UNR>
 KernelFn pick_group(uint32_t v) {
-  if (v <= 1) return agg_group<1, RELU, UNR, PIPE>;
-  if (v <= 2) return agg_group<2, RELU, UNR, PIPE>;
-  if (v <= 4) return agg_group<4, RELU, UNR, PIPE>;
-  if (v <= 8) return agg_group<8, RELU, UNR, PIPE>;
-  if (v <= 16) return agg_group<16, RELU, UNR, PIPE>;
-  if (v <= 32) return agg_group<32, RELU, UNR, PIPE>;
+  if (v <= 1) return agg_group<1, RELU, UNR>;
+  if (v <= 2) return agg_group<2, RELU, UNR>;
+  if (v <= 4) return agg_group<4, RELU, UNR>;
+  if (v <= 8) return agg_group<8, RELU, UNR>;
+  if (v <= 16) return agg_group<16, RELU, UNR>;
+  if (v <= 32) return agg_group<32, RELU, UNR>;
   return agg_wide<RELU>;
 }
 
@@ -829,22 +803,13 @@ template <bool RELU, bool REMOTE>
 KernelFn pick(uint32_t v) {
   if (!REMOTE && lean_mode() > 0) {
     switch (lean_mode()) {
+      // A/B knobs (MGG_AGG_LEAN; 1 = by plan shape, pick_lean; 2 = always the
+      // warp-window kernel below): 3 = MINB 3 cap, 10 = 48 registers at every
+      // width, 20 = always group-per-partition. The other variants measured
+      // are in profiles/r01_k1_experiments.md.
       case 3: return pick_local<RELU, 3>(v);
-      case 4: return pick_local<RELU, 4>(v);
-      case 5: return pick_local<RELU, 2>(v);
       case 10: return pick_local_r<RELU, 48>(v);
-      case 11: return pick_local_r<RELU, 56>(v);
-      case 12: return pick_local_r<RELU, 48>(v);
-      case 20: return pick_group<RELU, 4>(v);
-      case 21: return pick_group<RELU, 8>(v);
-      case 22: return pick_group<RELU, 2>(v);
-      case 23: return pick_group<RELU, 2, true>(v);
-      case 24: return pick_group<RELU, 4, true>(v);
-      case 25: return pick_group<RELU, 1, true>(v);
-      case 26: return pick_group_r<RELU, 4, 40>(v);
-      case 27: return pick_group_r<RELU, 4, 32>(v);
-      case 28: return pick_group<RELU, 8, true>(v);
-      case 29: return pick_group_r<RELU, 8, 48>(v);
+      case 20: return pick_group<RELU, 8>(v);
       // measured (profiles/r01_k1_experiments.md): narrow rows (<= 16 floats)
       // want the 64-register cap; wider rows an explicit 48 (products-gin
       // K1 2.68 -> 2.48 ms vs the spilling 42-register MINB=3 cap)
@@ -875,7 +840,7 @@ KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
   if (lean_mode() != 1) return pick<RELU, false>(v);
   const bool short_parts =
       granularity == 0 && (ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts);
-  if (short_parts) return pick_group<RELU, 8, true>(v);
+  if (short_parts) return pick_group<RELU, 8>(v);
   return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
 }
 
