@@ -164,6 +164,11 @@ __device__ __forceinline__ void tmem_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
@@ -534,14 +539,19 @@ __global__ void __launch_bounds__(kThreadsFor<EG>, 1)
 #pragma unroll
         for (int c = 0; c < NP; ++c) y[c] = fmaxf(y[c], 0.f);
       } else if (a.act == 2) {
+        // NP = round16(m): only the last 16 columns can be padding, so the
+        // column test is compile-time true elsewhere
+        const int m = static_cast<int>(a.m);
         float mx = -FLT_MAX;
 #pragma unroll
         for (int c = 0; c < NP; ++c)
-          if (c < static_cast<int>(a.m)) mx = fmaxf(mx, y[c]);
+          if (c < NP - 16 || c < m) mx = fmaxf(mx, y[c]);
+        // e^(y - mx) = 2^(y·log2e - mx·log2e): one FFMA + MUFU.EX2 per column
+        const float l2e = 1.4426950408889634f, off = -mx * l2e;
         float sum = 0.f;
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
-          y[c] = c < static_cast<int>(a.m) ? __expf(y[c] - mx) : 0.f;
+          y[c] = (c < NP - 16 || c < m) ? ex2_approx(fmaf(y[c], l2e, off)) : 0.f;
           sum += y[c];
         }
         oscale = 1.f / sum;
