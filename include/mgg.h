@@ -464,6 +464,11 @@ int mgg_engine_get_hidden(mgg_engine* e, uint32_t which, float* rows, uint32_t* 
  * part): out = self_scale*f(x) + Σ f(x_u); x/out num_nodes x dim host rows. */
 int mgg_engine_aggregate_host(mgg_engine* e, const float* x, uint32_t dim,
                               float self_scale, int relu_in, float* out);
+/* The same restricted to one kind of partition: phase 1 = local only, 2 =
+ * remote only (the phase-separated ablation's halves; their sums add up to
+ * the full aggregation). */
+int mgg_engine_aggregate_phase_host(mgg_engine* e, const float* x, uint32_t dim,
+                                    float self_scale, int relu_in, int phase, float* out);
 /* Median-of-reps K1 latency (ns) at aggregation width `dim` for the current
  * config, max over local parts — the tuner's SimulateFn. */
 int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps,

@@ -89,9 +89,10 @@ class Engine {
   /// Post-aggregation accumulator of layer `which` (N x width host rows).
   std::uint32_t get_hidden(std::uint32_t which, float* rows);
 
-  /// Standalone K1 through the engine's plans (single-process only).
+  /// Standalone K1 through the engine's plans (single-process only);
+  /// phase 1 = local partitions only, 2 = remote only (0 = both).
   void aggregate_host(const float* x, std::uint32_t dim, float self_scale,
-                      bool relu_in, float* out);
+                      bool relu_in, float* out, int phase = 0);
   /// Median K1 ns at width `dim`, max over local parts (tuner SimulateFn).
   std::uint64_t time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase);
   /// Device event trace of one K1 at width `dim` on every local part, in the

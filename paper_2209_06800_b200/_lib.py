@@ -161,6 +161,7 @@ _sig("mgg_lane_wait_host", I, vp, U32, U32)
 _sig("mgg_lane_wait_mark", I, vp, U32, I, U32)
 _sig("mgg_engine_get_hidden", I, vp, U32, f32p, u32p)
 _sig("mgg_engine_aggregate_host", I, vp, f32p, U32, C.c_float, I, f32p)
+_sig("mgg_engine_aggregate_phase_host", I, vp, f32p, U32, C.c_float, I, I, f32p)
 _sig("mgg_engine_time_aggregate", I, vp, U32, U32, I, u64p)
 _sig("mgg_engine_stats", I, vp, u64p)
 _sig("mgg_engine_trace_csv", I, vp, U32, U64, U32, C.POINTER(C.c_void_p))

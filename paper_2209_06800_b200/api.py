@@ -474,11 +474,18 @@ class Engine:
         check(lib.mgg_engine_get_hidden(self._h, which, _p(out, C.c_float), C.byref(w)))
         return out
 
-    def aggregate(self, x: np.ndarray, self_scale: float = 1.0, relu_in: bool = False):
+    def aggregate(self, x: np.ndarray, self_scale: float = 1.0, relu_in: bool = False,
+                  phase: int = 0):
+        """out = self_scale*f(x) + sum of f(x_u); phase 1/2 = local/remote partitions only."""
         x = np.ascontiguousarray(x, np.float32)
         out = np.zeros_like(x)
-        check(lib.mgg_engine_aggregate_host(self._h, _p(x, C.c_float), x.shape[1],
-                                            self_scale, int(relu_in), _p(out, C.c_float)))
+        if phase:
+            check(lib.mgg_engine_aggregate_phase_host(self._h, _p(x, C.c_float), x.shape[1],
+                                                      self_scale, int(relu_in), phase,
+                                                      _p(out, C.c_float)))
+        else:
+            check(lib.mgg_engine_aggregate_host(self._h, _p(x, C.c_float), x.shape[1],
+                                                self_scale, int(relu_in), _p(out, C.c_float)))
         return out
 
     def time_aggregate(self, dim: int, reps: int = 5, phase: int = 0) -> int:

@@ -502,6 +502,10 @@ int mgg_engine_aggregate_host(mgg_engine* e, const float* x, uint32_t dim, float
                               int relu_in, float* out) {
   return guard([&] { e->e->aggregate_host(x, dim, self_scale, relu_in != 0, out); });
 }
+int mgg_engine_aggregate_phase_host(mgg_engine* e, const float* x, uint32_t dim,
+                                    float self_scale, int relu_in, int phase, float* out) {
+  return guard([&] { e->e->aggregate_host(x, dim, self_scale, relu_in != 0, out, phase); });
+}
 int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps, int phase,
                               uint64_t* ns) {
   return guard([&] { *ns = e->e->time_aggregate(dim, reps, phase); });

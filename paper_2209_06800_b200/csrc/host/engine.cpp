@@ -674,7 +674,8 @@ mgg_store* Engine::scratch(std::uint32_t dim, int slot) {
 }
 
 void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
-                            bool relu_in, float* out) {
+                            bool relu_in, float* out, int phase) {
+  if (phase < 0 || phase > 2) throw InputError("engine: aggregate phase must be 0, 1 or 2");
   for (auto d : dev_)
     if (d < 0) throw InputError("engine: aggregate_host needs every part in this process");
   mgg_store* in = scratch(dim, 0);
@@ -684,7 +685,7 @@ void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
     ok(mgg_rows_init(ctx_, p, in, acc, self_scale, relu_in ? 1 : 0));
   ok(mgg_barrier(ctx_, flags_));
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
-    mgg_agg_opts o{relu_in ? 1 : 0, 0, halo_for(p, dim), 1};
+    mgg_agg_opts o{relu_in ? 1 : 0, phase, halo_for(p, dim), 1};
     ok(mgg_aggregate(ctx_, plans_[p], in, acc, &o));
   }
   ok(mgg_store_download(acc, out, 0, g_.num_nodes, dim));

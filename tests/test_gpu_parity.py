@@ -284,6 +284,27 @@ def test_ablation_mappings_match_oracle(mgg, oracle_mod, mapping, granularity, p
         eng.close()
 
 
+@pytest.mark.parametrize("fetch", ["fine", "halo"])
+@pytest.mark.parametrize("mapping", [0, 1])
+def test_phase_halves_sum_to_aggregate(mgg, oracle_mod, fetch, mapping):
+    # phase 1 (local partitions) + phase 2 (remote partitions) = the full sum:
+    # the phase-separated ablation runs the same partitions, just split
+    g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 18, 12)
+    for dim, cfg in ((16, (16, 4, 4)), (64, (32, 2, 2)), (200, (8, 4, 2))):
+        x = mgg.random_features(g.num_nodes, dim, seed=dim + 5)
+        eng = mgg.Engine(g, 3, [0, 0, 0], mgg.make_gcn(dim, 8, 4), *cfg)
+        eng.set_mapping(mapping, 0)
+        eng.set_remote_fetch(fetch)
+        loc = eng.aggregate(x, 1.0, relu_in=True, phase=1)
+        rem = eng.aggregate(x, 0.0, relu_in=True, phase=2)
+        ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
+        assert_rows_close(loc + rem, ref, what=f"phases {fetch} map={mapping} dim={dim}")
+        assert np.abs(rem).max() > 0 and np.abs(loc - np.maximum(x, 0)).max() > 0
+        with pytest.raises(mgg.MggError):
+            eng.aggregate(x, 1.0, phase=3)
+        eng.close()
+
+
 @pytest.mark.parametrize("fetch", ["fine", "halo", "auto"])
 @pytest.mark.parametrize("parts", [2, 3, 4])
 def test_remote_fetch_modes(mgg, oracle_mod, fetch, parts):
