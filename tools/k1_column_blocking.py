@@ -1,3 +1,7 @@
+#!/usr/bin/env python
+"""Column-blocked K1 probe (not adopted): split the columns into B ranges, one K1
+pass per range over the same output; sums the per-pass times.
+profiles/r01_k1_column_blocking.jsonl."""
 import json, sys
 import numpy as np
 sys.path.insert(0, '.')

@@ -1,3 +1,7 @@
+#!/usr/bin/env python
+"""Fine-fetch (paired) K1 time per pair-kernel variant (MGG_AGG_PAIR) at 2 and 8
+logical parts. Variants 2-6 of profiles/r01_k1_variants/pair_variants.jsonl are
+from the experiment build at commit d90d2b5; now 0 = warp-window, 1 = agg_gpair."""
 import json, os, sys
 sys.path.insert(0, '.')
 import bench

@@ -1,3 +1,6 @@
+#!/usr/bin/env python
+"""K1 time vs gather-table size at ~61M edges, width 16 (node count swept):
+profiles/r01_k1_table_size.jsonl."""
 import json, sys
 sys.path.insert(0, '.')
 import paper_2209_06800_b200 as mgg

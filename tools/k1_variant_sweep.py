@@ -1,3 +1,8 @@
+#!/usr/bin/env python
+"""K1 time per local-kernel variant (MGG_AGG_LEAN) and config, 1 part.
+The variant numbers 20-29 of profiles/r01_k1_variants/*.jsonl refer to the
+experiment build at commit d90d2b5 (aggregate.cu pick()); since ad84700 only
+1 (auto), 2 (warp-window), 3, 10 and 20 (group) remain."""
 import json, os, sys
 sys.path.insert(0, '.')
 import bench
