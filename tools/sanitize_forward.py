@@ -21,4 +21,18 @@ for model, parts, fetch in [(mgg.make_gcn(100, 16, 41, seed=1), 1, "auto"),
     z = np.zeros((g.num_nodes, model.out_dim), np.float32)
     eng.forward_host(x, z)
     eng.close()
+# K1 variants: group / group-per-pair at several widths, phases, whole-list,
+# and the traced pair kernel
+for dim in (3, 16, 64, 200):
+    x = mgg.random_features(g.num_nodes, dim, seed=dim)
+    for ps, parts, fetch in ((32, 1, "auto"), (8, 1, "auto"), (16, 3, "fine"), (16, 3, "halo")):
+        eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 8, 4), ps=ps, dist=4, wpb=2)
+        eng.set_remote_fetch(fetch)
+        for phase in (0, 1, 2):
+            eng.aggregate(x, 1.0, relu_in=True, phase=phase)
+        if parts > 1 and fetch == "fine" and dim <= 128:
+            eng.trace_csv(dim, capacity=1 << 12)
+        eng.set_mapping(0, 1)
+        eng.aggregate(x, 1.0)
+        eng.close()
 print("sanitize run ok")
