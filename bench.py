@@ -165,6 +165,15 @@ class ClockSampler:
         num = [float(x) if x.replace(".", "").isdigit() else float("nan") for x in f[:2]]
         self.samples.append((num[0], num[1], mask))
 
+    def sample_now(self):
+        """One sample from the calling thread (used right after the timed work
+        is queued, while the device is still executing it)."""
+        try:
+            if self._nvml:
+                self._sample_nvml()
+        except Exception:  # noqa: BLE001
+            pass
+
     def _run(self):
         while not self._stop.is_set():
             try:
@@ -376,6 +385,7 @@ def main():
         for _ in range(args.steps):
             eng.forward()  # CUDA-graph replay on a single-device context
         lib.mgg_event_record(ctx, my_part, 100001)
+        clk.sample_now()  # the queued steps are still running
         eng.synchronize()
         if world > 1:
             dist.barrier()
