@@ -75,3 +75,15 @@ def test_product_arm_fails_loudly_without_gpu(mgg):
         capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode != 0
     assert "no CUDA device" in (out.stderr + out.stdout)
+
+
+def test_traffic_table_covers_every_workload():
+    # roofline.traffic comes from the committed ncu capture of each workload's
+    # tuned config (profiles/k1_traffic.json); a retune must come with a capture
+    import types
+    for name, (_, g, _, tuned) in bench.WORKLOADS.items():
+        ps, dist, wpb = tuned
+        parts = 2 if name == "config1" else 1
+        args = types.SimpleNamespace(workload=name, ps=ps, dist=dist, wpb=wpb)
+        t = bench._traffic(args, parts)
+        assert t is not None and t > 0, f"no ncu traffic for {name} {tuned} parts={parts}"
