@@ -827,6 +827,14 @@ KernelFn pick(uint32_t v) {
   }
 }
 
+int group_unroll() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_GROUP_UNR");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 // Local-only K1 flavour for one launch (lean_mode 1 = by the plan's shape).
 // Measured (profiles/r01_k1_experiments.md): the warp-window kernel wins
 // when most partitions are full ps = 32 windows (Reddit 0.53 vs 0.80 ms,
@@ -840,7 +848,9 @@ KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
   if (lean_mode() != 1) return pick<RELU, false>(v);
   const bool short_parts =
       granularity == 0 && (ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts);
-  if (short_parts) return pick_group<RELU, 8>(v);
+  // 8 rows in flight per group; MGG_AGG_GROUP_UNR=4 (A/B) is 8% faster on the
+  // skewed Orkut-RMAT shape and 1-2% slower on the uniform ones
+  if (short_parts) return group_unroll() == 4 ? pick_group<RELU, 4>(v) : pick_group<RELU, 8>(v);
   return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
 }
 
