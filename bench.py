@@ -230,6 +230,17 @@ def agg_widths(model):
     return [min(dims[l], model.hidden) for l in range(model.layers)]
 
 
+def k1_form(row_ptr, ps: int, parts: int) -> str:
+    """Which local K1 a single-device launch runs (the launcher's rule,
+    csrc/cuda/aggregate.cu pick_lean; multi-part fine launches use agg_gpair)."""
+    if parts > 1:
+        return "agg_gpair (group per pair) / agg_group halo passes"
+    deg = np.diff(np.asarray(row_ptr, dtype=np.int64))
+    nparts = int(((deg + ps - 1) // ps).sum())
+    short = ps <= 16 or 3 * int(deg.sum()) < 2 * ps * nparts
+    return "agg_group (group per partition)" if short else "agg_local (warp window)"
+
+
 def agg_bytes(edges: int, parts: int, rows: int, dim: int) -> int:
     """Algorithmic bytes of one K1 launch at width dim: gathered
     rows + 4-B column ids + 8-B partition records + accumulator read/write."""
@@ -500,7 +511,9 @@ def main():
                        "remote_fetch": args.fetch,
                        "l2": "inputs larger than L2 (X + CSR >= 1 GB), no flush",
                        "layer_forward_ms": round(ms_step, 4)},
-            "roofline": {"bound": "hbm", "kernel": f"K1 aggregation, width {w0}",
+            "roofline": {"bound": "hbm",
+                         "kernel": f"K1 aggregation, width {w0}: "
+                                   f"{k1_form(g.row_ptr, args.ps, n)}",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": _traffic(args, n),

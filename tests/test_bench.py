@@ -87,3 +87,14 @@ def test_traffic_table_covers_every_workload():
         args = types.SimpleNamespace(workload=name, ps=ps, dist=dist, wpb=wpb)
         t = bench._traffic(args, parts)
         assert t is not None and t > 0, f"no ncu traffic for {name} {tuned} parts={parts}"
+
+
+def test_k1_form_rule():
+    # mirrors pick_lean: ps <= 16 or partitions under 2/3 full -> group kernel
+    import numpy as np
+    full = np.arange(0, 33 * 100, 33)          # rows of 33 -> windows 32 + 1 (avg 16.5)
+    assert bench.k1_form(full, 32, 1).startswith("agg_group")
+    long_rows = np.arange(0, 64 * 100, 64)     # rows of 64 at ps 32 -> full windows
+    assert bench.k1_form(long_rows, 32, 1).startswith("agg_local")
+    assert bench.k1_form(long_rows, 16, 1).startswith("agg_group")
+    assert bench.k1_form(long_rows, 32, 2).startswith("agg_gpair")
