@@ -230,7 +230,7 @@ def agg_widths(model):
     return [min(dims[l], model.hidden) for l in range(model.layers)]
 
 
-def k1_form(row_ptr, ps: int, parts: int) -> str:
+def k1_form(row_ptr, ps: int, parts: int, width: int = 16) -> str:
     """Which local K1 a single-device launch runs (the launcher's rule,
     csrc/cuda/aggregate.cu pick_lean; multi-part fine launches use agg_gpair)."""
     if parts > 1:
@@ -238,7 +238,11 @@ def k1_form(row_ptr, ps: int, parts: int) -> str:
     deg = np.diff(np.asarray(row_ptr, dtype=np.int64))
     nparts = int(((deg + ps - 1) // ps).sum())
     short = ps <= 16 or 3 * int(deg.sum()) < 2 * ps * nparts
-    return "agg_group (group per partition)" if short else "agg_local (warp window)"
+    if not short:
+        return "agg_local (warp window)"
+    pitch = (width + 3) // 4 * 4
+    return ("agg_group_hint (group per partition, L2 hints)" if 8 < pitch <= 16
+            else "agg_group (group per partition)")
 
 
 def agg_bytes(edges: int, parts: int, rows: int, dim: int) -> int:
@@ -513,7 +517,7 @@ def main():
                        "layer_forward_ms": round(ms_step, 4)},
             "roofline": {"bound": "hbm",
                          "kernel": f"K1 aggregation, width {w0}: "
-                                   f"{k1_form(g.row_ptr, args.ps, n)}",
+                                   f"{k1_form(g.row_ptr, args.ps, n, w0)}",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": _traffic(args, n),

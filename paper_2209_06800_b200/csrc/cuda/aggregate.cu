@@ -617,6 +617,83 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
     }
   }
 }
+// agg_group with L2 eviction hints: gathered rows evict-last (they are the
+// only reuse K1 has), column ids and accumulator reductions evict-first.
+template <int VEC, bool RELU, int UNR>
+__device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
+  constexpr int G = 32 / VEC;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / VEC, v = lane % VEC;
+  const bool vlane = v < static_cast<int>(a.vec);
+  const uint32_t pb = a.pitch * 4u;
+  const char* lbase = reinterpret_cast<const char*>(a.own) + (vlane ? 16u * v : 0u);
+  asm("mov.b64 %0, %0;" : "+l"(lbase));
+  uint64_t pol_last, pol_first;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  auto load = [&](uint32_t c) {
+    float4 x;
+    asm("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(lbase + static_cast<size_t>(c) * pb), "l"(pol_last));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  auto ldcol = [&](const uint32_t* p) {
+    uint32_t r;
+    // volatile: a plain asm is speculatable, and the tail's guarded column
+    // loads would be if-converted into unguarded reads past the partition
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;"
+                 : "=r"(r)
+                 : "l"(p), "l"(pol_first));
+    return r;
+  };
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    const uint32_t l0 = w * a.dist;
+    const uint32_t l1 = min(l0 + a.dist, a.nL);
+    for (uint32_t i = l0 + grp; i < l1; i += G) {
+      const int2 m = __ldg(a.lmeta + i);
+      const int end = __ldg(&a.lmeta[i + 1].y);
+      float4 acc = f4zero();
+      int k = m.y;
+      // column ids of step s+1 load while step s's rows are in flight
+      uint32_t c[UNR];
+      if (k + UNR <= end) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) c[u] = ldcol(a.lcols + k + u);
+      }
+      for (; k + UNR <= end; k += UNR) {
+        float4 t[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) t[u] = load(c[u]);
+        if (k + 2 * UNR <= end) {
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = ldcol(a.lcols + k + UNR + u);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+      }
+      if (k < end) {
+        float4 t[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          t[u] = k + u < end ? load(ldcol(a.lcols + k + u)) : f4zero();
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+      }
+      if (vlane)
+        asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
+                         a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v),
+                     "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w), "l"(pol_first)
+                     : "memory");
+    }
+  }
+}
 // Group-per-partition form of the paired (fine-fetch) K1: group g of a
 // logical warp takes pairs i = g, g + 32/VEC, ... of the warp's local and
 // remote groups and keeps the reference's async discipline per pair
@@ -758,6 +835,14 @@ KernelFn pick_group(uint32_t v) {
   if (v <= 32) return agg_group<32, RELU, UNR>;
   return agg_wide<RELU>;
 }
+template <int VEC, bool RELU, int UNR>
+__global__ void __launch_bounds__(512, 2) agg_group_hint(AggArgs a) {
+  agg_group_hint_body<VEC, RELU, UNR>(a);
+}
+template <bool RELU>
+KernelFn pick_group_hint(uint32_t v) {
+  return v <= 4 ? agg_group_hint<4, RELU, 8> : agg_group_hint<16, RELU, 8>;
+}
 
 // The register budget is the occupancy knob of this latency-bound gather:
 // MINB resident 512-thread CTAs (64 / 42 / 32 registers), or an explicit cap.
@@ -827,6 +912,14 @@ KernelFn pick(uint32_t v) {
   }
 }
 
+int l2_hint() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_L2HINT");  // -1 auto, 0 off, 1 on
+    return e ? std::atoi(e) : -1;
+  }();
+  return m;
+}
+
 int group_unroll() {
   static const int m = [] {
     const char* e = std::getenv("MGG_AGG_GROUP_UNR");
@@ -850,6 +943,11 @@ KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
       granularity == 0 && (ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts);
   // 8 rows in flight per group; MGG_AGG_GROUP_UNR=4 (A/B) is 8% faster on the
   // skewed Orkut-RMAT shape and 1-2% slower on the uniform ones
+  // narrow rows (<= 16 floats): L2 evict-last on the gathered rows, evict-first
+  // on the column ids and the reductions (products-shaped K1 -1.7%, Orkut
+  // -0.5%; the 256-B GIN rows lose 0.5-2% with it, so they go without)
+  const bool hint = l2_hint() < 0 ? v > 2 && v <= 4 : l2_hint() == 1 && (v == 4 || v == 16);
+  if (short_parts && hint) return pick_group_hint<RELU>(v);
   if (short_parts) return group_unroll() == 4 ? pick_group<RELU, 4>(v) : pick_group<RELU, 8>(v);
   return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
 }

@@ -96,5 +96,6 @@ def test_k1_form_rule():
     assert bench.k1_form(full, 32, 1).startswith("agg_group")
     long_rows = np.arange(0, 64 * 100, 64)     # rows of 64 at ps 32 -> full windows
     assert bench.k1_form(long_rows, 32, 1).startswith("agg_local")
-    assert bench.k1_form(long_rows, 16, 1).startswith("agg_group")
+    assert bench.k1_form(long_rows, 16, 1).startswith("agg_group_hint")
+    assert bench.k1_form(long_rows, 16, 1, width=64) == "agg_group (group per partition)"
     assert bench.k1_form(long_rows, 32, 2).startswith("agg_gpair")

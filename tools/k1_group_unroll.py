@@ -4,7 +4,7 @@ profiles/r01_k1_variants/group_unr4_vs_8.jsonl."""
 import json, os, sys
 sys.path.insert(0, '.')
 import bench, paper_2209_06800_b200 as mgg
-u = os.environ.get("MGG_AGG_GROUP_UNR", "0")
+u = os.environ.get("MGG_AGG_GROUP_UNR", "0") + "/h" + os.environ.get("MGG_AGG_L2HINT", "0")
 for w in ("products-gcn", "orkut-gcn", "orkut-rmat-gcn", "products-gin", "products-rmat-gin"):
     label, g, model, _ = bench.build(mgg, w)
     dim = bench.agg_widths(model)[0]
