@@ -75,7 +75,7 @@ WORKLOADS = {
     "products-rmat-gin": ("GIN-5L hidden 64 ogbn-products-shaped RMAT variant",
                           ("rmat", 2_449_029, 61_859_140), ("gin", 100, 64, 47, 5), (16, 16, 2)),
     "orkut-rmat-gcn": ("GCN-2L com-Orkut-shaped RMAT variant",
-                       ("rmat", 3_072_441, 117_185_083), ("gcn", 128, 16, 32, 2), (32, 16, 4)),
+                       ("rmat", 3_072_441, 117_185_083), ("gcn", 128, 16, 32, 2), (16, 16, 2, 3)),
 }
 
 
@@ -94,6 +94,9 @@ def _args():
     ap.add_argument("--fetch", default="auto", choices=["auto", "fine", "halo"],
                     help="remote rows: per-edge peer reads in K1 (fine, the paper's design) or "
                          "one deduplicated pull per layer (halo); auto picks by bytes moved")
+    ap.add_argument("--k1-form", type=int, default=None, choices=[0, 1, 2, 3],
+                    help="local-only K1 form (0 by shape, 1 warp-window, 2/3 group with 8/4 "
+                         "rows in flight); default: the workload's tuned form")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
@@ -101,6 +104,8 @@ def _args():
     a.ps = a.ps or tuned[0]
     a.dist = a.dist or tuned[1]
     a.wpb = a.wpb or tuned[2]
+    if a.k1_form is None:  # the tuner post-pass's K1 form, 0 (by shape) if none
+        a.k1_form = tuned[3] if len(tuned) > 3 and (a.ps, a.dist, a.wpb) == tuned[:3] else 0
     return a
 
 
@@ -230,17 +235,24 @@ def agg_widths(model):
     return [min(dims[l], model.hidden) for l in range(model.layers)]
 
 
-def k1_form(row_ptr, ps: int, parts: int, width: int = 16) -> str:
+def k1_form(row_ptr, ps: int, parts: int, width: int = 16, form: int = 0) -> str:
     """Which local K1 a single-device launch runs (the launcher's rule,
     csrc/cuda/aggregate.cu pick_lean; multi-part fine launches use agg_gpair)."""
     if parts > 1:
         return "agg_gpair (group per pair) / agg_group halo passes"
+    pitch = (width + 3) // 4 * 4
+    if form == 1:
+        return "agg_local (warp window)"
+    if form == 3:
+        return "agg_group (group per partition, 4 rows in flight)"
+    if form == 2:
+        return ("agg_group_hint (group per partition, L2 hints)" if 8 < pitch <= 16
+                else "agg_group (group per partition)")
     deg = np.diff(np.asarray(row_ptr, dtype=np.int64))
     nparts = int(((deg + ps - 1) // ps).sum())
     short = ps <= 16 or 3 * int(deg.sum()) < 2 * ps * nparts
     if not short:
         return "agg_local (warp window)"
-    pitch = (width + 3) // 4 * 4
     return ("agg_group_hint (group per partition, L2 hints)" if 8 < pitch <= 16
             else "agg_group (group per partition)")
 
@@ -377,6 +389,8 @@ def main():
     setup_s = time.perf_counter() - t0
     if args.fetch != "auto":
         eng.set_remote_fetch(args.fetch)
+    if args.k1_form:
+        eng.set_k1_form(args.k1_form)
     if world > 1:
         mdist.exchange_ipc(eng, rank, world)
         dist.barrier()
@@ -511,13 +525,14 @@ def main():
                                                    "(reference/RMAT generator) seed 0",
                        "nodes": N, "edges": E, "dim": model.in_dim, "hidden": model.hidden,
                        "classes": model.out_dim, "layers": layers, "agg_widths": widths,
-                       "ps": args.ps, "dist": args.dist, "wpb": args.wpb, "parts": n,
+                       "ps": args.ps, "dist": args.dist, "wpb": args.wpb, "k1_form": args.k1_form,
+                       "parts": n,
                        "remote_fetch": args.fetch,
                        "l2": "inputs larger than L2 (X + CSR >= 1 GB), no flush",
                        "layer_forward_ms": round(ms_step, 4)},
             "roofline": {"bound": "hbm",
                          "kernel": f"K1 aggregation, width {w0}: "
-                                   f"{k1_form(g.row_ptr, args.ps, n, w0)}",
+                                   f"{k1_form(g.row_ptr, args.ps, n, w0, args.k1_form)}",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": _traffic(args, n),

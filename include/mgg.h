@@ -208,6 +208,11 @@ int mgg_trace_read(mgg_trace* t, uint64_t* events, uint64_t cap, uint64_t* n,
  * with opts.halo reads them locally. */
 int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, float* halo);
 int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* halo_len);
+/* Local-only K1 form for this plan's launches (single-part and halo passes):
+ * 0 = by the plan's shape (default), 1 = warp-window, 2 = group-per-partition
+ * with 8 rows in flight per group, 3 = the same with 4. Same partitions and
+ * sums in every form; the tuner's post-pass picks among them. */
+int mgg_dplan_set_k1_form(mgg_dplan* plan, uint32_t form);
 
 /* out[r] = scale * f(in[r]) for the part's own rows (self term / copies).
  * f: 0 identity, 1 ReLU. */
@@ -445,6 +450,8 @@ int mgg_engine_set_input(mgg_engine* e, const float* x);
  * (re-captured after re-planning); mgg_engine_set_graphs(e, 0) disables it. */
 int mgg_engine_forward(mgg_engine* e);
 int mgg_engine_set_graphs(mgg_engine* e, int on);
+/* Local-only K1 form of every plan of the engine (mgg_dplan_set_k1_form). */
+int mgg_engine_set_k1_form(mgg_engine* e, uint32_t form);
 /* z: num_nodes x out_dim; only this process's rows are written. */
 int mgg_engine_get_output(mgg_engine* e, float* z);
 /* End to end: H2D x, forward, D2H z (synchronous). */

@@ -77,6 +77,10 @@ class Engine {
   /// Replay forward() from a captured CUDA graph when the context allows it
   /// (one device, all parts local, not profiling); on by default there.
   void set_graphs(bool on);
+  /// Local-only K1 form for every plan (0 by shape, 1 warp-window, 2 group with
+  /// 8 rows in flight, 3 group with 4); kept across re-plans.
+  void set_k1_form(std::uint32_t form);
+  std::uint32_t k1_form() const { return k1_form_; }
   void synchronize();
   void get_output(float* z);                 // N x out_dim host rows
   void forward_host(const float* x, float* z);  // submit_host + wait
@@ -176,6 +180,7 @@ class Engine {
   mgg_store* scratch_[2] = {nullptr, nullptr};
   bool profiling_ = false;
   bool graphs_ = true;
+  std::uint32_t k1_form_ = 0;
   bool eager_warm_ = false;           // one eager forward before the first capture
   mgg_exec* exec_ = nullptr;          // captured forward()
   mgg_store* exec_input_ = nullptr;   // input store the capture read

@@ -149,6 +149,7 @@ _sig("mgg_remote_partition_bytes", U64, U64, U64, I, U64)
 _sig("mgg_engine_set_input", I, vp, f32p)
 _sig("mgg_engine_forward", I, vp)
 _sig("mgg_engine_set_graphs", I, vp, I)
+_sig("mgg_engine_set_k1_form", I, vp, U32)
 _sig("mgg_engine_get_output", I, vp, f32p)
 _sig("mgg_engine_forward_host", I, vp, f32p, f32p)
 _sig("mgg_engine_submit_host", I, vp, f32p, f32p, u64p)

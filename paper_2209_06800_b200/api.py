@@ -437,6 +437,11 @@ class Engine:
     def forward(self) -> None:
         check(lib.mgg_engine_forward(self._h))
 
+    def set_k1_form(self, form: int) -> None:
+        """Local-only K1 form: 0 by the plan's shape, 1 warp-window, 2 group (8 rows
+        in flight per group), 3 group (4) — mgg_engine_set_k1_form."""
+        check(lib.mgg_engine_set_k1_form(self._h, form))
+
     def set_graphs(self, on: bool) -> None:
         """CUDA-graph replay of forward() on single-device contexts (default on)."""
         check(lib.mgg_engine_set_graphs(self._h, int(on)))

@@ -937,8 +937,13 @@ int group_unroll() {
 // +1%, register caps 40/32 for more warps: +4-10%).
 template <bool RELU>
 KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
-                   uint32_t granularity) {
+                   uint32_t granularity, uint32_t form) {
   if (lean_mode() != 1) return pick<RELU, false>(v);
+  if (form == 1 || (form > 1 && granularity == 1))
+    return v <= 4 ? pick_local<RELU, 2>(v) : pick_local_r<RELU, 48>(v);
+  if (form == 2) return v > 2 && v <= 4 && l2_hint() != 0 ? pick_group_hint<RELU>(v)
+                                                          : pick_group<RELU, 8>(v);
+  if (form == 3) return pick_group<RELU, 4>(v);
   const bool short_parts =
       granularity == 0 && (ps <= 16 || 3 * edges < 2 * static_cast<uint64_t>(ps) * parts);
   // 8 rows in flight per group; MGG_AGG_GROUP_UNR=4 (A/B) is 8% faster on the
@@ -1128,8 +1133,8 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
   KernelFn k = remote ? (relu_in ? pick_pair<true>(a.vec, p->granularity)
                                  : pick_pair<false>(a.vec, p->granularity))
-                      : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity)
-                                 : pick_lean<false>(a.vec, p->ps, lparts, ledges, p->granularity));
+                      : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity, p->k1_form)
+                                 : pick_lean<false>(a.vec, p->ps, lparts, ledges, p->granularity, p->k1_form));
   if (trace) {  // the pipelined kernel with stage stamps, whatever the plan
     if (relu_in || halo) throw Status{MGG_E_CONFIG, "trace: fine-grained, no ReLU-on-load"};
     // the pair kernel that runs untraced: group-per-pair unless the

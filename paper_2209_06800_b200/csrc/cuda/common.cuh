@@ -97,6 +97,9 @@ struct mgg_dplan {
   uint32_t ps = 1, dist = 1, wpb = 1, mapping = 0, granularity = 0;
   uint64_t rows = 0, n_local = 0, n_remote = 0;
   uint64_t local_edges = 0, remote_edges = 0;  // column ids per kind
+  // local-only K1 form: 0 by the plan's shape, 1 warp-window, 2 group (8 rows
+  // in flight per group), 3 group (4 rows in flight) — mgg_dplan_set_k1_form
+  uint32_t k1_form = 0;
   int2* lmeta = nullptr;
   uint32_t* lcols = nullptr;
   int2* rmeta = nullptr;

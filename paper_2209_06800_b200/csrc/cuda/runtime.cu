@@ -878,6 +878,12 @@ int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, floa
   });
 }
 
+int mgg_dplan_set_k1_form(mgg_dplan* plan, uint32_t form) {
+  if (!plan || form > 3) return MGG_E_INPUT;
+  plan->k1_form = form;
+  return MGG_OK;
+}
+
 int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* n) {
   if (!plan || !n) return MGG_E_INPUT;
   *n = plan->halo_len;

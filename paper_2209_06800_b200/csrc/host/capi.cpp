@@ -480,6 +480,9 @@ int mgg_engine_get_output(mgg_engine* e, float* z) {
 int mgg_engine_forward_host(mgg_engine* e, const float* x, float* z) {
   return guard([&] { e->e->forward_host(x, z); });
 }
+int mgg_engine_set_k1_form(mgg_engine* e, uint32_t form) {
+  return guard([&] { e->e->set_k1_form(form); });
+}
 int mgg_engine_set_graphs(mgg_engine* e, int on) {
   return guard([&] { e->e->set_graphs(on != 0); });
 }

@@ -292,6 +292,7 @@ void Engine::build_plans() {
     d.remote_cols = fp.remote.cols.data();
     d.remote_cols_len = fp.remote.cols.size();
     ok(mgg_dplan_upload(ctx_, &d, &plans_[p]));
+    ok(mgg_dplan_set_k1_form(plans_[p], k1_form_));
     stats_.local_parts += d.n_local;
     stats_.remote_parts += d.n_remote;
     stats_.local_edges += d.local_cols_len;
@@ -454,6 +455,15 @@ void Engine::build_row_scales() {
 void Engine::set_graphs(bool on) {
   graphs_ = on;
   if (!on) drop_exec();
+}
+
+void Engine::set_k1_form(std::uint32_t form) {
+  if (form > 3) throw InputError("engine: k1 form must be 0..3");
+  ok(mgg_ctx_synchronize(ctx_));
+  drop_exec();  // the captured graph holds the previous kernels
+  k1_form_ = form;
+  for (auto* p : plans_)
+    if (p) ok(mgg_dplan_set_k1_form(p, form));
 }
 
 void Engine::drop_exec() {

@@ -35,8 +35,9 @@ def test_workload_table_matches_baseline():
     for key in ("configs[0]", "configs[1]", "configs[2]", "configs[3]"):
         assert key in labels
     for name, (_, g, m, tuned) in bench.WORKLOADS.items():
-        ps, dist, wpb = tuned
+        ps, dist, wpb = tuned[:3]
         assert 1 <= ps <= 32 and 1 <= dist <= 16 and 1 <= wpb <= 16, name
+        assert len(tuned) == 3 or tuned[3] in (0, 1, 2, 3), name
         assert g[0] in ("powerlaw", "rmat") and m[0] in ("gcn", "gcn-norm", "gin"), name
 
 
@@ -82,7 +83,7 @@ def test_traffic_table_covers_every_workload():
     # tuned config (profiles/k1_traffic.json); a retune must come with a capture
     import types
     for name, (_, g, _, tuned) in bench.WORKLOADS.items():
-        ps, dist, wpb = tuned
+        ps, dist, wpb = tuned[:3]
         parts = 2 if name == "config1" else 1
         args = types.SimpleNamespace(workload=name, ps=ps, dist=dist, wpb=wpb)
         t = bench._traffic(args, parts)
@@ -99,3 +100,5 @@ def test_k1_form_rule():
     assert bench.k1_form(long_rows, 16, 1).startswith("agg_group_hint")
     assert bench.k1_form(long_rows, 16, 1, width=64) == "agg_group (group per partition)"
     assert bench.k1_form(long_rows, 32, 2).startswith("agg_gpair")
+    assert bench.k1_form(long_rows, 16, 1, form=1).startswith("agg_local")
+    assert "4 rows" in bench.k1_form(long_rows, 32, 1, form=3)

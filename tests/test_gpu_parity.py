@@ -76,8 +76,12 @@ def test_aggregate_local_flavours(mgg, oracle_mod, ps, dim):
     for parts in (1, 3):
         eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 8, 4), ps=ps, dist=4, wpb=4)
         eng.set_remote_fetch("halo")
-        out = eng.aggregate(x, 1.0, relu_in=True)
-        assert_rows_close(out, ref, what=f"ps={ps} dim={dim} parts={parts}")
+        for form in (0, 1, 2, 3):  # by shape, warp-window, group x8, group x4
+            eng.set_k1_form(form)
+            out = eng.aggregate(x, 1.0, relu_in=True)
+            assert_rows_close(out, ref, what=f"ps={ps} dim={dim} parts={parts} form={form}")
+        with pytest.raises(mgg.MggError):
+            eng.set_k1_form(4)
         eng.close()
 
 
@@ -462,7 +466,7 @@ def test_full_size_forward_matches_oracle(mgg, oracle_mod, workload):
     the fp64 one, and the engine must stay within 2x of it."""
     import bench
     _, g, model, _ = bench.build(mgg, workload)
-    ps, dist, wpb = bench.WORKLOADS[workload][3]
+    ps, dist, wpb = bench.WORKLOADS[workload][3][:3]
     x = mgg.random_features(g.num_nodes, model.in_dim, seed=1)
     eng = mgg.Engine(g, 1, [0], model, ps=ps, dist=dist, wpb=wpb)
     try:

@@ -8,7 +8,7 @@ u = os.environ.get("MGG_AGG_GROUP_UNR", "0") + "/h" + os.environ.get("MGG_AGG_L2
 for w in ("products-gcn", "orkut-gcn", "orkut-rmat-gcn", "products-gin", "products-rmat-gin"):
     label, g, model, _ = bench.build(mgg, w)
     dim = bench.agg_widths(model)[0]
-    for cfg in (tuple(bench.WORKLOADS[w][3]), (16, 16, 2), (16, 16, 4)):
+    for cfg in (tuple(bench.WORKLOADS[w][3][:3]), (16, 16, 2), (16, 16, 4)):
         eng = mgg.Engine(g, 1, [0], model, *cfg)
         t = eng.time_aggregate(dim, 7) / 1e6
         eng.close()

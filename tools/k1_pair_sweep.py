@@ -10,7 +10,7 @@ mode = os.environ.get("MGG_AGG_PAIR", "1")
 for w in sys.argv[1:]:
     label, g, model, _ = bench.build(mgg, w)
     dim = bench.agg_widths(model)[0]
-    for cfg in (tuple(bench.WORKLOADS[w][3]), (32, 16, 2)):
+    for cfg in (tuple(bench.WORKLOADS[w][3][:3]), (32, 16, 2)):
         for n in (2, 8):
             eng = mgg.Engine(g, n, [0] * n, model, *cfg)
             eng.set_remote_fetch("fine")

@@ -11,7 +11,7 @@ mode = os.environ.get("MGG_AGG_LEAN", "1")
 for w in sys.argv[1:]:
     label, g, model, _ = bench.build(mgg, w)
     dim = bench.agg_widths(model)[0]
-    tuned = tuple(bench.WORKLOADS[w][3])
+    tuned = tuple(bench.WORKLOADS[w][3][:3])
     for cfg in (tuned, (16, 16, 2), (16, 8, 8), (16, 16, 8), (8, 16, 8)):
         eng = mgg.Engine(g, 1, [0], model, *cfg)
         t = eng.time_aggregate(dim, 7) / 1e6

@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--parts", default="1,2,4,8")
     args = ap.parse_args()
     label, g, model, _ = bench.build(mgg, args.workload)
-    ps, dist, wpb = bench.WORKLOADS[args.workload][3]
+    ps, dist, wpb = bench.WORKLOADS[args.workload][3][:3]
     dim = bench.agg_widths(model)[0]
     for n in (int(p) for p in args.parts.split(",")):
         eng = mgg.Engine(g, n, [0] * n, model, ps, dist, wpb)

@@ -55,7 +55,7 @@ def main():
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     label, g, model, _ = bench.build(mgg, args.workload)
-    ps, dist, wpb = bench.WORKLOADS[args.workload][3]
+    ps, dist, wpb = bench.WORKLOADS[args.workload][3][:3]
     dim = bench.agg_widths(model)[0]
     eng = mgg.Engine(g, args.parts, [0] * args.parts, model, ps, dist, wpb)
     eng.set_remote_fetch("fine")

@@ -5,6 +5,9 @@ SimulateFn on a bench workload, and (optionally) the exhaustive sweep it is
 judged against (acceptance criterion 7's shape). Writes JSON to stdout.
 
     python tools/tune_b200.py --workload reddit-gcn [--parts N] [--exhaustive]
+
+After the tuner, a post-pass times the four local-only K1 forms at the pick
+(`Engine.set_k1_form`) and reports the fastest (`k1_form`).
 """
 import argparse
 import json
@@ -42,6 +45,15 @@ def main():
            "tuner": {"trace": trace, "best": best, "evaluations": len(trace),
                      "seconds": round(time.perf_counter() - t0, 2),
                      "speedup_vs_origin": round(trace[0][3] / best[3], 2)}}
+    # post-pass (beyond the reference's tuner): the local-only K1 form at the
+    # pick — by shape (0), warp-window (1), group x8 (2), group x4 (3)
+    eng.set_config(*best[:3])
+    forms = {}
+    for f in (0, 1, 2, 3):
+        eng.set_k1_form(f)
+        forms[f] = eng.time_aggregate(dim, reps=args.reps)
+    eng.set_k1_form(0)
+    out["k1_form"] = {"ns": forms, "best": min(forms, key=forms.get)}
     if args.exhaustive:
         t0 = time.perf_counter()
         table = mgg.exhaustive(measure, hw, dim)
