@@ -959,8 +959,11 @@ KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
 
 int pair_mode() {
   static const int m = [] {
+    // opt-in (MGG_AGG_PAIR=1) until the intermittent illegal address it shows
+    // in the two-process IPC test (~1 run in 6, never single-process) is
+    // understood; the warp-window pair loop is the default
     const char* e = std::getenv("MGG_AGG_PAIR");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return m;
 }

@@ -16,6 +16,13 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-4
 
 
+def softmax_bar(zr, z32):
+    """Softmax tolerance: 1e-4 absolute, or twice the fp32 floor when the
+    logits are large enough that the fp32 CPU restatement itself lands
+    further than that from the fp64 oracle (the full-size test's criterion)."""
+    return max(TOL, 2 * float(np.abs(z32 - zr).max()))
+
+
 def assert_rows_close(got, ref, tol=TOL, what=""):
     assert got.shape == ref.shape, (got.shape, ref.shape)
     scale = np.abs(ref).max(axis=1, keepdims=True)
@@ -123,7 +130,8 @@ def test_gcn2_forward(mgg, oracle_mod, parts):
     assert_rows_close(np.maximum(a1, 0), h1, what="H1")
     a2 = eng.get_hidden(1)
     assert_rows_close(a2, oracle_mod.aggregate(g.row_ptr, g.col_idx, h1), what="A2")
-    assert np.abs(z - zr).max() <= TOL, np.abs(z - zr).max()
+    _, _, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+    assert np.abs(z - zr).max() <= softmax_bar(zr, z32), np.abs(z - zr).max()
     eng.close()
 
 
@@ -154,8 +162,14 @@ def test_streamed_submit_matches_oracle(mgg, oracle_mod, kind, parts):
             _, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, xs[i], model)
         else:
             _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, xs[i], model)
+        if kind == "gin":
+            _, z32 = oracle_mod.gin_forward(g.row_ptr, g.col_idx, xs[i], model, acc64=False)
+        else:
+            _, _, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, xs[i], model,
+                                                acc64=False)
         err = np.abs(zs[i] - zr).max()
-        assert err <= TOL, f"step {i}: {err}"
+        bar = softmax_bar(zr, z32)
+        assert err <= bar, f"step {i}: {err} (bar {bar})"
     eng.wait(tickets[0])  # already complete: no-op
     eng.close()
 
@@ -569,3 +583,29 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
     assert np.abs(lg).max() < 1e3  # normalised logits stay small
     assert np.abs(z - zr).max() <= TOL, np.abs(z - zr).max()
     assert np.abs(z2 - zr).max() <= TOL, np.abs(z2 - zr).max()
+
+
+def test_group_pair_kernel_opt_in(tmp_path):
+    # agg_gpair (MGG_AGG_PAIR=1, read once per process) on single-process
+    # multi-part fine-fetch aggregations and a forward, against the oracle
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, oracle, paper_2209_06800_b200 as mgg
+g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 18, 12)
+for dim, parts in ((16, 2), (64, 3), (200, 4)):
+    x = mgg.random_features(g.num_nodes, dim, seed=dim)
+    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 8), ps=16, dist=4, wpb=4)
+    eng.set_remote_fetch("fine")
+    ref = oracle.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
+    out = eng.aggregate(x, 1.0, relu_in=True)
+    err = (np.abs(out - ref) / np.maximum(np.abs(ref).max(1, keepdims=True), 1e-6)).max()
+    assert err <= 1e-4, (dim, parts, err)
+    eng.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=600, env={**os.environ, "MGG_AGG_PAIR": "1"})
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
