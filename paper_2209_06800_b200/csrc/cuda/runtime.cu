@@ -83,17 +83,23 @@ void refresh_tables(mgg_store* s) {
       MGG_CUDA(cudaMalloc(&d, kMaxParts * sizeof(float*)));
       s->dtable[p] = static_cast<const float**>(d);
     }
-    MGG_CUDA(cudaMemcpy(s->dtable[p], host.data(), kMaxParts * sizeof(float*),
-                        cudaMemcpyHostToDevice));
+    // the table is read by kernels on the part's non-blocking streams, which
+    // do not order behind a legacy-stream cudaMemcpy (a pageable H2D copy may
+    // return before its DMA lands): copy on the part's stream and wait
+    MGG_CUDA(cudaMemcpyAsync(s->dtable[p], host.data(), kMaxParts * sizeof(float*),
+                             cudaMemcpyHostToDevice, ctx->stream[p]));
+    MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
   }
 }
 
+// Setup uploads are ordered on `st` (the consumer's stream); the caller
+// synchronises `st` before the buffers are handed out.
 template <class T>
-T* upload_array(const T* host, size_t n) {
+T* upload_array(const T* host, size_t n, cudaStream_t st) {
   void* d = nullptr;
   const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
   MGG_CUDA(cudaMalloc(&d, bytes));
-  if (n) MGG_CUDA(cudaMemcpy(d, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  if (n) MGG_CUDA(cudaMemcpyAsync(d, host, n * sizeof(T), cudaMemcpyHostToDevice, st));
   return static_cast<T*>(d);
 }
 
@@ -469,9 +475,12 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
         const size_t bytes = std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256);
         void* d = nullptr;
         MGG_CUDA(cudaMalloc(&d, bytes));
-        MGG_CUDA(cudaMemset(d, 0, bytes));
         s->shard[p] = static_cast<float*>(d);
         s->owned[p] = 1;
+        // zero padding/rows on the part's stream, complete before any use
+        // (a legacy-stream memset is not ordered before non-blocking streams)
+        MGG_CUDA(cudaMemsetAsync(d, 0, bytes, ctx->stream[p]));
+        MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
       }
       refresh_tables(s);
     } catch (...) {
@@ -598,7 +607,7 @@ static int copy_rows(const mgg_store* cs, float* host_rw, const float* host_ro,
       float* dev = s->shard[p] + (a - s->lb[p]) * s->pitch;
       const size_t hoff = (a - row_begin) * (size_t)ld;
       const size_t row_bytes = size_t(s->dim) * 4;
-      if (ld == s->pitch) {  // identical layout: one 1D copy
+      if (ld == s->pitch && s->pitch == s->dim) {  // identical, unpadded layout: one 1D copy
         if (up)
           MGG_CUDA(cudaMemcpyAsync(dev, host_ro + hoff, (b - a) * row_bytes, cudaMemcpyHostToDevice, st));
         else
@@ -700,7 +709,11 @@ int mgg_dbuf_create(mgg_ctx* ctx, uint32_t part, const void* host, size_t bytes,
       delete b;
       check(e, "cudaMalloc");
     }
-    if (bytes && host) MGG_CUDA(cudaMemcpy(b->ptr, host, bytes, cudaMemcpyHostToDevice));
+    if (bytes && host) {
+      cudaStream_t st = ctx->stream[part];
+      MGG_CUDA(cudaMemcpyAsync(b->ptr, host, bytes, cudaMemcpyHostToDevice, st));
+      MGG_CUDA(cudaStreamSynchronize(st));
+    }
     *out = b;
   });
 }
@@ -746,16 +759,21 @@ int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* d, mgg_dplan** out) {
       p->n_remote = d->n_remote;
       p->local_edges = d->local_cols_len;
       p->remote_edges = d->remote_cols_len;
-      p->lmeta = reinterpret_cast<int2*>(upload_array(d->local_meta, 2 * (d->n_local + 1)));
-      p->rmeta = reinterpret_cast<int2*>(upload_array(d->remote_meta, 2 * (d->n_remote + 1)));
-      p->lcols = upload_array(d->local_cols, d->local_cols_len);
-      launch_strip_owner(p->lcols, d->local_cols_len, ctx->stream[d->part]);
-      p->rcols = upload_array(d->remote_cols, d->remote_cols_len);
+      // every upload and the owner strip are ordered on the part's stream and
+      // complete before the plan is returned: the plan is later read from
+      // the part's aux stream and from captured graphs too
+      cudaStream_t st = ctx->stream[d->part];
+      p->lmeta = reinterpret_cast<int2*>(upload_array(d->local_meta, 2 * (d->n_local + 1), st));
+      p->rmeta = reinterpret_cast<int2*>(upload_array(d->remote_meta, 2 * (d->n_remote + 1), st));
+      p->lcols = upload_array(d->local_cols, d->local_cols_len, st);
+      launch_strip_owner(p->lcols, d->local_cols_len, st);
+      p->rcols = upload_array(d->remote_cols, d->remote_cols_len, st);
       if (d->halo_rows && d->halo_len && d->remote_halo_cols) {
-        p->halo_rows = upload_array(d->halo_rows, d->halo_len);
+        p->halo_rows = upload_array(d->halo_rows, d->halo_len, st);
         p->halo_len = d->halo_len;
-        p->rcols_halo = upload_array(d->remote_halo_cols, d->remote_cols_len);
+        p->rcols_halo = upload_array(d->remote_halo_cols, d->remote_cols_len, st);
       }
+      MGG_CUDA(cudaStreamSynchronize(st));
       p->num_local_warps = (d->n_local + d->dist - 1) / d->dist;
       const uint64_t nr_w = (d->n_remote + d->dist - 1) / d->dist;
       p->num_warps = d->mapping == 0 ? std::max(p->num_local_warps, nr_w)

@@ -83,16 +83,9 @@ def _run_pair(fetch, kind):
 
 @pytest.mark.parametrize("fetch,kind", [("auto", "gcn"), ("fine", "gcn"), ("halo", "gin")])
 def test_two_processes_ipc_forward(fetch, kind):
-    import warnings
-
     import paper_2209_06800_b200 as mgg
     assert mgg.cuda_available()
     res = _run_pair(fetch, kind)
-    if any(tb and "illegal memory access" in tb for _, _, _, tb in res):
-        # known intermittent failure of two processes sharing one GPU (DESIGN §10,
-        # open): one fresh retry, reported; a second failure fails the test
-        warnings.warn("two-process IPC run hit the known intermittent illegal address; retried")
-        res = _run_pair(fetch, kind)
     for rank, err, remote, tb in res:
         assert tb is None, tb
         assert remote > 0, "no remote edges: the peer path was not exercised"

@@ -609,3 +609,36 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=600, env={**os.environ, "MGG_AGG_PAIR": "1"})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dim", [41, 6, 16])
+@pytest.mark.parametrize("ld_kind", ["dim", "pitch", "wide"])
+def test_store_copy_row_layouts(mgg, dim, ld_kind):
+    """mgg_store_upload/download for every host row stride the header allows
+    (ld == dim, ld == the store's padded pitch, ld > pitch), including
+    dim % 4 != 0 with ld == pitch (the 1D fast path dropped rows)."""
+    import ctypes as C
+    from paper_2209_06800_b200._lib import check, lib
+    n = 1000
+    pitch = (dim + 3) // 4 * 4
+    ld = {"dim": dim, "pitch": pitch, "wide": pitch + 8}[ld_kind]
+    rng = np.random.default_rng(dim + ld)
+    host = rng.standard_normal((n, ld)).astype(np.float32)
+    ctx = C.c_void_p()
+    check(lib.mgg_ctx_create(2, (C.c_int32 * 2)(0, 0), C.byref(ctx)))
+    lb = (C.c_uint64 * 3)(0, 377, n)
+    s = C.c_void_p()
+    check(lib.mgg_store_create(ctx, lb, dim, C.byref(s)))
+    fp = C.POINTER(C.c_float)
+    check(lib.mgg_store_upload(s, host.ctypes.data_as(fp), 0, n, ld))
+    back = np.full((n, ld), 7.0, np.float32)
+    check(lib.mgg_store_download(s, back.ctypes.data_as(fp), 0, n, ld))
+    # the padded device rows, read back at the pitch (padding must be zero)
+    raw = np.full((n, pitch), 7.0, np.float32)
+    check(lib.mgg_store_download(s, raw.ctypes.data_as(fp), 0, n, pitch))
+    check(lib.mgg_ctx_synchronize(ctx))
+    lib.mgg_store_destroy(s)
+    lib.mgg_ctx_destroy(ctx)
+    assert np.array_equal(back[:, :dim], host[:, :dim])
+    assert np.all(back[:, dim:] == 7.0), "download wrote past dim into the caller's row padding"
+    assert np.array_equal(raw[:, :dim], host[:, :dim])
