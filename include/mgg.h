@@ -208,6 +208,10 @@ int mgg_trace_read(mgg_trace* t, uint64_t* events, uint64_t cap, uint64_t* n,
  * with opts.halo reads them locally. */
 int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, float* halo);
 int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* halo_len);
+/* Names of the kernels the plan's latest K1 (mgg_aggregate / _traced /
+ * mgg_time_aggregate) launched, demangled, ';'-separated (halo mode: the
+ * local pass then the remote pass), NUL-terminated into buf[cap]. */
+int mgg_dplan_k1_kernels(const mgg_dplan* plan, char* buf, size_t cap);
 /* Local-only K1 form for this plan's launches (single-part and halo passes):
  * 0 = by the plan's shape (default), 1 = warp-window, 2 = group-per-partition
  * with 8 rows in flight per group, 3 = the same with 4. Same partitions and
@@ -492,6 +496,9 @@ int mgg_engine_trace_csv(mgg_engine* e, uint32_t dim, uint64_t capacity, uint32_
  * halo_rows, halo_parts} */
 int mgg_engine_stats(const mgg_engine* e, uint64_t* stats);
 mgg_ctx* mgg_engine_ctx(mgg_engine* e);
+/* mgg_dplan_k1_kernels of local part `part`'s plan (the K1 forms the
+ * engine's latest aggregation of that part ran). */
+int mgg_engine_k1_kernels(const mgg_engine* e, uint32_t part, char* buf, size_t cap);
 /* Per-op device timing of subsequent forwards (events around every op of the
  * layer program on the first local part's stream; no host sync added). */
 int mgg_engine_set_profiling(mgg_engine* e, int on);

@@ -118,6 +118,8 @@ class Engine {
                   plan_build_ns = 0, halo_rows = 0, halo_parts = 0;
   };
   Stats stats() const;
+  /// Kernels the latest K1 of local part `part` launched (mgg_dplan_k1_kernels).
+  std::string k1_kernels(std::uint32_t part) const;
 
  private:
   enum class OpKind { dense, init, aggregate, barrier, softmax, dense_chain };

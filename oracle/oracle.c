@@ -318,3 +318,115 @@ void orc_gin_forward(int acc64, int threads, uint64_t n,
   free(a);
   free(t);
 }
+
+/* ------------------------------------------------------------------------ */
+/* synthetic inputs for bench.py's reference arm (no product code on it)     */
+/* ------------------------------------------------------------------------ */
+
+/* SplitMix64 (R:proj/include/pipeshard/rng.hpp:26-54). */
+static uint64_t sm_next(uint64_t* s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t sm_below(uint64_t* s, uint64_t n) {
+  const uint64_t reject_from = ~0ull - (~0ull % n);
+  uint64_t v;
+  do v = sm_next(s);
+  while (v >= reject_from);
+  return v % n;
+}
+static double sm_unit(uint64_t* s) { return (double)(sm_next(s) >> 11) * 0x1.0p-53; }
+
+static int cmp_u64(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : x > y;
+}
+static void sort_rows(uint64_t n, const uint64_t* row_ptr, uint64_t* col) {
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < (int64_t)n; ++v)
+    qsort(col + row_ptr[v], row_ptr[v + 1] - row_ptr[v], sizeof(uint64_t), cmp_u64);
+}
+
+/* R:proj/src/graph.cpp:139-176 — per node one degree draw (uniform: floor(d)
+ * + Bernoulli(frac); powerlaw: Pareto alpha 1.6 clipped to [1, N-1]), then
+ * that many uniform neighbors, one stream; rows sorted, duplicates kept.
+ * Returns E; fills row_ptr[n+1] / col[E] only when col != NULL. */
+uint64_t orc_gen_synthetic(int kind, uint64_t n, double avg, uint64_t seed,
+                           uint64_t* row_ptr, uint64_t* col) {
+  uint64_t s = seed, e = 0;
+  const uint64_t whole = (uint64_t)avg;
+  const double frac = avg - (double)whole;
+  const double alpha = 1.6;
+  double x_min = avg * (alpha - 1.0) / alpha;
+  if (x_min < 0.5) x_min = 0.5;
+  const double neg_inv_alpha = -1.0 / alpha;
+  const double cap = n == 1 ? 1.0 : (double)(n - 1);
+  const double hi = cap > 1.0 ? cap : 1.0;
+  if (row_ptr) row_ptr[0] = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    uint64_t deg;
+    if (kind == 0) {
+      deg = whole + (sm_unit(&s) < frac ? 1 : 0);
+    } else {
+      const double u = sm_unit(&s);
+      double x = floor(x_min * pow(1.0 - u, neg_inv_alpha));
+      if (x < 1.0) x = 1.0;
+      if (x > hi) x = hi;
+      deg = (uint64_t)x;
+    }
+    for (uint64_t k = 0; k < deg; ++k) {
+      const uint64_t c = sm_below(&s, n);
+      if (col) col[e] = c;
+      ++e;
+    }
+    if (row_ptr) row_ptr[v + 1] = e;
+  }
+  if (col && row_ptr) sort_rows(n, row_ptr, col);
+  return e;
+}
+
+/* RMAT edge stream of the product's generator (csrc/host/graph.cpp gen_rmat;
+ * not a reference algorithm — a locality-bearing input): blocks
+ * of 65536 edges, block b seeded seed ^ (0xD1B54A32D192ED03 * (b + 1)); per
+ * edge scale quadrant draws (a, b, c, 1-a-b-c), out-of-range pairs redrawn.
+ * CSR row = source, rows sorted, duplicates kept. row_ptr[n+1], col[m]. */
+void orc_gen_rmat(uint64_t n, uint64_t m, uint64_t seed, double a, double b, double c,
+                  uint64_t* row_ptr, uint64_t* col) {
+  unsigned scale = 0;
+  while (n > 1 && (1ull << scale) < n) ++scale;
+  const double ab = a + b, abc = a + b + c;
+  const uint64_t kBlock = 1u << 16, blocks = (m + kBlock - 1) / kBlock;
+  uint64_t* src = (uint64_t*)malloc(sizeof(uint64_t) * (m ? m : 1));
+  uint64_t* dst = (uint64_t*)malloc(sizeof(uint64_t) * (m ? m : 1));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t blk = 0; blk < (int64_t)blocks; ++blk) {
+    uint64_t s = seed ^ (0xD1B54A32D192ED03ull * (uint64_t)(blk + 1));
+    const uint64_t lo = (uint64_t)blk * kBlock, hi = lo + kBlock < m ? lo + kBlock : m;
+    for (uint64_t i = lo; i < hi; ++i) {
+      uint64_t u, v;
+      do {
+        u = v = 0;
+        for (unsigned l = 0; l < scale; ++l) {
+          const double r = sm_unit(&s);
+          const unsigned q = r < a ? 0u : r < ab ? 1u : r < abc ? 2u : 3u;
+          u = (u << 1) | (q >> 1);
+          v = (v << 1) | (q & 1u);
+        }
+      } while (u >= n || v >= n);
+      src[i] = u;
+      dst[i] = v;
+    }
+  }
+  memset(row_ptr, 0, sizeof(uint64_t) * (n + 1));
+  for (uint64_t i = 0; i < m; ++i) ++row_ptr[src[i] + 1];
+  for (uint64_t v = 0; v < n; ++v) row_ptr[v + 1] += row_ptr[v];
+  uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+  memcpy(cur, row_ptr, sizeof(uint64_t) * n);
+  for (uint64_t i = 0; i < m; ++i) col[cur[src[i]]++] = dst[i];
+  free(cur);
+  free(src);
+  free(dst);
+  sort_rows(n, row_ptr, col);
+}

@@ -103,6 +103,13 @@ void orc_gin_forward(int acc64, int threads, uint64_t n,
                      const float* w2, const float* b2, double eps,
                      float* logits, float* z);
 
+/* ---- synthetic inputs (bench.py --impl reference builds its graph with
+ * these or with oracle/_ref, never with the product) --------------------- */
+uint64_t orc_gen_synthetic(int kind, uint64_t n, double avg, uint64_t seed,
+                           uint64_t* row_ptr, uint64_t* col);
+void orc_gen_rmat(uint64_t n, uint64_t m, uint64_t seed, double a, double b, double c,
+                  uint64_t* row_ptr, uint64_t* col);
+
 #ifdef __cplusplus
 }
 #endif

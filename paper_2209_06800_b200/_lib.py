@@ -145,6 +145,7 @@ _sig("mgg_engine_set_mapping", I, vp, I, I)
 _sig("mgg_engine_set_remote_fetch", I, vp, I)
 _sig("mgg_halo_pull", I, vp, vp, vp, vp)
 _sig("mgg_dplan_halo_len", I, vp, u64p)
+_sig("mgg_dplan_k1_kernels", I, vp, C.c_char_p, C.c_size_t)
 _sig("mgg_remote_partition_bytes", U64, U64, U64, I, U64)
 _sig("mgg_engine_set_input", I, vp, f32p)
 _sig("mgg_engine_forward", I, vp)
@@ -165,6 +166,7 @@ _sig("mgg_engine_aggregate_host", I, vp, f32p, U32, C.c_float, I, f32p)
 _sig("mgg_engine_aggregate_phase_host", I, vp, f32p, U32, C.c_float, I, I, f32p)
 _sig("mgg_engine_time_aggregate", I, vp, U32, U32, I, u64p)
 _sig("mgg_engine_stats", I, vp, u64p)
+_sig("mgg_engine_k1_kernels", I, vp, U32, C.c_char_p, C.c_size_t)
 _sig("mgg_engine_trace_csv", I, vp, U32, U64, U32, C.POINTER(C.c_void_p))
 _sig("mgg_trace_create", I, vp, U32, U64, U32, PP)
 _sig("mgg_trace_destroy", I, vp)

@@ -537,6 +537,12 @@ class Engine:
                 "blocks", "launches", "plan_build_ns", "halo_rows", "halo_parts"]
         return {k: int(v) for k, v in zip(keys, s)}
 
+    def k1_kernels(self, part: int = 0) -> list[str]:
+        """Kernels the latest K1 of local part `part` launched (demangled)."""
+        buf = C.create_string_buffer(1024)
+        check(lib.mgg_engine_k1_kernels(self._h, part, buf, len(buf)))
+        return [k for k in buf.value.decode().split(";") if k]
+
 
 def host_alloc(shape, dtype=np.float32) -> np.ndarray:
     """Pinned host array (cudaHostAlloc) for full-speed H2D/D2H. The block is

@@ -34,7 +34,11 @@
 // launch from the plan's shape (pick_lean / pick_pair below).
 #include <cuda_runtime.h>
 
+#include <cxxabi.h>
+
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -959,11 +963,11 @@ KernelFn pick_lean(uint32_t v, uint32_t ps, uint64_t parts, uint64_t edges,
 
 int pair_mode() {
   static const int m = [] {
-    // opt-in (MGG_AGG_PAIR=1) until the intermittent illegal address it shows
-    // in the two-process IPC test (~1 run in 6, never single-process) is
-    // understood; the warp-window pair loop is the default
+    // group-per-pair is the default fine-fetch pair loop (the round-1
+    // two-process illegal address was the plan-upload race fixed in
+    // runtime.cu, not this kernel); MGG_AGG_PAIR=0 = the warp-window loop
     const char* e = std::getenv("MGG_AGG_PAIR");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   return m;
 }
@@ -980,6 +984,31 @@ int pair_mode() {
 template <bool RELU>
 KernelFn pick_pair(uint32_t v, uint32_t granularity) {
   return pair_mode() == 0 || granularity == 1 ? pick<RELU, true>(v) : pick_gpair<RELU, 4, 4>(v);
+}
+
+// Demangled short name of a K1 instantiation ("agg_group_hint<4, false, 8>"),
+// cached per function.
+const std::string& kernel_name(const void* fn) {
+  static std::mutex mu;
+  static std::map<const void*, std::string> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  const char* raw = nullptr;
+  std::string name = "?";
+  if (cudaFuncGetName(&raw, fn) == cudaSuccess && raw) {
+    int st = 0;
+    char* dm = abi::__cxa_demangle(raw, nullptr, nullptr, &st);
+    name = st == 0 && dm ? dm : raw;
+    std::free(dm);
+    const auto paren = name.find('(');  // drop the parameter list
+    if (paren != std::string::npos) name.resize(paren);
+    for (const char* pre : {"void ", "(anonymous namespace)::", "mgg::dev::"})
+      for (size_t q; (q = name.find(pre)) != std::string::npos;) name.erase(q, std::strlen(pre));
+  } else {
+    cudaGetLastError();
+  }
+  return cache.emplace(fn, name).first->second;
 }
 
 // Resident CTAs per SM for (kernel, CTA size), cached per device.
@@ -1153,6 +1182,8 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   k<<<grid, threads, 0, st>>>(a);
   MGG_CUDA(cudaGetLastError());
   count_launch(ctx);
+  if (!p->k1_names.empty()) p->k1_names += ';';
+  p->k1_names += kernel_name(reinterpret_cast<const void*>(k));
 }
 
 void launch_rows_init(const float* in, float* out, uint64_t rows, uint32_t pitch,

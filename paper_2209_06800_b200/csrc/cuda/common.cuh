@@ -108,6 +108,9 @@ struct mgg_dplan {
   uint32_t* halo_rows = nullptr;   // distinct packed remote rows
   uint64_t halo_len = 0;
   uint32_t* rcols_halo = nullptr;  // remote columns -> halo rows
+  // kernels launched by the plan's latest K1 (';'-separated, demangled;
+  // mgg_dplan_k1_kernels) — the bench labels its roofline with them
+  mutable std::string k1_names;
 };
 
 namespace mgg::dev {

@@ -119,6 +119,7 @@ void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg
                    const mgg_agg_opts* o, cudaStream_t st) {
   const int relu = o ? o->relu_in : 0, phase = o ? o->phase : 0;
   const float* halo = o ? o->halo : nullptr;
+  plan->k1_names.clear();
   if (!halo) {
     launch_aggregate(ctx, plan, in, out, relu, phase, nullptr, st);
     return;
@@ -899,6 +900,14 @@ int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, floa
 int mgg_dplan_set_k1_form(mgg_dplan* plan, uint32_t form) {
   if (!plan || form > 3) return MGG_E_INPUT;
   plan->k1_form = form;
+  return MGG_OK;
+}
+
+int mgg_dplan_k1_kernels(const mgg_dplan* plan, char* buf, size_t cap) {
+  if (!plan || !buf || cap == 0) return MGG_E_INPUT;
+  const size_t n = std::min(cap - 1, plan->k1_names.size());
+  std::memcpy(buf, plan->k1_names.data(), n);
+  buf[n] = 0;
   return MGG_OK;
 }
 

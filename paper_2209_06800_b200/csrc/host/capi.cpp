@@ -531,6 +531,16 @@ int mgg_engine_stats(const mgg_engine* e, uint64_t* s) {
 }
 mgg_ctx* mgg_engine_ctx(mgg_engine* e) { return e ? e->e->ctx() : nullptr; }
 
+int mgg_engine_k1_kernels(const mgg_engine* e, uint32_t part, char* buf, size_t cap) {
+  return guard([&] {
+    if (!e || !buf || cap == 0) throw InputError("engine_k1_kernels: null argument");
+    const std::string s = e->e->k1_kernels(part);
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  });
+}
+
 int mgg_engine_set_profiling(mgg_engine* e, int on) {
   return guard([&] { e->e->set_profiling(on != 0); });
 }

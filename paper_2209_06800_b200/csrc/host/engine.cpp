@@ -775,4 +775,11 @@ Engine::Stats Engine::stats() const {
   return s;
 }
 
+std::string Engine::k1_kernels(std::uint32_t part) const {
+  if (part >= num_parts_ || !plans_[part]) throw InputError("k1_kernels: part is not local");
+  char buf[512];
+  ok(mgg_dplan_k1_kernels(plans_[part], buf, sizeof buf));
+  return buf;
+}
+
 }  // namespace mgg

@@ -585,9 +585,12 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
     assert np.abs(z2 - zr).max() <= TOL, np.abs(z2 - zr).max()
 
 
-def test_group_pair_kernel_opt_in(tmp_path):
-    # agg_gpair (MGG_AGG_PAIR=1, read once per process) on single-process
-    # multi-part fine-fetch aggregations and a forward, against the oracle
+@pytest.mark.parametrize("pair,kernel", [("1", "agg_gpair"), ("0", "agg_kernel")])
+def test_pair_kernel_forms(pair, kernel):
+    # the fine-fetch pair loop: agg_gpair (default) and the warp-window loop
+    # (MGG_AGG_PAIR=0, read once per process) on single-process multi-part
+    # aggregations against the oracle; the launched kernel is read back
+    # through mgg_engine_k1_kernels
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -603,11 +606,14 @@ for dim, parts in ((16, 2), (64, 3), (200, 4)):
     out = eng.aggregate(x, 1.0, relu_in=True)
     err = (np.abs(out - ref) / np.maximum(np.abs(ref).max(1, keepdims=True), 1e-6)).max()
     assert err <= 1e-4, (dim, parts, err)
+    names = eng.k1_kernels(0)
+    want = {kernel!r} if dim <= 128 else "agg_wide"  # rows > 128 floats: one form
+    assert any(n.startswith(want) for n in names), names
     eng.close()
 print("ok")
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                       timeout=600, env={**os.environ, "MGG_AGG_PAIR": "1"})
+                       timeout=600, env={**os.environ, "MGG_AGG_PAIR": pair})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
