@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """Benchmark of the MGG hot path on B200 (contract: one JSON line on rank 0).
 
-Default workload (BASELINE.json configs[1], fits one GPU): 2-layer GCN
-(hidden 16, 41 classes) on a synthetic Reddit-shaped graph — 232,965 nodes,
-the reference's `powerlaw` generator (SplitMix64 seed 0, avg degree 492 ->
-114.2M edges), input dim 602, X ~ U[-1,1) (seed 1), Glorot weights (seed 2).
+Default workload: north_star's target shape — 2-layer GCN (hidden 16, 47
+classes) on a synthetic ogbn-products-shaped graph: 2,449,029 nodes, the
+reference's `powerlaw` generator (SplitMix64 seed 0, avg degree 25.259 ->
+60.8M edges), input dim 100, X ~ U[-1,1) (seed 1), Glorot weights (seed 2).
+BASELINE configs[1] (GCN-2L, Reddit-shaped, dim 602) is measured in the same
+run and reported under "secondary" (device value + K1 roofline).
 Other configs (--workload): config1 (RMAT 100K/1.6M, dim 16, 2 logical
-partitions), products-gcn (north_star target shape), products-gin
-(configs[2]), orkut-gcn (configs[3]).
+partitions), reddit-gcn (configs[1]), products-gin (configs[2]), orkut-gcn
+(configs[3]), RMAT variants.
 
 A step = one full forward (every layer: Update GEMM(s), K1 aggregation(s),
 head) over the whole graph. metric = aggregation GEdges/s = layers x E / step
@@ -18,10 +20,14 @@ L2, so no flush between steps.
             exactly K steps (barrier + synchronize both sides), max over ranks.
   e2e     : the same metric through the C-ABI `mgg_engine_forward_host`
             with pinned HOST X in / Z out (H2D + D2H inside the timed region).
-  roofline: dominant kernel (K1 aggregation): algorithmic bytes per launch
+  roofline: dominant kernel (K1 aggregation, the kernel names the library
+            reports for the launch), bound by what binds it: "hbm" when the
+            gathered table exceeds half the L2 — algorithmic bytes per launch
             (E·(4·pitch + 4) + 8·P + 8·rows·pitch) / its average
-            event-timed duration inside the timed region, vs MEASURED_PEAKS
-            hbm_gbs; plus the live K5 gather-probe ceiling (l2_gather).
+            event-timed duration vs MEASURED_PEAKS hbm_gbs; "l2" when it fits —
+            gathered-row bytes only (E·4·pitch) / duration vs the live K5
+            gather probe (uniform random rows, rows-only bytes: like for
+            like). `dram` = the committed ncu DRAM bytes of that launch.
   cpu_baseline: the oracle port (oracle/oracle.c, fp32 accumulate, all host
             threads) of the same forward on the same graph, rank 0, N=1.
 
@@ -29,6 +35,9 @@ L2, so no flush between steps.
 reference (pipeshard) has no layer arithmetic, so this arm times the oracle
 port of the forward (same workload) on all host cores, and reports the
 reference library's own metadata-build time beside it when oracle/_ref exists.
+It never loads the product: the graph comes from the reference library's own
+generator (oracle/_ref) or the oracle's C restatement of it, X and W from the
+numpy generators below (identical arrays, tests/test_bench.py).
 
 Multi-GPU: torchrun, one process per GPU; part r = rank r's edge-balanced
 node range (Alg. 1); remote rows read in-kernel over NVLink from peer shards
@@ -85,7 +94,10 @@ def _args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mgg", choices=["mgg", "reference"])
-    ap.add_argument("--workload", default="reddit-gcn", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="products-gcn", choices=sorted(WORKLOADS))
+    ap.add_argument("--secondary", default="reddit-gcn",
+                    help="comma-separated workloads also measured at N=1 (device value + "
+                         "roofline only); 'none' to skip")
     ap.add_argument("--ps", type=int, default=None)
     ap.add_argument("--dist", type=int, default=None)
     ap.add_argument("--wpb", type=int, default=None)
@@ -210,6 +222,9 @@ class ClockSampler:
                 "samples": len(self.samples), "source": self.source}
 
 
+L2_BYTES = 126 * 2**20  # B200 L2
+
+
 def build(mgg, name):
     label, gspec, mspec, _ = WORKLOADS[name]
     t0 = time.perf_counter()
@@ -227,6 +242,63 @@ def build(mgg, name):
     return label, g, model, gen_s
 
 
+# ---- numpy input generators of the reference arm (no product code): the same
+# arrays as paper_2209_06800_b200.api.make_gcn / make_gin / random_features
+class NpModel:
+    def __init__(self, kind, layers, in_dim, hidden, out_dim, w1, b1=None, w2=None, b2=None,
+                 eps=0.0, norm=0):
+        self.kind, self.layers, self.in_dim, self.hidden, self.out_dim = (
+            kind, layers, in_dim, hidden, out_dim)
+        self.w1, self.b1, self.w2, self.b2, self.eps, self.norm = w1, b1, w2, b2, eps, norm
+
+    def gin_dims(self):
+        return [self.in_dim] + [self.hidden] * (self.layers - 1) + [self.out_dim]
+
+
+def np_model(mspec, seed=2):
+    mk, din, hid, out, layers = mspec
+    rng = np.random.default_rng(seed)
+
+    def glorot(fi, fo):
+        lim = np.sqrt(6.0 / (fi + fo))
+        return rng.uniform(-lim, lim, size=(fi, fo)).astype(np.float32)
+    if mk in ("gcn", "gcn-norm"):
+        w = np.concatenate([glorot(din, hid).ravel(), glorot(hid, out).ravel()])
+        return NpModel(0, 2, din, hid, out, w.astype(np.float32), norm=int(mk == "gcn-norm"))
+    dims = [din] + [hid] * (layers - 1) + [out]
+    w1, b1, w2, b2 = [], [], [], []
+    for l in range(layers):
+        w1.append(glorot(dims[l], hid).ravel())
+        b1.append(rng.uniform(-0.1, 0.1, hid).astype(np.float32))
+        w2.append(glorot(hid, dims[l + 1]).ravel())
+        b2.append(rng.uniform(-0.1, 0.1, dims[l + 1]).astype(np.float32))
+    cat = lambda xs: np.ascontiguousarray(np.concatenate(xs), np.float32)  # noqa: E731
+    return NpModel(1, layers, din, hid, out, cat(w1), cat(b1), cat(w2), cat(b2), 0.0)
+
+
+def np_features(n, d, seed=1):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, d)).astype(np.float32)
+
+
+def ref_graph(name):
+    """CSR of the workload's graph without the product: the reference
+    library's own generator (oracle/_ref) for powerlaw graphs, else the
+    oracle's C restatement (bit-identical; tests/test_bench.py)."""
+    import oracle
+    kind, n, avg = WORKLOADS[name][1]
+    t0 = time.perf_counter()
+    if kind == "rmat":
+        rp, cl = oracle.gen_rmat(n, int(avg), 0)
+        src = "oracle.c RMAT restatement"
+    elif oracle.ref_available():
+        rp, cl = oracle.RefGraph.gen(1, n, avg, 0).csr()
+        src = "reference gen_synthetic (oracle/_ref)"
+    else:
+        rp, cl = oracle.gen_synthetic(1, n, avg, 0)
+        src = "oracle.c gen_synthetic restatement"
+    return rp, cl, src, time.perf_counter() - t0
+
+
 def agg_widths(model):
     """Aggregation width of each layer (aggregate at min(in, out) width)."""
     if model.kind == 0:
@@ -235,9 +307,23 @@ def agg_widths(model):
     return [min(dims[l], model.hidden) for l in range(model.layers)]
 
 
+def workload_config(name, args, nodes, edges, model, parts):
+    """The `config` object both arms print (identical for the same flags)."""
+    label, gspec = WORKLOADS[name][0], WORKLOADS[name][1]
+    return {"workload": label, "name": name,
+            "graph": f"{gspec[0]} (reference generator / RMAT) seed 0",
+            "nodes": int(nodes), "edges": int(edges), "dim": model.in_dim,
+            "hidden": model.hidden, "classes": model.out_dim, "layers": model.layers,
+            "agg_widths": agg_widths(model), "ps": args.ps, "dist": args.dist,
+            "wpb": args.wpb, "k1_form": args.k1_form, "parts": parts,
+            "remote_fetch": args.fetch,
+            "l2": "inputs larger than L2 (X + CSR >= 250 MB), no flush"}
+
+
 def k1_form(row_ptr, ps: int, parts: int, width: int = 16, form: int = 0) -> str:
     """Which local K1 a single-device launch runs (the launcher's rule,
-    csrc/cuda/aggregate.cu pick_lean; multi-part fine launches use agg_gpair)."""
+    csrc/cuda/aggregate.cu pick_lean) — a host-side prediction, checked in
+    tests against the names the library reports (mgg_engine_k1_kernels)."""
     if parts > 1:
         return "agg_gpair (group per pair) / agg_group halo passes"
     pitch = (width + 3) // 4 * 4
@@ -264,12 +350,46 @@ def agg_bytes(edges: int, parts: int, rows: int, dim: int) -> int:
     return edges * (4 * pitch + 4) + 8 * parts + 2 * rows * 4 * pitch
 
 
-def _traffic(args, parts):
+def roofline(nodes, edges, parts, rows, dim, launch_ms, gather_peak, traffic, kernels):
+    """Roofline of one K1 launch against the resource that binds it (see the
+    module docstring). Returns the JSON object."""
+    pitch = (dim + 3) // 4 * 4
+    table = nodes * pitch * 4
+    algo = agg_bytes(edges, parts, rows, dim)
+    t = launch_ms * 1e-3
+    hbm_peak, hbm_src = _peaks()
+    r = {"kernel": f"K1 aggregation, width {dim}: " + " + ".join(kernels),
+         "avg_launch_ms": round(launch_ms, 4), "algorithmic_bytes_per_launch": algo,
+         "gather_table_bytes": table, "unit": "GB/s"}
+    if table <= L2_BYTES // 2 and gather_peak:
+        rows_bytes = edges * 4 * pitch
+        achieved = rows_bytes / t / 1e9
+        r.update(bound="l2", achieved=round(achieved, 1), peak=round(gather_peak, 1),
+                 frac=round(achieved / gather_peak, 4),
+                 peak_source="K5 gather probe, this run: uniform random rows of the same "
+                             "table shape, rows-only bytes (like for like: numerator = "
+                             "E*4*pitch gathered-row bytes)")
+    else:
+        achieved = algo / t / 1e9
+        r.update(bound="hbm", achieved=round(achieved, 1), peak=hbm_peak,
+                 frac=round(achieved / hbm_peak, 4), peak_source=hbm_src)
+    r["traffic"] = traffic
+    if traffic:
+        r["dram"] = {"bytes_per_launch": traffic, "achieved": round(traffic / t / 1e9, 1),
+                     "frac": round(traffic / t / 1e9 / hbm_peak, 4),
+                     "vs_algorithmic": round(traffic / algo, 4),
+                     "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of this "
+                               "launch (profiles/k1_traffic.json)"}
+    return r
+
+
+def _traffic(args, parts, name=None):
     """DRAM bytes per K1 launch from the committed ncu capture of this config."""
+    name = name or args.workload
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
             for t in json.load(f):
-                if t.get("workload") == args.workload and t.get("config") == [
+                if t.get("workload") == name and t.get("config") == [
                         args.ps, args.dist, args.wpb] and t.get("parts", 1) == parts:
                     return t["dram_bytes_per_launch"]
     except Exception:  # noqa: BLE001
@@ -286,53 +406,59 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_forward_time(g, x, model, threads=None):
+def cpu_forward_time(row_ptr, col, x, model, threads=None):
     threads = host_threads() if threads is None else threads
     import oracle
     t0 = time.perf_counter()
     if model.kind == 0:
-        oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model, norm=model.norm, acc64=False,
+        oracle.gcn2_forward(row_ptr, col, x, model, norm=model.norm, acc64=False,
                             threads=threads)
     else:
-        oracle.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False, threads=threads)
+        oracle.gin_forward(row_ptr, col, x, model, acc64=False, threads=threads)
     return time.perf_counter() - t0
 
 
 def run_reference(args):
-    """--impl reference: CPU implementation of the path on the host cores."""
+    """--impl reference: CPU implementation of the path on the host cores
+    (oracle/ only — the product library is never loaded on this arm)."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     import oracle
-    import paper_2209_06800_b200 as mgg
-    label, g, model, _ = build(mgg, args.workload)
-    e = g.num_edges
+    name = args.workload
+    label, _, mspec, _ = WORKLOADS[name]
+    row_ptr, col, gsrc, gen_s = ref_graph(name)
+    n, e = len(row_ptr) - 1, len(col)
+    model = np_model(mspec)
     layers = model.layers
-    x = mgg.random_features(g.num_nodes, model.in_dim, seed=1)
+    x = np_features(n, model.in_dim, seed=1)
     cores = host_threads()
     for _ in range(max(args.warmup, 0)):
-        cpu_forward_time(g, x, model)
-    times = [cpu_forward_time(g, x, model) for _ in range(max(args.steps, 1))]
+        cpu_forward_time(row_ptr, col, x, model)
+    times = [cpu_forward_time(row_ptr, col, x, model) for _ in range(max(args.steps, 1))]
     t = sum(times) / len(times)
     value = layers * e / t / 1e9
     meta = None
     if oracle.ref_available():
-        r = oracle.RefGraph.from_csr(g.row_ptr, g.col_idx)
-        secs, nparts = r.time_metadata(args.gpus, args.ps, args.dist, args.wpb, model.in_dim)
-        meta = {"ref_metadata_build_s": round(secs, 4), "partitions": nparts}
+        r = oracle.RefGraph.from_csr(row_ptr, col)
+        secs, nparts = r.time_metadata(max(args.gpus, 1), args.ps, args.dist, args.wpb,
+                                       model.in_dim)
+        meta = {"ref_metadata_build_s": round(secs, 4), "partitions": nparts,
+                "what": "the reference library's split + local/remote split + ps-partitions "
+                        "+ warp/block mapping of every part, 1 host thread"}
+    parts = args.parts or (2 if name == "config1" else max(args.gpus, 1))
     line = {
         "impl": "reference", "metric": f"aggregation GEdges/s ({label.split()[0]} forward)",
         "value": round(value, 4), "unit": "GEdges/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": label, "nodes": g.num_nodes, "edges": e,
-                   "dim": model.in_dim, "hidden": model.hidden, "classes": model.out_dim,
-                   "layers": layers},
+        "config": workload_config(name, args, n, e, model, parts),
         "cpu_baseline": {"value": round(value, 4), "unit": "GEdges/s", "cores": cores,
                          "kind": "port",
                          "sample": "full forward of the workload per step (oracle.c fp32, "
                                    "OpenMP all host threads); the reference library has no "
                                    "layer arithmetic",
+                         "graph_source": gsrc, "graph_gen_s": round(gen_s, 2),
                          "reference_metadata": meta},
         "e2e": {"value": round(value, 4), "unit": "GEdges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -340,32 +466,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = _args()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+def _reexec_under_torchrun(args):
+    """`--gpus N` outside torchrun: one process per GPU via torch.distributed.run."""
+    import socket
 
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but {have} CUDA device(s) visible "
+                         "(--parts N runs N logical partitions on one GPU)")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.run(cmd).returncode)
+
+
+def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=True):
+    """One workload through the product: device value (+ e2e, cpu, overlap
+    when `full`). Returns the JSON fields (rank 0) or None."""
     import ctypes
-
-    import paper_2209_06800_b200 as mgg
-    from paper_2209_06800_b200 import dist as mdist
-    from paper_2209_06800_b200._lib import lib
-
-    world, rank, local_rank = mdist.env_world()
-    # MGG_BENCH_DEVICE pins every rank to one device: validates the multi-rank
-    # path (IPC + K3 across processes) on a one-GPU box; never set for numbers
-    local_rank = int(os.environ.get("MGG_BENCH_DEVICE", local_rank))
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group(backend="cpu:gloo,cuda:nccl")
-    if not mgg.cuda_available():
-        raise SystemExit("bench.py: no CUDA device visible (the product has no CPU path)")
-
-    label, g, model, gen_s = build(mgg, args.workload)
+    label, g, model, gen_s = build(mgg, name)
     N, E = g.num_nodes, g.num_edges
     layers = model.layers
     x = mgg.host_alloc((N, model.in_dim))
@@ -376,7 +500,7 @@ def main():
         n = world
         part_device = mdist.part_devices(world, rank, local_rank)
     else:
-        n = args.parts or (2 if args.workload == "config1" else max(args.gpus, 1))
+        n = args.parts or (2 if name == "config1" else 1)
         part_device = [0] * n  # logical partitions on one GPU
     widths = agg_widths(model)
     w0 = widths[0]
@@ -430,46 +554,47 @@ def main():
     eng.synchronize()
     ops, nfw = eng.profile()
     eng.set_profiling(False)
+    kernels = eng.k1_kernels(my_part)  # K1 forms of the last layer's launch
     if world > 1:
         dist.barrier()
-    if world > 1:
         total_ms = mdist.max_over_ranks(total_ms)
     ms_step = total_ms / args.steps
     value = layers * E / (ms_step * 1e-3) / 1e9
 
-    # dominant kernel: the first layer's K1 launch(es) inside the timed region
+    # dominant kernel: the first layer's K1 launch(es)
     st = eng.stats()
     agg = [t for k, w, t in ops if k == "aggregate" and w == w0]
     agg_ms_per_launch = agg[0] / nfw if agg else float("nan")
     my_edges = st["local_edges"] + st["remote_edges"]
     my_parts = st["local_parts"] + st["remote_parts"]
     rows = N if world == 1 else N // world
-    algo = agg_bytes(my_edges, my_parts, rows, w0)
-    peak, peak_kind = _peaks()
-    achieved = algo / (agg_ms_per_launch * 1e-3) / 1e9
     total_op_ms = max(sum(t for _, _, t in ops), 1e-9)
     share = sum(t for k, _, t in ops if k == "aggregate") / total_op_ms
+    roof = roofline(N, my_edges, my_parts, rows, w0, agg_ms_per_launch, gather_peak,
+                    _traffic(args, n, name), kernels)
+    roof["share_of_step"] = round(share, 4)
 
     # remote-access hiding (mirrors the phase-separated
     # decomposition R:proj/src/sim.cpp:127-142, 530-569): K1 of the first
     # aggregation width with only remote partitions (comm), only local ones
     # (compute) and both pipelined in one launch; max over parts
     overlap = None
-    if st["remote_parts"] > 0:
+    if full and st["remote_parts"] > 0:
         t_pipe = eng.time_aggregate(w0, 5, 0)
         t_loc = eng.time_aggregate(w0, 5, 1)
         t_rem = eng.time_aggregate(w0, 5, 2)
         if world > 1:
             t_pipe, t_loc, t_rem = (mdist.max_over_ranks(float(t)) for t in
                                     (t_pipe, t_loc, t_rem))
+        hidden = max(0.0, t_rem + t_loc - t_pipe)
         overlap = {"k1_pipelined_ns": int(t_pipe), "k1_local_only_ns": int(t_loc),
                    "k1_remote_only_ns": int(t_rem),
-                   "hidden_remote_fraction": round(
-                       max(0.0, (t_rem + t_loc - t_pipe)) / max(t_rem, 1), 4),
+                   "hidden_remote_fraction": round(hidden / max(t_rem, 1), 4),
+                   "overlap_of_shorter_phase": round(hidden / max(min(t_rem, t_loc), 1), 4),
                    "remote_fetch": "halo" if st.get("halo_rows", 0) else "fine"}
 
     e2e = None
-    if not args.no_e2e:
+    if full and not args.no_e2e:
         # two pinned input/output buffer pairs, alternated: every step copies
         # its own X in and its own Z out
         xs = [x, mgg.host_alloc((N, model.in_dim))]
@@ -502,9 +627,9 @@ def main():
                       "step's kernels), host wall clock"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if full and rank == 0 and world == 1 and not args.no_cpu:
         try:
-            tc = cpu_forward_time(g, np.asarray(x), model)
+            tc = cpu_forward_time(g.row_ptr, g.col_idx, np.asarray(x), model)
             cpu = {"value": round(layers * E / tc / 1e9, 4), "unit": "GEdges/s",
                    "cores": host_threads(), "kind": "port",
                    "sample": "one full forward of the same workload (oracle.c, fp32 "
@@ -512,50 +637,77 @@ def main():
                    "seconds": round(tc, 3)}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "error": str(ex)[:200]}
+    eng.close()
+    if rank != 0:
+        return None
+    return {
+        "metric": f"aggregation GEdges/s ({label.split()[0]} forward)",
+        "value": round(value, 4), "ms_per_step": round(ms_step, 4),
+        "config": workload_config(name, args, N, E, model, n),
+        "roofline": roof,
+        "ops": [{"kind": k, "width": w, "ms": round(t / nfw, 4)} for k, w, t in ops],
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "overlap": overlap,
+        "clocks": clk.summary(),
+        "setup": {"graph_gen_s": round(gen_s, 2), "engine_setup_s": round(setup_s, 2),
+                  "plan_build_ms": round(st["plan_build_ns"] / 1e6, 1),
+                  "remote_edge_fraction": round(st["remote_edges"] / max(my_edges, 1), 4)},
+    }
 
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _reexec_under_torchrun(args)
+
+    import paper_2209_06800_b200 as mgg
+    from paper_2209_06800_b200 import dist as mdist
+    from paper_2209_06800_b200._lib import lib
+
+    world, rank, local_rank = mdist.env_world()
+    # MGG_BENCH_DEVICE pins every rank to one device: validates the multi-rank
+    # path (IPC + K3 across processes) on a one-GPU box; never set for numbers
+    local_rank = int(os.environ.get("MGG_BENCH_DEVICE", local_rank))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend="cpu:gloo,cuda:nccl")
+    if not mgg.cuda_available():
+        raise SystemExit("bench.py: no CUDA device visible (the product has no CPU path)")
+
+    main_line = measure(args.workload, args, mgg, lib, mdist, world, rank, local_rank, dist)
+    secondary = []
+    names = [] if args.secondary in ("", "none") else args.secondary.split(",")
+    for name in names:
+        if name == args.workload or world > 1:
+            continue
+        sargs = argparse.Namespace(**vars(args))
+        tuned = WORKLOADS[name][3]
+        sargs.ps, sargs.dist, sargs.wpb = tuned[:3]
+        sargs.k1_form = tuned[3] if len(tuned) > 3 else 0
+        sargs.parts = None
+        r = measure(name, sargs, mgg, lib, mdist, world, rank, local_rank, dist, full=False)
+        if r:
+            secondary.append({k: r[k] for k in ("metric", "value", "ms_per_step", "config",
+                                                 "roofline", "ops", "gpu_launches", "clocks")}
+                             | {"unit": "GEdges/s", "steps": args.steps})
     if rank == 0:
+        m = main_line
         line = {
-            "metric": f"aggregation GEdges/s ({label.split()[0]} forward)",
-            "value": round(value, 4), "unit": "GEdges/s", "n_gpus": world,
+            "metric": m["metric"], "value": m["value"], "unit": "GEdges/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": label, "graph": f"{WORKLOADS[args.workload][1][0]} "
-                                                   "(reference/RMAT generator) seed 0",
-                       "nodes": N, "edges": E, "dim": model.in_dim, "hidden": model.hidden,
-                       "classes": model.out_dim, "layers": layers, "agg_widths": widths,
-                       "ps": args.ps, "dist": args.dist, "wpb": args.wpb, "k1_form": args.k1_form,
-                       "parts": n,
-                       "remote_fetch": args.fetch,
-                       "l2": "inputs larger than L2 (X + CSR >= 1 GB), no flush",
-                       "layer_forward_ms": round(ms_step, 4)},
-            "roofline": {"bound": "hbm",
-                         "kernel": f"K1 aggregation, width {w0}: "
-                                   f"{k1_form(g.row_ptr, args.ps, n, w0, args.k1_form)}",
-                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4),
-                         "traffic": _traffic(args, n),
-                         "algorithmic_bytes_per_launch": algo,
-                         "avg_launch_ms": round(agg_ms_per_launch, 4),
-                         "share_of_step": round(share, 4), "peak_source": peak_kind,
-                         "l2_gather": None if not gather_peak else {
-                             "peak": round(gather_peak, 1), "unit": "GB/s",
-                             "frac": round(achieved / gather_peak, 4),
-                             "source": "K5 probe (paper_2209_06800_b200/probes.py), this run"},
-                         "note": "gathered rows are counted per edge (SURVEY 8d); when the "
-                                 "gather table fits L2 the binding ceiling is the L2->SM "
-                                 "gather rate (l2_gather); traffic = ncu DRAM bytes/launch"},
-            "ops": [{"kind": k, "width": w, "ms": round(t / nfw, 4)} for k, w, t in ops],
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "overlap": overlap,
-            "clocks": clk.summary(),
-            "setup": {"graph_gen_s": round(gen_s, 2), "engine_setup_s": round(setup_s, 2),
-                      "plan_build_ms": round(st["plan_build_ns"] / 1e6, 1),
-                      "remote_edge_fraction": round(st["remote_edges"] / max(my_edges, 1), 4)},
+            "ms_per_step": m["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": m["config"], "roofline": m["roofline"], "ops": m["ops"],
+            "cpu_baseline": m["cpu_baseline"], "e2e": m["e2e"],
+            "gpu_launches": m["gpu_launches"], "overlap": m["overlap"], "clocks": m["clocks"],
+            "setup": m["setup"], "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
 

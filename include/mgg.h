@@ -87,6 +87,25 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim,
                      mgg_store** out);
 int mgg_store_destroy(mgg_store* s);
 int mgg_store_info(const mgg_store* s, uint32_t* dim, uint32_t* pitch);
+/* Where a local part's shards live (stores created after the call):
+ *  MGG_MEM_DEVICE (0)       cudaMalloc on the part's device (default);
+ *  MGG_MEM_HOST_MAPPED (1)  pinned host memory mapped into the device: a slow
+ *      "peer" — every row read crosses PCIe with microsecond latency; measures
+ *      remote-latency hiding (R:PAPER.md:405-419) on a one-GPU box;
+ *  MGG_MEM_MANAGED (2)      cudaMallocManaged, home = the part's device: a
+ *      reader on another device faults the pages it touches over — the
+ *      reference's paged_remote baseline (R:proj/src/sim.cpp:503-518,
+ *      571-595) on real multi-GPU hardware;
+ *  MGG_MEM_MANAGED_HOST (3) cudaMallocManaged, home = host memory: the same
+ *      page-fault-driven remote fetch on one GPU (pages migrate over PCIe).
+ * Non-device shards cannot be IPC-exported. */
+enum { MGG_MEM_DEVICE = 0, MGG_MEM_HOST_MAPPED = 1, MGG_MEM_MANAGED = 2,
+       MGG_MEM_MANAGED_HOST = 3 };
+int mgg_ctx_set_shard_memory(mgg_ctx* ctx, uint32_t part, int kind);
+/* Prefetches the store's managed shards back to their home (every paged
+ * measurement starts cold; mgg_time_aggregate does this before each timed
+ * rep, outside the timed window). No-op for device / host-mapped shards. */
+int mgg_store_rehome(mgg_store* s);
 /* CUDA IPC handle (64 bytes) of a local shard / import a peer's shard. */
 int mgg_store_ipc_export(const mgg_store* s, uint32_t part, void* handle64);
 int mgg_store_ipc_import(mgg_store* s, uint32_t part, const void* handle64);
@@ -208,6 +227,10 @@ int mgg_trace_read(mgg_trace* t, uint64_t* events, uint64_t cap, uint64_t* n,
  * with opts.halo reads them locally. */
 int mgg_halo_pull(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, float* halo);
 int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* halo_len);
+/* Geometry of the plan's latest K1 launch: info[4] = {grid CTAs, threads per
+ * CTA, resident CTAs per SM (cudaOccupancyMaxActiveBlocksPerMultiprocessor),
+ * SMs of the device}. */
+int mgg_dplan_k1_launch_info(const mgg_dplan* plan, uint32_t* info);
 /* Names of the kernels the plan's latest K1 (mgg_aggregate / _traced /
  * mgg_time_aggregate) launched, demangled, ';'-separated (halo mode: the
  * local pass then the remote pass), NUL-terminated into buf[cap]. */
@@ -306,6 +329,10 @@ uint64_t mgg_ctx_launch_count(const mgg_ctx* ctx);
 int mgg_event_record(mgg_ctx* ctx, uint32_t part, uint32_t slot);
 /* Waits for slot b, then *ms = elapsed(a -> b). */
 int mgg_event_elapsed(mgg_ctx* ctx, uint32_t part, uint32_t a, uint32_t b, float* ms);
+/* ms between slot a of part_a and slot b of part_b (both parts on the same
+ * device: their streams share the device clock). */
+int mgg_event_elapsed_between(mgg_ctx* ctx, uint32_t part_a, uint32_t a, uint32_t part_b,
+                              uint32_t b, float* ms);
 
 /* ======================================================================= */
 /* B. host facade                                                           */
@@ -484,6 +511,22 @@ int mgg_engine_aggregate_phase_host(mgg_engine* e, const float* x, uint32_t dim,
  * config, max over local parts — the tuner's SimulateFn. */
 int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps,
                               int phase, uint64_t* median_ns);
+/* The same per part: ns[num_parts] (0 for parts of other processes). */
+int mgg_engine_time_aggregate_each(mgg_engine* e, uint32_t dim, uint32_t reps, int phase,
+                                   uint64_t* ns);
+/* Measured MultiGpuReport (R:proj/include/pipeshard/sim.hpp:115-123,
+ * multi_gpu_run R:proj/src/sim.cpp:597-624): every local part's K1 at width
+ * `dim` run concurrently, median of `reps`. summary[4] = {max_gpu_ns,
+ * barrier_ns, total_ns (max + barrier), remote_bytes}; per_part[num_parts x 9]
+ * = {local (1/0), total_ns (concurrent), alone_ns, remote_bytes, local_bytes,
+ * num_warps, num_blocks, active_sms, part}; per_part_f[num_parts x 2] =
+ * {achieved_occupancy (occupancy calculator x grid), sm_utilization (SMs
+ * given CTAs / SMs)}. */
+int mgg_engine_measure_multi_gpu(mgg_engine* e, uint32_t dim, uint32_t reps,
+                                 uint64_t* summary, uint64_t* per_part, double* per_part_f);
+/* Shard placement of local part `part` (MGG_MEM_*); re-creates the engine's
+ * stores (set the input again). Single-process engines only. */
+int mgg_engine_set_shard_memory(mgg_engine* e, uint32_t part, int kind);
 /* Device event trace of one K1 launch at width `dim` on every local part
  * (mgg_aggregate_traced), as the reference's multi-GPU trace CSV
  * (R:proj/tools/cli.cpp:144-155): "gpu,cycle,sm,warp,stage,event" rows,

@@ -59,6 +59,7 @@ class Engine {
   const NePlacement& placement() const { return ne_; }
   const KernelConfig& config() const { return cfg_; }
   mgg_ctx* ctx() const { return ctx_; }
+  std::uint32_t num_parts() const { return num_parts_; }
 
   std::vector<std::uint8_t> export_ipc(std::uint32_t part) const;
   void import_ipc(std::uint32_t part, const std::vector<std::uint8_t>& blob);
@@ -97,8 +98,43 @@ class Engine {
   /// phase 1 = local partitions only, 2 = remote only (0 = both).
   void aggregate_host(const float* x, std::uint32_t dim, float self_scale,
                       bool relu_in, float* out, int phase = 0);
-  /// Median K1 ns at width `dim`, max over local parts (tuner SimulateFn).
+  /// Median K1 ns at width `dim`, max over local parts (each part alone).
   std::uint64_t time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase);
+  /// The same per local part (0 for parts of other processes).
+  std::vector<std::uint64_t> time_aggregate_each(std::uint32_t dim, std::uint32_t reps,
+                                                 int phase);
+
+  /// Measured counterpart of the reference's SimReport / MultiGpuReport
+  /// (R:proj/include/pipeshard/sim.hpp:62-78, 115-123; multi_gpu_run
+  /// R:proj/src/sim.cpp:597-624): one K1 at width `dim` on every local part
+  /// *concurrently* (start-aligned, then the K3/event barrier), median of
+  /// `reps`. Per part: its K1 ns inside the concurrent run and alone, the
+  /// remote bytes it moved, launch occupancy and SM coverage. total = max
+  /// over parts + barrier. Several processes: each reports its own parts;
+  /// the caller takes the max over ranks.
+  struct PartReport {
+    std::uint32_t part = 0;
+    std::uint64_t total_ns = 0;    // K1 of this part while the others run too
+    std::uint64_t alone_ns = 0;    // the same K1 with the device to itself
+    double achieved_occupancy = 0; // resident warps / warp slots of the SMs it ran on
+                                   // (occupancy calculator x grid; not an ncu counter)
+    double sm_utilization = 0;     // SMs given CTAs / SMs of the device
+    std::uint64_t remote_bytes = 0, local_bytes = 0;  // gathered-row bytes
+    std::uint32_t num_warps = 0, num_blocks = 0, active_sms = 0;
+    std::string kernels;
+  };
+  struct MultiGpuReport {
+    std::vector<PartReport> per_gpu;
+    std::uint64_t max_gpu_ns = 0, barrier_ns = 0, total_ns = 0, remote_bytes = 0;
+    double mean_occupancy = 0, mean_utilization = 0;
+  };
+  MultiGpuReport measure_multi_gpu(std::uint32_t dim, std::uint32_t reps);
+
+  /// Placement of local part `part`'s shards (MGG_MEM_* of include/mgg.h):
+  /// device (default), host-mapped (slow-peer emulation) or managed (the
+  /// paged_remote baseline). Re-creates every store (contents are lost:
+  /// set_input again); single-process engines only.
+  void set_shard_memory(std::uint32_t part, int kind);
   /// Device event trace of one K1 at width `dim` on every local part, in the
   /// reference's multi-GPU trace CSV schema (R:proj/tools/cli.cpp:144-155).
   std::string trace_csv(std::uint32_t dim, std::uint64_t capacity, std::uint32_t warp_limit);

@@ -69,6 +69,8 @@ def orc():
              U32, I, f32p, f32p, f32p)
         _sig(L, "orc_gin_forward", None, I, I, U64, u64p, u64p, f32p, U32, u32p, U32, f32p,
              f32p, f32p, f32p, D, f32p, f32p)
+        _sig(L, "orc_gen_synthetic", U64, I, U64, D, U64, u64p, u64p)
+        _sig(L, "orc_gen_rmat", None, U64, U64, U64, D, D, D, u64p, u64p)
         _orc = L
     return _orc
 
@@ -165,6 +167,26 @@ def gin_forward(row_ptr, col, x, model, acc64=True, threads=0):
                           *[_p(a, C.c_float) for a in arrs], model.eps, _p(lg, C.c_float),
                           _p(z, C.c_float))
     return lg, z
+
+
+def gen_synthetic(kind, n, avg, seed):
+    """R:proj/src/graph.cpp:139-176 restated (kind 0 uniform, 1 powerlaw):
+    (row_ptr u64[n+1], col u64[E]) — bench.py's reference arm builds its
+    input with this (or the reference library itself), never the product."""
+    L = orc()
+    e = L.orc_gen_synthetic(kind, n, float(avg), seed, None, None)
+    rp = np.zeros(n + 1, np.uint64)
+    cl = np.zeros(max(e, 1), np.uint64)
+    L.orc_gen_synthetic(kind, n, float(avg), seed, _p(rp, C.c_uint64), _p(cl, C.c_uint64))
+    return rp, cl[:e]
+
+
+def gen_rmat(n, m, seed, a=0.57, b=0.19, c=0.19):
+    """The RMAT input of bench/tests as plain C (see oracle.c): CSR arrays."""
+    rp = np.zeros(n + 1, np.uint64)
+    cl = np.zeros(max(m, 1), np.uint64)
+    orc().orc_gen_rmat(n, m, seed, a, b, c, _p(rp, C.c_uint64), _p(cl, C.c_uint64))
+    return rp, cl[:m]
 
 
 # ----------------------------------------------------------------------------

@@ -22,6 +22,7 @@ from ._lib import (AggOpts, ConfigError, CudaError, InputError, IntegrityError, 
                    MEASURE_FN, ModelDesc, MggError, ParseError, check, lib)
 
 UNIFORM, POWERLAW, RMAT = 0, 1, 2
+MEM_DEVICE, MEM_HOST_MAPPED, MEM_MANAGED, MEM_MANAGED_HOST = 0, 1, 2, 3
 EQUAL_NODES, FOLLOW_SPLIT = 0, 1
 INTERLEAVED, SEGREGATED = 0, 1
 PARTITIONED, WHOLE_LIST = 0, 1
@@ -497,6 +498,42 @@ class Engine:
         ns = C.c_uint64()
         check(lib.mgg_engine_time_aggregate(self._h, dim, reps, phase, C.byref(ns)))
         return ns.value
+
+    def time_aggregate_each(self, dim: int, reps: int = 5, phase: int = 0) -> list[int]:
+        """Median K1 ns per part, each part alone (0 for remote parts)."""
+        ns = np.zeros(self.num_parts, np.uint64)
+        check(lib.mgg_engine_time_aggregate_each(self._h, dim, reps, phase, _p(ns, C.c_uint64)))
+        return [int(v) for v in ns]
+
+    def measure_multi_gpu(self, dim: int, reps: int = 5) -> dict:
+        """Measured MultiGpuReport (R:proj/include/pipeshard/sim.hpp:115-123):
+        every local part's K1 concurrently; see mgg_engine_measure_multi_gpu."""
+        n = self.num_parts
+        summ = np.zeros(4, np.uint64)
+        pp = np.zeros(9 * n, np.uint64)
+        pf = np.zeros(2 * n, np.float64)
+        check(lib.mgg_engine_measure_multi_gpu(self._h, dim, reps, _p(summ, C.c_uint64),
+                                               _p(pp, C.c_uint64),
+                                               pf.ctypes.data_as(C.POINTER(C.c_double))))
+        keys = ["local", "total_ns", "alone_ns", "remote_bytes", "local_bytes", "num_warps",
+                "num_blocks", "active_sms", "part"]
+        per = []
+        for p in range(n):
+            row = {k: int(v) for k, v in zip(keys, pp[9 * p: 9 * p + 9])}
+            if not row.pop("local"):
+                continue
+            row["achieved_occupancy"] = float(pf[2 * p])
+            row["sm_utilization"] = float(pf[2 * p + 1])
+            per.append(row)
+        return {"per_gpu": per, "max_gpu_ns": int(summ[0]), "barrier_ns": int(summ[1]),
+                "total_ns": int(summ[2]), "remote_bytes": int(summ[3]),
+                "mean_occupancy": float(np.mean([r["achieved_occupancy"] for r in per])),
+                "mean_utilization": float(np.mean([r["sm_utilization"] for r in per]))}
+
+    def set_shard_memory(self, part: int, kind: int) -> None:
+        """MEM_DEVICE / MEM_HOST_MAPPED / MEM_MANAGED / MEM_MANAGED_HOST for part
+        `part`'s shards (re-creates the stores: set_input again)."""
+        check(lib.mgg_engine_set_shard_memory(self._h, part, kind))
 
     def trace_csv(self, dim: int, capacity: int = 1 << 20, warp_limit: int = 0xFFFFFFFF) -> str:
         """Device event trace of one K1 at width `dim` (mgg_engine_trace_csv):

@@ -806,6 +806,178 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
     }
   }
 }
+// Fine-fetch K1 with the remote rows staged in shared memory (agg_pipe):
+// the paper's remote get into shared memory (R:PAPER.md:400-419) with the
+// reference's per-pair order (issue R_i, reduce L_i, consume R_i;
+// R:proj/src/sim.cpp:102-125), deepened into a per-lane ring. Each lane owns
+// R 16-B slots in shared memory; the group's remote rows — every R partition
+// of every pair the group will visit, in consumption order — stream through
+// the ring as cp.async copies straight from the owner's shard (peer / IPC /
+// host-mapped address) into the slots, always R rows ahead of the consumer:
+// one copy is issued per row consumed, so exactly R commit groups are in
+// flight and `cp.async.wait_group R-1` releases the oldest. In-flight rows
+// hold no registers (the register-staged agg_gpair keeps PF float4 per lane
+// and re-issues the rest of R_i at consume time, exposing the remote latency
+// once per 4 rows); local partitions are reduced from registers meanwhile.
+// A lane reads back only the slots it filled itself, so no barrier is needed.
+template <int VEC, bool RELU, int UNR, int R>
+__device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
+  static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
+  constexpr int G = 32 / VEC;
+  extern __shared__ float4 pipe_ring[];
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / VEC, v = lane % VEC;
+  const bool vlane = v < static_cast<int>(a.vec);
+  const uint32_t voff = vlane ? 16u * v : 0u;
+  const uint32_t pb = a.pitch * 4u;
+  const char* lbase = reinterpret_cast<const char*>(a.own) + voff;
+  asm("mov.b64 %0, %0;" : "+l"(lbase));
+  const uint32_t ring0 = static_cast<uint32_t>(__cvta_generic_to_shared(pipe_ring + threadIdx.x));
+  const uint32_t rstride = blockDim.x * 16u;
+  auto ld = [&](const char* p) {
+    float4 x;
+    asm(MGG_LD_INSN " {%0,%1,%2,%3}, [%4];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(p));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  auto raddr = [&](uint32_t c) {
+    const char* b =
+        a.halo ? reinterpret_cast<const char*>(a.halo)
+               : reinterpret_cast<const char*>(
+                     __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
+    return b + voff + static_cast<size_t>(c & kMask) * pb;
+  };
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  const uint32_t wib = threadIdx.x >> 5;
+
+  // producer cursor: the group's remote rows in consumption order
+  uint32_t plb = b0, pw = b0 * a.wpb + wib, pr0 = 0, pr1 = 0, pi = grp;
+  int pk = 0, pend = 0;
+  bool pdone = b0 >= b1 || pw >= a.num_warps;
+  if (!pdone) {
+    uint32_t l0, l1;
+    warp_groups(a, pw, l0, l1, pr0, pr1);
+  }
+  uint32_t issued = 0, consumed = 0;
+  auto produce = [&]() {
+    while (!pdone && pk >= pend) {  // open the next non-empty remote partition
+      if (pr0 + pi < pr1) {
+        pk = __ldg(&a.rmeta[pr0 + pi].y);
+        pend = __ldg(&a.rmeta[pr0 + pi + 1].y);
+        pi += G;
+      } else if (++plb >= b1 || (pw += a.wpb) >= a.num_warps) {
+        pdone = true;
+      } else {
+        uint32_t l0, l1;
+        warp_groups(a, pw, l0, l1, pr0, pr1);
+        pi = grp;
+      }
+    }
+    if (!pdone) {
+      const char* src = raddr(__ldg(a.rcols + pk));
+      ++pk;
+      const uint32_t dst = ring0 + (issued & (R - 1)) * rstride;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // empty past the end
+    ++issued;
+  };
+#pragma unroll 1
+  for (int s = 0; s < R; ++s) produce();
+
+  for (uint32_t lb = b0; lb < b1; ++lb) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    uint32_t l0, l1, r0, r1;
+    warp_groups(a, w, l0, l1, r0, r1);
+    const uint32_t nl = l1 - l0, nr = r1 - r0, n = max(nl, nr);
+    for (uint32_t i = grp; i < n; i += G) {
+      // (1) R_i is already in flight (issued up to R rows ago)
+      // (2) reduce L_i from registers
+      if (i < nl) {
+        const int2 m = __ldg(a.lmeta + l0 + i);
+        const int end = __ldg(&a.lmeta[l0 + i + 1].y);
+        float4 acc = f4zero();
+        int k = m.y;
+        for (; k + UNR <= end; k += UNR) {
+          uint32_t c[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) t[u] = ld(lbase + static_cast<size_t>(c[u]) * pb);
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (k < end) {
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+            t[u] = k + u < end ? ld(lbase + static_cast<size_t>(__ldg(a.lcols + k + u)) * pb)
+                               : f4zero();
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+      }
+      // (3) consume R_i from the ring; every row consumed issues the next
+      if (i < nr) {
+        const int2 m = __ldg(a.rmeta + r0 + i);
+        const int end = __ldg(&a.rmeta[r0 + i + 1].y);
+        float4 acc = f4zero();
+        for (int k = m.y; k < end; ++k) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(R - 1) : "memory");
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                       : "r"(ring0 + (consumed & (R - 1)) * rstride)
+                       : "memory");
+          ++consumed;
+          if (RELU) x = f4relu(x);
+          acc = f4add(acc, x);
+          produce();  // refills the slot just read (after its value is used)
+        }
+        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+template <int VEC, bool RELU, int UNR, int R>
+__global__ void __launch_bounds__(512, 2) agg_pipe(AggArgs a) {
+  agg_pipe_body<VEC, RELU, UNR, R>(a);
+}
+// dynamic shared memory of the pipe kernels: R 16-B slots per thread
+std::map<const void*, uint32_t>& pipe_slots() {
+  static std::map<const void*, uint32_t> m;
+  return m;
+}
+template <bool RELU, int R>
+KernelFn pick_pipe(uint32_t v) {
+  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 4, R>
+               : v <= 2  ? agg_pipe<2, RELU, 4, R>
+               : v <= 4  ? agg_pipe<4, RELU, 4, R>
+               : v <= 8  ? agg_pipe<8, RELU, 4, R>
+               : v <= 16 ? agg_pipe<16, RELU, 4, R>
+               : v <= 32 ? agg_pipe<32, RELU, 4, R>
+                         : agg_wide<RELU>;
+  if (v <= 32) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    pipe_slots()[reinterpret_cast<const void*>(k)] = R;
+  }
+  return k;
+}
+uint32_t dyn_smem(KernelFn k, int threads) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pipe_slots().find(reinterpret_cast<const void*>(k));
+  return it == pipe_slots().end() ? 0u : it->second * 16u * static_cast<uint32_t>(threads);
+}
+
 template <int VEC, int PF>
 __global__ void __launch_bounds__(512, 2) agg_gpair_traced(AggArgs a) {
   agg_gpair_body<VEC, false, 4, PF, true>(a);
@@ -981,9 +1153,25 @@ int pair_mode() {
 // MGG_AGG_PAIR=0 keeps the warp-window pair loop (ablations, A/B).
 // Whole-list plans (granularity 1, the no_np ablation) keep the warp per
 // list of the paper's baseline.
+int pipe_depth() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_PIPE_DEPTH");  // ring slots per lane
+    return e ? std::atoi(e) : 8;
+  }();
+  return m;
+}
+
 template <bool RELU>
 KernelFn pick_pair(uint32_t v, uint32_t granularity) {
-  return pair_mode() == 0 || granularity == 1 ? pick<RELU, true>(v) : pick_gpair<RELU, 4, 4>(v);
+  if (pair_mode() == 0 || granularity == 1) return pick<RELU, true>(v);
+  if (pair_mode() == 2) {
+    switch (pipe_depth()) {
+      case 4: return pick_pipe<RELU, 4>(v);
+      case 16: return pick_pipe<RELU, 16>(v);
+      default: return pick_pipe<RELU, 8>(v);
+    }
+  }
+  return pick_gpair<RELU, 4, 4>(v);
 }
 
 // Demangled short name of a K1 instantiation ("agg_group_hint<4, false, 8>"),
@@ -1022,7 +1210,11 @@ unsigned resident_grid(KernelFn k, int threads) {
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int per_sm = 0, sms = 0;
-  MGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0));
+  const uint32_t smem = dyn_smem(k, threads);
+  if (smem > 48 * 1024)
+    MGG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  MGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem));
   MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const unsigned g = static_cast<unsigned>(std::max(1, per_sm) * sms);
   cache[key] = g;
@@ -1178,8 +1370,18 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
     a.trace_warps = trace->warp_limit;
   }
   const int threads = 32 * static_cast<int>(p->wpb);
-  const unsigned grid = std::min<unsigned>(resident_grid(k, threads), a.num_lblocks);
-  k<<<grid, threads, 0, st>>>(a);
+  const unsigned full = resident_grid(k, threads);
+  const unsigned grid = std::min<unsigned>(full, a.num_lblocks);
+  k<<<grid, threads, dyn_smem(k, threads), st>>>(a);
+  {
+    int dev = 0, sms = 0;
+    MGG_CUDA(cudaGetDevice(&dev));
+    MGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    p->last_grid = grid;
+    p->last_threads = static_cast<uint32_t>(threads);
+    p->last_sms = static_cast<uint32_t>(sms);
+    p->last_resident = full / std::max(1, sms);
+  }
   MGG_CUDA(cudaGetLastError());
   count_launch(ctx);
   if (!p->k1_names.empty()) p->k1_names += ';';

@@ -49,6 +49,7 @@ struct mgg_ctx {
   // logical partitions); the K3 barrier becomes a cross-stream event join
   bool part_streams = false;
   std::vector<cudaEvent_t> bar_ev;     // per part: barrier join events
+  std::vector<int> shard_mem;          // per part: MGG_MEM_* of new stores
 };
 
 struct mgg_store {
@@ -57,6 +58,8 @@ struct mgg_store {
   std::vector<uint64_t> lb;            // num_parts + 1
   std::vector<float*> shard;           // as seen by this process
   std::vector<uint8_t> owned, imported;
+  std::vector<uint8_t> mem;            // per part: MGG_MEM_* of the shard
+  std::vector<size_t> bytes;           // per local part: shard allocation
   // per local part: device copy of the shard table for that part's device
   std::vector<const float**> dtable;
   // per local part: two dense H2D/D2H slabs (2p, 2p+1) and their events
@@ -111,6 +114,8 @@ struct mgg_dplan {
   // kernels launched by the plan's latest K1 (';'-separated, demangled;
   // mgg_dplan_k1_kernels) — the bench labels its roofline with them
   mutable std::string k1_names;
+  // geometry of the plan's latest K1 launch (mgg_dplan_k1_launch_info)
+  mutable uint32_t last_grid = 0, last_threads = 0, last_resident = 0, last_sms = 0;
 };
 
 namespace mgg::dev {
@@ -156,6 +161,8 @@ void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t ro
                      const float* wt, const float* bias, const float* pre_bias, uint32_t m,
                      uint32_t pre, uint32_t act, float* out, uint32_t out_pitch, float* out2,
                      float out2_scale, cudaStream_t st, const float* row_scale = nullptr);
+/// Managed shards of `s` back to their home (see mgg_store_rehome).
+void rehome(mgg_store* s, cudaStream_t st);
 void launch_barrier(unsigned* const* flag_shards_dev, unsigned* own, uint32_t me,
                     uint32_t num_parts, uint32_t epoch, cudaStream_t st);
 

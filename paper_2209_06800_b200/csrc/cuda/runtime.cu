@@ -105,6 +105,21 @@ T* upload_array(const T* host, size_t n, cudaStream_t st) {
 
 }  // namespace
 
+// Managed shards back to their home (owner device or host), ordered on `st`
+// (each part's own stream when null), and waited for when st is null.
+void rehome(mgg_store* s, cudaStream_t st) {
+  mgg_ctx* ctx = s->ctx;
+  for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+    if (!s->owned[p] || (s->mem[p] != MGG_MEM_MANAGED && s->mem[p] != MGG_MEM_MANAGED_HOST))
+      continue;
+    MGG_CUDA(cudaSetDevice(ctx->device[p]));
+    const int home = s->mem[p] == MGG_MEM_MANAGED ? ctx->device[p] : cudaCpuDeviceId;
+    cudaStream_t q = st ? st : ctx->stream[p];
+    MGG_CUDA(cudaMemPrefetchAsync(s->shard[p], s->bytes[p], home, q));
+    if (!st) MGG_CUDA(cudaStreamSynchronize(q));
+  }
+}
+
 void launch_barrier(unsigned* const* shards, unsigned* own, uint32_t me, uint32_t n,
                     uint32_t epoch, cudaStream_t st) {
   barrier_kernel<<<1, 32, 0, st>>>(shards, own, me, n, epoch);
@@ -186,6 +201,7 @@ int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out
       c->rp.assign(num_parts, nullptr);
       c->lane_ev.assign(num_parts, std::vector<cudaEvent_t>(9, nullptr));
       c->marks.assign(num_parts, {});
+      c->shard_mem.assign(num_parts, MGG_MEM_DEVICE);
       int first = -1;
       for (uint32_t p = 0; p < num_parts; ++p) {
         const int d = c->device[p];
@@ -452,6 +468,23 @@ int mgg_event_elapsed(mgg_ctx* ctx, uint32_t part, uint32_t a, uint32_t b, float
   });
 }
 
+int mgg_event_elapsed_between(mgg_ctx* ctx, uint32_t part_a, uint32_t a, uint32_t part_b,
+                              uint32_t b, float* ms) {
+  return guard([&] {
+    enter(ctx, part_a);
+    enter(ctx, part_b);
+    if (ctx->device[part_a] != ctx->device[part_b])
+      throw Status{MGG_E_INPUT, "event_elapsed_between: parts on different devices"};
+    const auto& pa = ctx->evpool[part_a];
+    const auto& pb = ctx->evpool[part_b];
+    if (a >= pa.size() || b >= pb.size() || !pa[a] || !pb[b])
+      throw Status{MGG_E_INPUT, "event_elapsed_between: slot never recorded"};
+    MGG_CUDA(cudaEventSynchronize(pb[b]));
+    MGG_CUDA(cudaEventSynchronize(pa[a]));
+    MGG_CUDA(cudaEventElapsedTime(ms, pa[a], pb[b]));
+  });
+}
+
 int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_store** out) {
   return guard([&] {
     if (!ctx || !part_lb || !out) throw Status{MGG_E_INPUT, "store_create: null argument"};
@@ -467,6 +500,8 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
       s->shard.assign(ctx->num_parts, nullptr);
       s->owned.assign(ctx->num_parts, 0);
       s->imported.assign(ctx->num_parts, 0);
+      s->mem.assign(ctx->num_parts, MGG_MEM_DEVICE);
+      s->bytes.assign(ctx->num_parts, 0);
       s->dtable.assign(ctx->num_parts, nullptr);
       s->stage.assign(2 * ctx->num_parts, nullptr);
       s->stage_ev.assign(5 * ctx->num_parts, nullptr);
@@ -474,21 +509,71 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
         if (ctx->device[p] < 0) continue;
         MGG_CUDA(cudaSetDevice(ctx->device[p]));
         const size_t bytes = std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256);
+        const int kind = ctx->shard_mem[p];
         void* d = nullptr;
-        MGG_CUDA(cudaMalloc(&d, bytes));
+        switch (kind) {
+          case MGG_MEM_HOST_MAPPED: {
+            void* h = nullptr;
+            MGG_CUDA(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+            std::memset(h, 0, bytes);
+            s->shard[p] = static_cast<float*>(h);  // freed through the host pointer
+            MGG_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+            if (d != h) {
+              cudaFreeHost(h);
+              s->shard[p] = nullptr;
+              throw Status{MGG_E_CUDA, "store_create: host-mapped shard needs unified addressing"};
+            }
+            break;
+          }
+          case MGG_MEM_MANAGED:
+          case MGG_MEM_MANAGED_HOST:
+            MGG_CUDA(cudaMallocManaged(&d, bytes, cudaMemAttachGlobal));
+            break;
+          default:
+            MGG_CUDA(cudaMalloc(&d, bytes));
+        }
         s->shard[p] = static_cast<float*>(d);
         s->owned[p] = 1;
-        // zero padding/rows on the part's stream, complete before any use
-        // (a legacy-stream memset is not ordered before non-blocking streams)
-        MGG_CUDA(cudaMemsetAsync(d, 0, bytes, ctx->stream[p]));
-        MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
+        s->mem[p] = static_cast<uint8_t>(kind);
+        s->bytes[p] = bytes;
+        if (kind != MGG_MEM_HOST_MAPPED) {
+          // zero padding/rows on the part's stream, complete before any use
+          // (a legacy-stream memset is not ordered before non-blocking streams)
+          MGG_CUDA(cudaMemsetAsync(d, 0, bytes, ctx->stream[p]));
+          MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
+        }
       }
       refresh_tables(s);
+      rehome(s, nullptr);
     } catch (...) {
       mgg_store_destroy(s);
       throw;
     }
     *out = s;
+  });
+}
+
+int mgg_ctx_set_shard_memory(mgg_ctx* ctx, uint32_t part, int kind) {
+  return guard([&] {
+    enter(ctx, part);
+    if (kind < MGG_MEM_DEVICE || kind > MGG_MEM_MANAGED_HOST)
+      throw Status{MGG_E_INPUT, "set_shard_memory: unknown memory kind"};
+    if (kind != MGG_MEM_DEVICE) {
+      int v = 0;
+      MGG_CUDA(cudaDeviceGetAttribute(&v, kind == MGG_MEM_HOST_MAPPED
+                                              ? cudaDevAttrCanMapHostMemory
+                                              : cudaDevAttrConcurrentManagedAccess,
+                                      ctx->device[part]));
+      if (!v) throw Status{MGG_E_CONFIG, "set_shard_memory: device cannot use that memory kind"};
+    }
+    ctx->shard_mem[part] = kind;
+  });
+}
+
+int mgg_store_rehome(mgg_store* s) {
+  return guard([&] {
+    if (!s) throw Status{MGG_E_INPUT, "store_rehome: null store"};
+    rehome(s, nullptr);
   });
 }
 
@@ -498,7 +583,10 @@ int mgg_store_destroy(mgg_store* s) {
   for (uint32_t p = 0; p < ctx->num_parts; ++p) {
     if (s->owned[p] && s->shard[p]) {
       cudaSetDevice(ctx->device[p]);
-      cudaFree(s->shard[p]);
+      if (s->mem[p] == MGG_MEM_HOST_MAPPED)
+        cudaFreeHost(s->shard[p]);
+      else
+        cudaFree(s->shard[p]);
     }
     if (s->imported[p] && s->shard[p]) cudaIpcCloseMemHandle(s->shard[p]);
     if (s->dtable[p]) {
@@ -528,6 +616,8 @@ int mgg_store_ipc_export(const mgg_store* s, uint32_t part, void* handle64) {
   return guard([&] {
     if (!s || part >= s->ctx->num_parts || !s->owned[part])
       throw Status{MGG_E_INPUT, "ipc_export: part is not a local shard"};
+    if (s->mem[part] != MGG_MEM_DEVICE)
+      throw Status{MGG_E_CONFIG, "ipc_export: shard is not device memory"};
     MGG_CUDA(cudaSetDevice(s->ctx->device[part]));
     cudaIpcMemHandle_t h;
     MGG_CUDA(cudaIpcGetMemHandle(&h, s->shard[part]));
@@ -911,6 +1001,15 @@ int mgg_dplan_k1_kernels(const mgg_dplan* plan, char* buf, size_t cap) {
   return MGG_OK;
 }
 
+int mgg_dplan_k1_launch_info(const mgg_dplan* plan, uint32_t* info) {
+  if (!plan || !info) return MGG_E_INPUT;
+  info[0] = plan->last_grid;
+  info[1] = plan->last_threads;
+  info[2] = plan->last_resident;
+  info[3] = plan->last_sms;
+  return MGG_OK;
+}
+
 int mgg_dplan_halo_len(const mgg_dplan* plan, uint64_t* n) {
   if (!plan || !n) return MGG_E_INPUT;
   *n = plan->halo_len;
@@ -1056,8 +1155,15 @@ int mgg_time_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in,
     cudaStream_t st = enter(ctx, plan->part);
     reps = std::max(reps, 1u);
     std::vector<float> ms(reps);
+    bool paged = false;
+    for (uint32_t q = 0; q < ctx->num_parts; ++q)
+      paged |= in->owned[q] && (in->mem[q] == MGG_MEM_MANAGED || in->mem[q] == MGG_MEM_MANAGED_HOST);
     run_aggregate(ctx, plan, in, out, opts, st);
     for (uint32_t r = 0; r < reps; ++r) {
+      if (paged) {  // every rep starts with the pages at home (outside the window)
+        rehome(const_cast<mgg_store*>(in), st);
+        MGG_CUDA(cudaSetDevice(ctx->device[plan->part]));
+      }
       MGG_CUDA(cudaEventRecord(ctx->ev0[plan->part], st));
       run_aggregate(ctx, plan, in, out, opts, st);
       MGG_CUDA(cudaEventRecord(ctx->ev1[plan->part], st));

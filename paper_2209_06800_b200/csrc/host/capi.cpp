@@ -513,6 +513,46 @@ int mgg_engine_time_aggregate(mgg_engine* e, uint32_t dim, uint32_t reps, int ph
                               uint64_t* ns) {
   return guard([&] { *ns = e->e->time_aggregate(dim, reps, phase); });
 }
+int mgg_engine_time_aggregate_each(mgg_engine* e, uint32_t dim, uint32_t reps, int phase,
+                                   uint64_t* ns) {
+  return guard([&] {
+    if (!ns) throw mgg::InputError("time_aggregate_each: null output");
+    const auto v = e->e->time_aggregate_each(dim, reps, phase);
+    std::memcpy(ns, v.data(), v.size() * sizeof(uint64_t));
+  });
+}
+int mgg_engine_measure_multi_gpu(mgg_engine* e, uint32_t dim, uint32_t reps,
+                                 uint64_t* summary, uint64_t* per_part, double* per_part_f) {
+  return guard([&] {
+    if (!summary || !per_part || !per_part_f)
+      throw mgg::InputError("measure_multi_gpu: null output");
+    const auto r = e->e->measure_multi_gpu(dim, reps);
+    summary[0] = r.max_gpu_ns;
+    summary[1] = r.barrier_ns;
+    summary[2] = r.total_ns;
+    summary[3] = r.remote_bytes;
+    const uint32_t n = e->e->num_parts();
+    std::memset(per_part, 0, sizeof(uint64_t) * 9 * n);
+    std::memset(per_part_f, 0, sizeof(double) * 2 * n);
+    for (const auto& p : r.per_gpu) {
+      uint64_t* q = per_part + 9 * p.part;
+      q[0] = 1;
+      q[1] = p.total_ns;
+      q[2] = p.alone_ns;
+      q[3] = p.remote_bytes;
+      q[4] = p.local_bytes;
+      q[5] = p.num_warps;
+      q[6] = p.num_blocks;
+      q[7] = p.active_sms;
+      q[8] = p.part;
+      per_part_f[2 * p.part] = p.achieved_occupancy;
+      per_part_f[2 * p.part + 1] = p.sm_utilization;
+    }
+  });
+}
+int mgg_engine_set_shard_memory(mgg_engine* e, uint32_t part, int kind) {
+  return guard([&] { e->e->set_shard_memory(part, kind); });
+}
 int mgg_engine_trace_csv(mgg_engine* e, uint32_t dim, uint64_t capacity, uint32_t warp_limit,
                          char** csv) {
   return guard([&] {

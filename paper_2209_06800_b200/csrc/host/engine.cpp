@@ -715,17 +715,132 @@ std::pair<mgg_store*, mgg_store*> Engine::agg_stores(std::uint32_t dim) {
 }
 
 std::uint64_t Engine::time_aggregate(std::uint32_t dim, std::uint32_t reps, int phase) {
+  const auto each = time_aggregate_each(dim, reps, phase);
+  return each.empty() ? 0 : *std::max_element(each.begin(), each.end());
+}
+
+std::vector<std::uint64_t> Engine::time_aggregate_each(std::uint32_t dim, std::uint32_t reps,
+                                                       int phase) {
   auto [in, out] = agg_stores(dim);
-  std::uint64_t worst = 0;
+  std::vector<std::uint64_t> ns(num_parts_, 0);
   for (std::uint32_t p = 0; p < num_parts_; ++p) {
     if (dev_[p] < 0) continue;
-    std::uint64_t ns = 0;
     // halo mode: each timed rep includes the deduplicated pull
     mgg_agg_opts o{0, phase, halo_for(p, dim), 1};
-    ok(mgg_time_aggregate(ctx_, plans_[p], in, out, &o, reps, &ns));
-    worst = std::max(worst, ns);
+    ok(mgg_time_aggregate(ctx_, plans_[p], in, out, &o, reps, &ns[p]));
   }
-  return worst;
+  return ns;
+}
+
+Engine::MultiGpuReport Engine::measure_multi_gpu(std::uint32_t dim, std::uint32_t reps) {
+  reps = std::max(reps, 1u);
+  auto [in, out] = agg_stores(dim);
+  const auto alone = time_aggregate_each(dim, reps, 0);
+  std::vector<std::uint32_t> local;
+  for (std::uint32_t p = 0; p < num_parts_; ++p)
+    if (dev_[p] >= 0) local.push_back(p);
+  if (local.empty()) throw InputError("engine: no local part");
+  const std::uint32_t p0 = local.front();
+  bool one_device = true;
+  for (auto p : local) one_device &= dev_[p] == dev_[p0];
+  // slots: per part [base + 3r] start, [+1] K1 end, [+2] after the barrier
+  constexpr std::uint32_t base = 200000;
+  std::vector<std::vector<float>> k1(num_parts_), upto(num_parts_);
+  for (std::uint32_t r = 0; r <= reps; ++r) {  // rep 0 warms up
+    ok(mgg_barrier(ctx_, flags_));  // start-aligned: every part past its tail
+    for (auto p : local) ok(mgg_event_record(ctx_, p, base + 3 * r));
+    for (auto p : local) {
+      mgg_agg_opts o{0, 0, halo_for(p, dim), 1};
+      ok(mgg_aggregate(ctx_, plans_[p], in, out, &o));
+      ok(mgg_event_record(ctx_, p, base + 3 * r + 1));
+    }
+    ok(mgg_barrier(ctx_, flags_));
+    for (auto p : local) ok(mgg_event_record(ctx_, p, base + 3 * r + 2));
+  }
+  for (std::uint32_t r = 1; r <= reps; ++r)
+    for (auto p : local) {
+      float a = 0, b = 0;
+      ok(mgg_event_elapsed(ctx_, p, base + 3 * r, base + 3 * r + 1, &a));
+      if (one_device)  // parts of one device: from the common start
+        ok(mgg_event_elapsed_between(ctx_, p0, base + 3 * r, p, base + 3 * r + 2, &b));
+      else
+        ok(mgg_event_elapsed(ctx_, p, base + 3 * r, base + 3 * r + 2, &b));
+      k1[p].push_back(a);
+      upto[p].push_back(b);
+    }
+  auto median = [](std::vector<float> v) {
+    std::sort(v.begin(), v.end());
+    return static_cast<std::uint64_t>(double(v[v.size() / 2]) * 1e6);
+  };
+  MultiGpuReport rep;
+  std::uint64_t until = 0;
+  for (auto p : local) {
+    PartReport pr;
+    pr.part = p;
+    pr.total_ns = median(k1[p]);
+    pr.alone_ns = alone[p];
+    std::uint32_t info[4] = {0, 0, 0, 0};
+    ok(mgg_dplan_k1_launch_info(plans_[p], info));
+    const double slots_per_sm = 2048.0;  // 64 resident warps per sm_100 SM
+    pr.active_sms = std::min(info[0], info[3]);
+    const double per_sm = info[3] ? double(info[0]) / info[3] : 0.0;  // CTAs per SM
+    pr.achieved_occupancy = std::min(per_sm, double(info[2])) * info[1] / slots_per_sm;
+    pr.sm_utilization = info[3] ? double(pr.active_sms) / info[3] : 0.0;
+    pr.kernels = k1_kernels(p);
+    std::uint32_t pitch = 0;
+    ok(mgg_store_info(in, nullptr, &pitch));
+    const FlatPlan fp =
+        build_flat_plan(g_, split_, ne_, p, cfg_, spec_.in_dim, mapping_, granularity_);
+    std::uint64_t halo_rows = 0;
+    ok(mgg_dplan_halo_len(plans_[p], &halo_rows));
+    pr.local_bytes = std::uint64_t(fp.local.cols.size()) * pitch * 4;
+    pr.remote_bytes =
+        (halo_for(p, dim) ? halo_rows : std::uint64_t(fp.remote.cols.size())) * pitch * 4;
+    pr.num_warps = static_cast<std::uint32_t>(fp.num_warps());
+    pr.num_blocks = static_cast<std::uint32_t>(fp.num_blocks());
+    rep.max_gpu_ns = std::max(rep.max_gpu_ns, pr.total_ns);
+    until = std::max(until, median(upto[p]));
+    rep.remote_bytes += pr.remote_bytes;
+    rep.mean_occupancy += pr.achieved_occupancy / local.size();
+    rep.mean_utilization += pr.sm_utilization / local.size();
+    rep.per_gpu.push_back(std::move(pr));
+  }
+  rep.total_ns = std::max(until, rep.max_gpu_ns);
+  rep.barrier_ns = rep.total_ns - rep.max_gpu_ns;
+  return rep;
+}
+
+void Engine::set_shard_memory(std::uint32_t part, int kind) {
+  if (part >= num_parts_ || dev_[part] < 0) throw InputError("engine: part is not local");
+  for (auto d : dev_)
+    if (d < 0) throw InputError("engine: shard memory kinds need every part in this process");
+  synchronize();
+  drop_exec();
+  ok(mgg_ctx_set_shard_memory(ctx_, part, kind));
+  std::vector<std::uint64_t> lb(num_parts_ + 1);
+  for (std::uint32_t p = 0; p < num_parts_; ++p) lb[p] = ne_.ranges[p].lb;
+  lb[num_parts_] = g_.num_nodes;
+  const bool dbl = in_bufs_[1] != nullptr;
+  for (auto* s : in_bufs_)
+    if (s && s != stores_[input_]) mgg_store_destroy(s);
+  in_bufs_[0] = in_bufs_[1] = nullptr;
+  in_marked_[0] = in_marked_[1] = false;
+  for (auto& s : stores_) {
+    std::uint32_t dim = 0;
+    ok(mgg_store_info(s, &dim, nullptr));
+    mgg_store_destroy(s);
+    s = nullptr;
+    ok(mgg_store_create(ctx_, lb.data(), dim, &s));
+  }
+  if (dbl) {
+    in_bufs_[0] = stores_[input_];
+    ok(mgg_store_create(ctx_, lb.data(), spec_.in_dim, &in_bufs_[1]));
+  }
+  for (auto*& s : scratch_) {
+    mgg_store_destroy(s);
+    s = nullptr;
+  }
+  eager_warm_ = false;
 }
 
 std::string Engine::trace_csv(std::uint32_t dim, std::uint64_t capacity,

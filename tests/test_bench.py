@@ -58,6 +58,63 @@ def test_reference_arm_json_line():
     assert line["e2e"]["h2d_bytes_per_step"] == 0
 
 
+def test_reference_arm_never_loads_the_product():
+    # the reference arm builds its graph/X/W from oracle/ and numpy only
+    code = (f"import runpy, sys; sys.path.insert(0, {ROOT!r}); "
+            "sys.argv = ['bench.py', '--impl', 'reference', '--workload', 'config1', "
+            "'--steps', '1', '--warmup', '0']; "
+            f"runpy.run_path({os.path.join(ROOT, 'bench.py')!r}, run_name='__main__'); "
+            "bad = [m for m in sys.modules if m.startswith('paper_2209_06800_b200')]; "
+            "assert not bad, bad; "
+            "maps = open('/proc/self/maps').read(); assert 'libmgg' not in maps")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env={**os.environ, "RANK": "0"})
+    assert out.returncode == 0, out.stderr[-2000:]
+
+
+def test_reference_inputs_identical_to_product_inputs(mgg):
+    import numpy as np
+    for name in ("config1", "products-gcn", "products-gin", "reddit-gcn-norm"):
+        mspec = bench.WORKLOADS[name][2]
+        a = bench.np_model(mspec)
+        mk, din, hid, out, layers = mspec
+        b = (mgg.make_gcn(din, hid, out, seed=2, norm=mk == "gcn-norm") if mk != "gin"
+             else mgg.make_gin(din, hid, out, layers=layers, seed=2))
+        for f in ("kind", "layers", "in_dim", "hidden", "out_dim", "eps", "norm"):
+            assert getattr(a, f) == getattr(b, f), (name, f)
+        for f in ("w1", "b1", "w2", "b2"):
+            x, y = getattr(a, f), getattr(b, f)
+            assert (x is None and y is None) or np.array_equal(x, y), (name, f)
+    assert np.array_equal(bench.np_features(1000, 37, 1), mgg.random_features(1000, 37, 1))
+    rp, cl, _, _ = bench.ref_graph("config1")
+    g = mgg.gen_rmat(100_000, 1_600_000, 0)
+    assert np.array_equal(rp, g.row_ptr) and np.array_equal(cl, g.col_idx)
+
+
+def test_reference_and_product_configs_agree():
+    import types
+    args = types.SimpleNamespace(ps=16, dist=8, wpb=8, k1_form=0, fetch="auto")
+    m = bench.np_model(bench.WORKLOADS["products-gcn"][2])
+    a = bench.workload_config("products-gcn", args, 10, 20, m, 1)
+    assert a == bench.workload_config("products-gcn", args, 10, 20, m, 1)
+    assert "layer_forward_ms" not in a  # nothing measured in the config
+
+
+def test_roofline_bound_by_table_size():
+    # Reddit-shaped width 16: 15 MB table -> L2-bound, rows-only bytes vs probe
+    r = bench.roofline(232_965, 114_166_771, 3_700_000, 232_965, 16, 0.53, 15_000.0,
+                       534_887_424, ["agg_local<4, false, 2>"])
+    assert r["bound"] == "l2" and r["peak"] == 15_000.0
+    assert abs(r["achieved"] - 114_166_771 * 64 / 0.53e-3 / 1e9) < 1
+    assert r["frac"] < 1.2 and r["dram"]["frac"] < 0.2
+    # products-shaped: 157 MB table -> HBM-bound on the algorithmic bytes
+    r = bench.roofline(2_449_029, 60_800_000, 4_000_000, 2_449_029, 16, 0.71, 15_000.0,
+                       4_390_000_000, ["agg_group_hint<4, false, 8>"])
+    assert r["bound"] == "hbm" and r["peak_source"] in ("measured", "fallback")
+    assert 0.5 < r["frac"] < 1.2
+    assert "agg_group_hint" in r["kernel"]
+
+
 def test_reference_arm_nonzero_rank_is_silent():
     out = subprocess.run(
         [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",

@@ -585,8 +585,10 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
     assert np.abs(z2 - zr).max() <= TOL, np.abs(z2 - zr).max()
 
 
-@pytest.mark.parametrize("pair,kernel", [("1", "agg_gpair"), ("0", "agg_kernel")])
-def test_pair_kernel_forms(pair, kernel):
+@pytest.mark.parametrize("pair,depth,kernel", [("1", "8", "agg_gpair"), ("0", "8", "agg_kernel"),
+                                               ("2", "8", "agg_pipe"), ("2", "4", "agg_pipe"),
+                                               ("2", "16", "agg_pipe")])
+def test_pair_kernel_forms(pair, depth, kernel):
     # the fine-fetch pair loop: agg_gpair (default) and the warp-window loop
     # (MGG_AGG_PAIR=0, read once per process) on single-process multi-part
     # aggregations against the oracle; the launched kernel is read back
@@ -598,9 +600,10 @@ def test_pair_kernel_forms(pair, kernel):
 import sys; sys.path.insert(0, {root!r})
 import numpy as np, oracle, paper_2209_06800_b200 as mgg
 g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 18, 12)
-for dim, parts in ((16, 2), (64, 3), (200, 4)):
+for dim, parts, cfg in ((16, 2, (16, 4, 4)), (64, 3, (16, 4, 4)), (200, 4, (16, 4, 4)),
+                        (3, 2, (32, 16, 2)), (16, 4, (1, 1, 1)), (32, 2, (8, 16, 16))):
     x = mgg.random_features(g.num_nodes, dim, seed=dim)
-    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 8), ps=16, dist=4, wpb=4)
+    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 8), *cfg)
     eng.set_remote_fetch("fine")
     ref = oracle.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
     out = eng.aggregate(x, 1.0, relu_in=True)
@@ -613,7 +616,8 @@ for dim, parts in ((16, 2), (64, 3), (200, 4)):
 print("ok")
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                       timeout=600, env={**os.environ, "MGG_AGG_PAIR": pair})
+                       timeout=600, env={**os.environ, "MGG_AGG_PAIR": pair,
+                                         "MGG_AGG_PIPE_DEPTH": depth})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
@@ -648,3 +652,57 @@ def test_store_copy_row_layouts(mgg, dim, ld_kind):
     assert np.array_equal(back[:, :dim], host[:, :dim])
     assert np.all(back[:, dim:] == 7.0), "download wrote past dim into the caller's row padding"
     assert np.array_equal(raw[:, :dim], host[:, :dim])
+
+
+@pytest.mark.parametrize("kind", [1, 2, 3])
+@pytest.mark.parametrize("fetch", ["fine", "halo"])
+def test_shard_memory_kinds_match_oracle(mgg, oracle_mod, kind, fetch):
+    """Part 1's shards in host-mapped (slow-peer emulation) or managed memory
+    (the paged_remote baseline, R:proj/src/sim.cpp:571-595): the same sums and
+    the same forward as device shards."""
+    g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 18, 7)
+    x = mgg.random_features(g.num_nodes, 16, seed=3)
+    model = mgg.make_gcn(16, 16, 8)
+    eng = mgg.Engine(g, 2, [0, 0], model, ps=16, dist=4, wpb=4)
+    eng.set_remote_fetch(fetch)
+    eng.set_shard_memory(1, kind)
+    out = eng.aggregate(x, 1.0)
+    assert_rows_close(out, oracle_mod.aggregate(g.row_ptr, g.col_idx, x),
+                      what=f"kind={kind} {fetch}")
+    each = eng.time_aggregate_each(16, 2, 0)  # paged: every rep re-homes first
+    assert all(t > 0 for t in each)
+    eng.set_input(x)
+    eng.forward()
+    z = eng.get_output()
+    _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+    assert np.abs(z - zr).max() <= TOL
+    eng.set_shard_memory(1, mgg.MEM_DEVICE)  # and back
+    assert_rows_close(eng.aggregate(x, 1.0), oracle_mod.aggregate(g.row_ptr, g.col_idx, x))
+    eng.close()
+
+
+@pytest.mark.parametrize("parts,fetch", [(1, "auto"), (2, "fine"), (4, "halo")])
+def test_measure_multi_gpu_report(mgg, parts, fetch):
+    """The measured MultiGpuReport: per part concurrent + alone ns, remote
+    bytes (fine: every remote edge's row; halo: each distinct row once),
+    total = max + barrier (R:proj/src/sim.cpp:597-624)."""
+    g = mgg.gen_synthetic(mgg.POWERLAW, 20000, 30, 9)
+    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(16, 16, 8), ps=16, dist=4, wpb=4)
+    eng.set_remote_fetch(fetch)
+    r = eng.measure_multi_gpu(16, 3)
+    assert len(r["per_gpu"]) == parts
+    assert r["total_ns"] == r["max_gpu_ns"] + r["barrier_ns"]
+    assert r["max_gpu_ns"] == max(p["total_ns"] for p in r["per_gpu"])
+    for p in r["per_gpu"]:
+        fp = mgg.build_flat_plan(g, parts, p["part"], 16, 4, 4, 16)
+        assert p["local_bytes"] == fp.local_cols_len * 64
+        if fetch == "fine":
+            assert p["remote_bytes"] == fp.remote_cols_len * 64
+        elif parts > 1:
+            assert 0 < p["remote_bytes"] < fp.remote_cols_len * 64
+        assert p["alone_ns"] > 0 and p["total_ns"] > 0
+        assert 0 < p["achieved_occupancy"] <= 1 and 0 < p["sm_utilization"] <= 1
+        assert p["num_blocks"] == fp.num_blocks and p["num_warps"] == fp.num_warps
+    if parts == 1:
+        assert r["remote_bytes"] == 0
+    eng.close()
