@@ -290,9 +290,15 @@ int mgg_dense_chain(mgg_ctx* ctx, uint32_t part, const mgg_store* in,
 int mgg_dense_chain_supported(uint32_t k, uint32_t m1, uint32_t m);
 
 /* K3 — cross-GPU layer barrier (R:PAPER.md:258 "result synchronization at
- * the end"; barrier_cycles, R:proj/src/sim.cpp:620): device-side flags in
- * peer-mapped memory, release/acquire at system scope, no host round trip.
- * No-op when every part is local to this process (stream order suffices). */
+ * the end"; barrier_cycles, R:proj/src/sim.cpp:620), never a host round trip:
+ *  - every part in this process (one device or several): each part's stream
+ *    waits for every other part's tail through events (cudaStreamWaitEvent
+ *    orders streams across devices; capturable into one CUDA graph);
+ *  - parts in other processes: the K3 kernel — release/acquire flags at
+ *    system scope in the peer-mapped `flags` store (one row per part, at
+ *    least num_parts + 1 columns: arrivals + the part's device-side epoch
+ *    counter, so captured barriers advance on every replay).
+ * MGG_BARRIER=k3 forces the kernel for same-process parts too (validation). */
 int mgg_barrier(mgg_ctx* ctx, mgg_store* flags);
 
 /* Timing with CUDA events on the part's stream around `reps` launches of
@@ -498,6 +504,9 @@ int mgg_engine_submit_host(mgg_engine* e, const float* x, float* z, uint64_t* ti
 int mgg_engine_wait(mgg_engine* e, uint64_t ticket);
 /* Layer-k intermediate (post-aggregation accumulator) rows, for parity. */
 int mgg_engine_get_hidden(mgg_engine* e, uint32_t which, float* rows, uint32_t* width);
+/* Pre-softmax logits of the last forward (N x out_dim): the engine's head
+ * GEMM re-run on the device without the softmax epilogue. */
+int mgg_engine_get_logits(mgg_engine* e, float* rows);
 /* Standalone aggregation through the engine's plans (K1 over every local
  * part): out = self_scale*f(x) + Σ f(x_u); x/out num_nodes x dim host rows. */
 int mgg_engine_aggregate_host(mgg_engine* e, const float* x, uint32_t dim,

@@ -93,6 +93,10 @@ class Engine {
   void wait(std::uint64_t ticket);
   /// Post-aggregation accumulator of layer `which` (N x width host rows).
   std::uint32_t get_hidden(std::uint32_t which, float* rows);
+  /// Pre-softmax logits of the last forward (N x out_dim host rows): the
+  /// head K2 re-run on the device without its softmax epilogue (or the
+  /// aggregated rows a softmax pass reads). Returns the width; rows may be null.
+  std::uint32_t get_logits(float* rows);
 
   /// Standalone K1 through the engine's plans (single-process only);
   /// phase 1 = local partitions only, 2 = remote only (0 = both).

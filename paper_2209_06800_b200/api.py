@@ -499,6 +499,13 @@ class Engine:
         check(lib.mgg_engine_time_aggregate(self._h, dim, reps, phase, C.byref(ns)))
         return ns.value
 
+    def get_logits(self) -> np.ndarray:
+        """Pre-softmax logits of the last forward (the engine's head K2, no
+        softmax epilogue), N x out_dim."""
+        z = np.zeros((self.graph.num_nodes, self.model.out_dim), np.float32)
+        check(lib.mgg_engine_get_logits(self._h, _p(z, C.c_float)))
+        return z
+
     def time_aggregate_each(self, dim: int, reps: int = 5, phase: int = 0) -> list[int]:
         """Median K1 ns per part, each part alone (0 for remote parts)."""
         ns = np.zeros(self.num_parts, np.uint64)

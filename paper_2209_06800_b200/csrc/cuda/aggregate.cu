@@ -853,22 +853,29 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
   cta_chunk(a.num_lblocks, b0, b1);
   const uint32_t wib = threadIdx.x >> 5;
 
-  // producer cursor: the group's remote rows in consumption order
+  // producer cursor over the group's remote rows in consumption order, kept
+  // one row (column id in flight) and one partition (bounds in flight) ahead
+  // so that issuing a copy never waits on a dependent metadata load
   uint32_t plb = b0, pw = b0 * a.wpb + wib, pr0 = 0, pr1 = 0, pi = grp;
-  int pk = 0, pend = 0;
-  bool pdone = b0 >= b1 || pw >= a.num_warps;
+  int pk = 0, pend = 0, qk = 0, qend = 0;
+  uint32_t ncol = 0;
+  bool qvalid = false, pdone = b0 >= b1 || pw >= a.num_warps;
   if (!pdone) {
     uint32_t l0, l1;
     warp_groups(a, pw, l0, l1, pr0, pr1);
   }
-  uint32_t issued = 0, consumed = 0;
-  auto produce = [&]() {
-    while (!pdone && pk >= pend) {  // open the next non-empty remote partition
+  // queue the bounds of the next remote partition of this group (no wait)
+  auto queue_next = [&]() {
+    qvalid = false;
+    while (!pdone) {
       if (pr0 + pi < pr1) {
-        pk = __ldg(&a.rmeta[pr0 + pi].y);
-        pend = __ldg(&a.rmeta[pr0 + pi + 1].y);
+        qk = __ldg(&a.rmeta[pr0 + pi].y);
+        qend = __ldg(&a.rmeta[pr0 + pi + 1].y);
         pi += G;
-      } else if (++plb >= b1 || (pw += a.wpb) >= a.num_warps) {
+        qvalid = true;
+        return;
+      }
+      if (++plb >= b1 || (pw += a.wpb) >= a.num_warps) {
         pdone = true;
       } else {
         uint32_t l0, l1;
@@ -876,9 +883,30 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
         pi = grp;
       }
     }
-    if (!pdone) {
-      const char* src = raddr(__ldg(a.rcols + pk));
-      ++pk;
+  };
+  // make the queued partition current (skipping empty ones)
+  auto advance = [&]() {
+    while (qvalid) {
+      pk = qk;
+      pend = qend;
+      queue_next();
+      if (pk < pend) {
+        ncol = __ldg(a.rcols + pk);
+        return;
+      }
+    }
+  };
+  queue_next();
+  advance();
+  uint32_t issued = 0, consumed = 0;
+  auto produce = [&]() {
+    if (pk < pend) {
+      const uint32_t c = ncol;
+      if (++pk < pend)
+        ncol = __ldg(a.rcols + pk);  // used by the next call
+      else
+        advance();
+      const char* src = raddr(c);
       const uint32_t dst = ring0 + (issued & (R - 1)) * rstride;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
@@ -1189,10 +1217,10 @@ const std::string& kernel_name(const void* fn) {
     char* dm = abi::__cxa_demangle(raw, nullptr, nullptr, &st);
     name = st == 0 && dm ? dm : raw;
     std::free(dm);
-    const auto paren = name.find('(');  // drop the parameter list
-    if (paren != std::string::npos) name.resize(paren);
     for (const char* pre : {"void ", "(anonymous namespace)::", "mgg::dev::"})
       for (size_t q; (q = name.find(pre)) != std::string::npos;) name.erase(q, std::strlen(pre));
+    const auto paren = name.find('(');  // drop the parameter list
+    if (paren != std::string::npos) name.resize(paren);
   } else {
     cudaGetLastError();
   }

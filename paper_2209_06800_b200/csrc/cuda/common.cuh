@@ -42,7 +42,6 @@ struct mgg_ctx {
   uint64_t launches = 0;
   uint64_t capture_base = 0;           // launch count at mgg_capture_begin
   bool capturing = false;
-  uint32_t epoch = 0;                  // barrier generation
   bool all_local = true;
   bool single_device = true;
   // parts sharing a device get their own compute/aux streams (concurrent
@@ -164,6 +163,6 @@ void launch_dense_tc(const float* in, uint32_t in_pitch, uint32_t k, uint64_t ro
 /// Managed shards of `s` back to their home (see mgg_store_rehome).
 void rehome(mgg_store* s, cudaStream_t st);
 void launch_barrier(unsigned* const* flag_shards_dev, unsigned* own, uint32_t me,
-                    uint32_t num_parts, uint32_t epoch, cudaStream_t st);
+                    uint32_t num_parts, cudaStream_t st);
 
 }  // namespace mgg::dev

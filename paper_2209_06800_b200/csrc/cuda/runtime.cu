@@ -32,11 +32,15 @@ void count_launch(mgg_ctx* ctx, uint64_t n) { ctx->launches += n; }
 
 namespace {
 
-// K3: announce `epoch` to every part, then wait until every part announced.
+// K3: announce this barrier's epoch to every part, then wait until every part
+// announced it. The epoch lives on the device (own[n], this part's counter,
+// advanced by each barrier launch of the part — they are stream-ordered), so
+// a barrier captured into a CUDA graph still advances on every replay.
 __global__ void barrier_kernel(unsigned* const* shards, unsigned* own, uint32_t me,
-                               uint32_t n, uint32_t epoch) {
+                               uint32_t n) {
   const uint32_t q = threadIdx.x;
   __threadfence_system();  // this GPU's prior kernels' writes before the flag
+  const unsigned epoch = *reinterpret_cast<volatile unsigned*>(own + n) + 1;
   if (q < n) {
     unsigned* slot = shards[q] + me;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
@@ -52,6 +56,7 @@ __global__ void barrier_kernel(unsigned* const* shards, unsigned* own, uint32_t 
     } while (static_cast<int>(seen - epoch) < 0);
   }
   __syncwarp();
+  if (q == 0) own[n] = epoch;
 }
 
 template <class F>
@@ -121,8 +126,8 @@ void rehome(mgg_store* s, cudaStream_t st) {
 }
 
 void launch_barrier(unsigned* const* shards, unsigned* own, uint32_t me, uint32_t n,
-                    uint32_t epoch, cudaStream_t st) {
-  barrier_kernel<<<1, 32, 0, st>>>(shards, own, me, n, epoch);
+                    cudaStream_t st) {
+  barrier_kernel<<<1, 32, 0, st>>>(shards, own, me, n);
   MGG_CUDA(cudaGetLastError());
 }
 
@@ -385,19 +390,22 @@ int mgg_ctx_join(mgg_ctx* ctx) {
 int mgg_capture_begin(mgg_ctx* ctx) {
   return guard([&] {
     if (!ctx) throw Status{MGG_E_INPUT, "capture_begin: null context"};
-    if (!ctx->all_local || !ctx->single_device)
-      throw Status{MGG_E_CONFIG, "capture: needs one device and all parts local"};
+    if (!ctx->all_local)
+      throw Status{MGG_E_CONFIG, "capture: needs every part in this process"};
     if (ctx->capturing) throw Status{MGG_E_INPUT, "capture_begin: already capturing"};
     const uint32_t p0 = first_local(ctx);
     cudaStream_t st = enter(ctx, p0);
     MGG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
     ctx->capturing = true;
     ctx->capture_base = ctx->launches;
-    if (ctx->part_streams) {  // pull the other parts' streams into the capture
-      MGG_CUDA(cudaEventRecord(ctx->bar_ev[p0], st));
-      for (uint32_t p = 0; p < ctx->num_parts; ++p)
-        if (p != p0) MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[p0], 0));
-    }
+    // pull the other parts' streams (other devices' too) into the capture
+    MGG_CUDA(cudaEventRecord(ctx->bar_ev[p0], st));
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      if (p != p0 && ctx->stream[p] != st) {
+        enter(ctx, p);
+        MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[p0], 0));
+      }
+    enter(ctx, p0);
   });
 }
 
@@ -408,12 +416,14 @@ int mgg_capture_end(mgg_ctx* ctx, mgg_exec** out) {
     const uint32_t p = first_local(ctx);
     cudaStream_t st = enter(ctx, p);
     ctx->capturing = false;
-    if (ctx->part_streams)  // join the other parts' streams back
-      for (uint32_t q = 0; q < ctx->num_parts; ++q)
-        if (q != p) {
-          MGG_CUDA(cudaEventRecord(ctx->bar_ev[q], ctx->stream[q]));
-          MGG_CUDA(cudaStreamWaitEvent(st, ctx->bar_ev[q], 0));
-        }
+    for (uint32_t q = 0; q < ctx->num_parts; ++q)  // join the other parts' streams back
+      if (q != p && ctx->stream[q] != st) {
+        enter(ctx, q);
+        MGG_CUDA(cudaEventRecord(ctx->bar_ev[q], ctx->stream[q]));
+        enter(ctx, p);
+        MGG_CUDA(cudaStreamWaitEvent(st, ctx->bar_ev[q], 0));
+      }
+    enter(ctx, p);
     cudaGraph_t g = nullptr;
     MGG_CUDA(cudaStreamEndCapture(st, &g));
     auto* e = new mgg_exec();
@@ -1116,33 +1126,51 @@ int mgg_rows_softmax(mgg_ctx* ctx, uint32_t part, const mgg_store* in, mgg_store
   });
 }
 
+// Barrier mode: 0 = events where possible (default), 1 = the K3 flag kernel
+// for every context with a flags store, also same-process parts (validation:
+// MGG_BARRIER=k3 exercises the cross-process kernel on a one-GPU box).
+static int barrier_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_BARRIER");
+    return e && std::string(e) == "k3" ? 1 : 0;
+  }();
+  return m;
+}
+
 int mgg_barrier(mgg_ctx* ctx, mgg_store* flags) {
   return guard([&] {
-    if (ctx->all_local && ctx->single_device) {
-      if (!ctx->part_streams) return;  // one stream per device: stream order suffices
-      // one stream per part: every part waits for every other part's work
-      for (uint32_t p = 0; p < ctx->num_parts; ++p)
-        MGG_CUDA(cudaEventRecord(ctx->bar_ev[p], ctx->stream[p]));
-      for (uint32_t p = 0; p < ctx->num_parts; ++p)
-        for (uint32_t q = 0; q < ctx->num_parts; ++q)
-          if (q != p) MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[q], 0));
-      return;
-    }
-    if (!flags) throw Status{MGG_E_INPUT, "barrier: flags store required"};
-    ++ctx->epoch;
-    if (ctx->all_local) {  // one process, several devices: host-side join
+    const bool k3 = !ctx->all_local || (barrier_mode() == 1 && flags && ctx->num_parts > 1);
+    if (!k3) {
+      // every part is driven by this process (one device or several): each
+      // part's stream waits for every other part's tail through events —
+      // cudaStreamWaitEvent orders streams across devices too, so there is
+      // no host round trip and the join is capturable into a CUDA graph
+      if (ctx->single_device && !ctx->part_streams) return;  // one stream: stream order
       for (uint32_t p = 0; p < ctx->num_parts; ++p) {
-        MGG_CUDA(cudaSetDevice(ctx->device[p]));
-        MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
+        enter(ctx, p);
+        MGG_CUDA(cudaEventRecord(ctx->bar_ev[p], ctx->stream[p]));
+      }
+      for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+        enter(ctx, p);
+        for (uint32_t q = 0; q < ctx->num_parts; ++q)
+          if (q != p && ctx->stream[q] != ctx->stream[p])
+            MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[q], 0));
       }
       return;
     }
+    // K3: some parts live in other processes — device-side flags over the
+    // peer-mapped flag store, release/acquire at system scope
+    if (!flags) throw Status{MGG_E_INPUT, "barrier: flags store required"};
+    if (flags->dim < ctx->num_parts + 1)
+      throw Status{MGG_E_INPUT, "barrier: flags store needs num_parts + 1 columns"};
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      if (flags->lb[p + 1] - flags->lb[p] != 1)
+        throw Status{MGG_E_INPUT, "barrier: flags store must hold one row per part"};
     for (uint32_t p = 0; p < ctx->num_parts; ++p) {
       if (ctx->device[p] < 0) continue;
       cudaStream_t st = enter(ctx, p);
       launch_barrier(reinterpret_cast<unsigned* const*>(const_cast<float**>(flags->dtable[p])),
-                     reinterpret_cast<unsigned*>(flags->shard[p]), p, ctx->num_parts,
-                     ctx->epoch, st);
+                     reinterpret_cast<unsigned*>(flags->shard[p]), p, ctx->num_parts, st);
       count_launch(ctx);
     }
   });

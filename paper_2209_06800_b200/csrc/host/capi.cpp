@@ -550,6 +550,12 @@ int mgg_engine_measure_multi_gpu(mgg_engine* e, uint32_t dim, uint32_t reps,
     }
   });
 }
+int mgg_engine_get_logits(mgg_engine* e, float* rows) {
+  return guard([&] {
+    if (!rows) throw mgg::InputError("get_logits: null output");
+    e->e->get_logits(rows);
+  });
+}
 int mgg_engine_set_shard_memory(mgg_engine* e, uint32_t part, int kind) {
   return guard([&] { e->e->set_shard_memory(part, kind); });
 }

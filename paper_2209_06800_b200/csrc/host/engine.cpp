@@ -45,7 +45,9 @@ Engine::Engine(const CsrGraph& g, std::uint32_t num_parts,
     ok(mgg_ctx_create(num_parts_, dev_.data(), &ctx_));
     std::vector<std::uint64_t> flag_lb(num_parts_ + 1);
     for (std::uint32_t p = 0; p <= num_parts_; ++p) flag_lb[p] = p;
-    ok(mgg_store_create(ctx_, flag_lb.data(), kMaxOwners, &flags_));
+    // K3 flags: one row per part, slot q = part q's arrival, slot num_parts =
+    // the part's own epoch counter
+    ok(mgg_store_create(ctx_, flag_lb.data(), kMaxOwners + 1, &flags_));
     build_row_scales();
     build_program();
     fuse_chains();
@@ -402,9 +404,10 @@ void Engine::set_input(const float* x) {
 }
 
 void Engine::forward() {
+  // every part in this process (one device or several): the forward replays
+  // as one CUDA graph — barriers are event joins across the parts' streams
   bool graphable = graphs_ && !profiling_;
-  for (std::uint32_t p = 0; p < num_parts_ && graphable; ++p)
-    graphable = dev_[p] >= 0 && dev_[p] == dev_[0];
+  for (std::uint32_t p = 0; p < num_parts_ && graphable; ++p) graphable = dev_[p] >= 0;
   if (!graphable) {
     forward_ops(false);
     return;
@@ -667,6 +670,43 @@ std::uint32_t Engine::get_hidden(std::uint32_t which, float* rows) {
     synchronize();
   }
   return dim;
+}
+
+std::uint32_t Engine::get_logits(float* rows) {
+  // the op that produced the output: a dense with the softmax epilogue, or a
+  // softmax pass over an aggregated store
+  int head = -1;
+  for (std::size_t i = 0; i < program_.size(); ++i)
+    if (program_[i].out == output_) head = static_cast<int>(i);
+  if (head < 0) throw InputError("engine: no output op");
+  Op op = program_[head];
+  std::uint32_t width = 0;
+  ok(mgg_store_info(stores_[output_], &width, nullptr));
+  if (!rows) return width;
+  for (auto d : dev_)
+    if (d < 0) throw InputError("engine: get_logits needs every part in this process");
+  mgg_store* lg = scratch(width, 1);
+  for (std::uint32_t p = 0; p < num_parts_; ++p) {
+    if (op.kind == OpKind::softmax) {  // logits = (row scale ·) the aggregated rows
+      ok(mgg_rows_init_rs(ctx_, p, stores_[op.in], lg, 1.f, 0, nullptr,
+                          op.rs ? rs_[op.rs][p] : nullptr));
+    } else if (op.kind == OpKind::dense) {  // the same K2 head, no softmax epilogue
+      mgg_dense_desc d{};
+      d.w = weights_[op.w][p];
+      d.bias = op.bias >= 0 ? weights_[op.bias][p] : nullptr;
+      d.pre_bias = op.pre_bias >= 0 ? weights_[op.pre_bias][p] : nullptr;
+      d.pre = op.pre;
+      d.act = op.act == 2 ? 0 : op.act;
+      d.out2_scale = 1.f;
+      d.row_scale = op.rs ? rs_[op.rs][p] : nullptr;
+      ok(mgg_dense(ctx_, p, stores_[op.in], &d, lg, nullptr));
+    } else {
+      throw InputError("engine: output op is not a dense or softmax");
+    }
+  }
+  ok(mgg_store_download(lg, rows, 0, g_.num_nodes, width));
+  synchronize();
+  return width;
 }
 
 mgg_store* Engine::scratch(std::uint32_t dim, int slot) {

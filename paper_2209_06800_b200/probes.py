@@ -63,3 +63,43 @@ def chase_ns(nbytes: int, device: int = 0, steps: int = 20000, seed: int = 0) ->
         return ns.value
     finally:
         ctx.close()
+
+
+def host_gather_gbps(rows: int, dim: int, n_idx: int, device: int = 0, reps: int = 3,
+                     seed: int = 0) -> float:
+    """gather_gbps with the table in pinned host memory read in place over
+    PCIe (MGG_MEM_HOST_MAPPED shards): the ceiling of a host-mapped "peer"."""
+    from .api import host_alloc
+    pitch = (dim + 3) // 4 * 4
+    rng = np.random.default_rng(seed)
+    table = host_alloc((rows, pitch))
+    table[:] = rng.uniform(-1, 1, (rows, pitch)).astype(np.float32)
+    ctx = _Ctx(device)
+    try:
+        idx = ctx.buf(rng.integers(0, rows, n_idx, dtype=np.uint32))
+        g = C.c_double()
+        check(lib.mgg_probe_gather(ctx.h, 0, table.ctypes.data, pitch, idx, n_idx, reps,
+                                   C.byref(g)))
+        return g.value
+    finally:
+        ctx.close()
+
+
+def host_chase_ns(nbytes: int, device: int = 0, steps: int = 2000, seed: int = 0) -> float:
+    """chase_ns over pinned host memory: the dependent-load latency of a
+    host-mapped "peer" row (one PCIe round trip per load)."""
+    from .api import host_alloc
+    n = max(nbytes // 128, 2)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n).astype(np.uint64)
+    nxt = host_alloc((n * 32,), np.uint32)
+    nxt[:] = 0
+    order = perm * 32
+    nxt[order] = np.roll(order, -1)
+    ctx = _Ctx(device)
+    try:
+        ns = C.c_double()
+        check(lib.mgg_probe_chase(ctx.h, 0, nxt.ctypes.data, steps, C.byref(ns)))
+        return ns.value
+    finally:
+        ctx.close()

@@ -68,3 +68,18 @@ def test_no_cpu_fallback_without_gpu(mgg):
     g = mgg.gen_synthetic(mgg.UNIFORM, 16, 2, 0)
     with pytest.raises(mgg.CudaError):
         mgg.Engine(g, 1, [0], mgg.make_gcn(4, 4, 2))
+
+
+def test_same_process_barrier_has_no_host_sync():
+    # the barrier between parts of one process (one device or
+    # several) is stream-ordered (events), never a host join
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2209_06800_b200", "csrc", "cuda", "runtime.cu")).read()
+    body = src[src.index("int mgg_barrier(mgg_ctx* ctx, mgg_store* flags) {"):]
+    body = body[:body.index("\nint ", 10)]
+    for bad in ("Synchronize", "cudaDeviceSynchronize", "cudaEventQuery"):
+        assert bad not in body, bad
+    assert "cudaStreamWaitEvent" in body
+    cap = src[src.index("int mgg_capture_begin("):]
+    cap = cap[:cap.index("\nint ", 10)]
+    assert "single_device" not in cap  # multi-device contexts capture too

@@ -706,3 +706,38 @@ def test_measure_multi_gpu_report(mgg, parts, fetch):
     if parts == 1:
         assert r["remote_bytes"] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("parts", [2, 4])
+def test_k3_barrier_forced_same_process(parts):
+    """MGG_BARRIER=k3: the cross-process flag kernel between logical parts of
+    one process, eager and replayed from a CUDA graph (the epoch advances on
+    the device, so every replay really synchronises), against the oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, oracle, paper_2209_06800_b200 as mgg
+g = mgg.gen_rmat(6000, 90000, seed=8)
+model = mgg.make_gcn(24, 16, 8)
+x = mgg.random_features(g.num_nodes, 24, seed=2)
+_, _, zr = oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+for fetch in ("fine", "halo"):
+    eng = mgg.Engine(g, {parts}, [0] * {parts}, model, ps=16, dist=2, wpb=4)
+    eng.set_remote_fetch(fetch)
+    eng.set_input(x)
+    for i in range(6):  # eager warm-up, capture, then graph replays
+        eng.forward()
+        if i % 2:
+            z = eng.get_output()
+            assert np.abs(z - zr).max() <= 1e-4, (fetch, i, np.abs(z - zr).max())
+    zz = np.zeros_like(zr)
+    eng.forward_host(x, zz)
+    assert np.abs(zz - zr).max() <= 1e-4
+    eng.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=600, env={**os.environ, "MGG_BARRIER": "k3"})
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

@@ -68,7 +68,8 @@ def run_one(args):
         hid = max(0.0, rem + loc - pipe)
         fp = mgg.build_flat_plan(g, 2, 0, args.ps, args.dist, args.wpb, args.dim)
         out.append({
-            "pair_form": os.environ.get("MGG_AGG_PAIR", "default"), "kernels": kern,
+            "pair_form": os.environ.get("MGG_AGG_PAIR", "default"),
+            "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"), "kernels": kern,
             "far": far, "nodes": args.nodes, "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
@@ -88,8 +89,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nodes", type=int, default=2_000_000)
     ap.add_argument("--avg", type=float, default=25.0)
-    ap.add_argument("--window", type=int, default=2000)
-    ap.add_argument("--far", default="0,0.002,0.005,0.01,0.02,0.05,0.2")
+    ap.add_argument("--window", type=int, default=64)
+    ap.add_argument("--far", default="0.0005,0.001,0.002,0.004,0.01,0.05")
     ap.add_argument("--dim", type=int, default=16)
     ap.add_argument("--ps", type=int, default=16)
     ap.add_argument("--dist", type=int, default=8)
@@ -97,7 +98,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--device-peer", dest="host", action="store_false",
                     help="keep part 1's shard in device memory (same-GPU peer)")
-    ap.add_argument("--forms", default="1,0,2", help="MGG_AGG_PAIR values, one process each")
+    ap.add_argument("--forms", default="1,0,2,2:16",
+                    help="MGG_AGG_PAIR[:MGG_AGG_PIPE_DEPTH] values, one process each")
+    ap.add_argument("--probe", action="store_true", help="host-mapped gather/latency probes")
     ap.add_argument("--out", default=None)
     ap.add_argument("--child", action="store_true")
     args = ap.parse_args()
@@ -105,11 +108,23 @@ def main():
         run_one(args)
         return
     rows = []
+    if args.probe:
+        from paper_2209_06800_b200 import probes
+        pr = {"probe": "host-mapped vs device, 16-float rows (64 B), 2M random rows",
+              "host_gather_gbps": round(probes.host_gather_gbps(1_000_000, 16, 2_000_000), 2),
+              "device_gather_gbps": round(probes.gather_gbps(1_000_000, 16, 2_000_000), 1),
+              "host_chase_ns": round(probes.host_chase_ns(64 << 20), 1),
+              "device_chase_ns": round(probes.chase_ns(1 << 30), 1)}
+        print(json.dumps(pr), flush=True)
+        rows.append(pr)
     for form in args.forms.split(","):
+        pair, _, depth = form.partition(":")
         cmd = [sys.executable, os.path.abspath(__file__), "--child"] + [
-            a for a in sys.argv[1:] if not a.startswith("--out") and a != args.out]
+            a for a in sys.argv[1:] if not a.startswith("--out") and a != args.out
+            and a != "--probe"]
         r = subprocess.run(cmd, capture_output=True, text=True,
-                           env={**os.environ, "MGG_AGG_PAIR": form})
+                           env={**os.environ, "MGG_AGG_PAIR": pair,
+                                "MGG_AGG_PIPE_DEPTH": depth or "8"})
         sys.stderr.write(r.stderr[-3000:])
         rows += [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
         for l in r.stdout.splitlines():
