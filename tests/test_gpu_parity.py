@@ -465,52 +465,91 @@ def test_gin_chain_widths(mgg, oracle_mod, hidden, eps):
         eng.close()
 
 
-@pytest.mark.parametrize("workload", ["reddit-gcn", "products-gin", "orkut-gcn"])
-def test_full_size_forward_matches_oracle(mgg, oracle_mod, workload):
-    """The bench workloads at BASELINE size (same generator, seeds, model, tuned
-    config, graph replay) against the fp64 oracle.
+_ORACLE_CACHE = {}
 
-    Parity bar (north_star): layer outputs within 1e-4 relative. Checked on the
-    logits (the last layer output before the softmax), rebuilt in fp64 from the
-    engine's last post-aggregation accumulator, per row relative to the row's
-    largest |logit|. The softmax probabilities themselves are compared against
-    the oracle with the fp32 floor as the tolerance: at this scale the logits
-    reach ~1e3, where one fp32 ulp is ~1e-4, so near-tied rows move by ~1e-3
-    under ANY fp32 evaluation — the fp32 oracle shows the same spread against
-    the fp64 one, and the engine must stay within 2x of it."""
+
+def _full_size_oracle(mgg, oracle_mod, workload):
+    """(graph, model, x, fp64 logits, fp64 softmax, fp32-oracle softmax), cached
+    per workload for the module (the CPU oracle is the slow part)."""
+    if workload not in _ORACLE_CACHE:
+        import bench
+        _ORACLE_CACHE.clear()
+        _, g, model, _ = bench.build(mgg, workload)
+        x = mgg.random_features(g.num_nodes, model.in_dim, seed=1)
+        if model.kind == 0:
+            _, lg, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+            _, _, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+        else:
+            lg, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
+            _, z32 = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+        _ORACLE_CACHE[workload] = (g, model, x, lg, zr, z32)
+    return _ORACLE_CACHE[workload]
+
+
+@pytest.mark.parametrize("workload,parts,fetch", [
+    ("config1", 2, "fine"), ("config1", 2, "halo"),            # BASELINE configs[0]
+    ("reddit-gcn", 1, "auto"),                                 # configs[1]
+    ("products-gcn", 1, "auto"), ("products-gcn", 4, "fine"),  # north_star shape
+    ("products-gcn", 4, "halo"),
+    ("products-gin", 1, "auto"),                               # configs[2]
+    ("orkut-gcn", 1, "auto")])                                 # configs[3]
+def test_full_size_forward_matches_oracle(mgg, oracle_mod, workload, parts, fetch):
+    """The BASELINE workloads at full size (same generator, seeds, model, tuned
+    config, graph replay; 1 or several logical parts, both remote-fetch modes)
+    against the fp64 oracle.
+
+    Parity bar (north_star): layer outputs within 1e-4 relative, checked on the
+    engine's own logits — its head K2 re-run without the softmax epilogue
+    (mgg_engine_get_logits) — per row relative to the row's largest |logit|.
+    The softmax probabilities are compared with the fp32 floor as the
+    tolerance: at this scale the logits reach ~1e3-1e9, where near-tied rows
+    move by ~1e-3 under ANY fp32 evaluation — the fp32 oracle shows the same
+    spread against the fp64 one, and the engine must stay within 2x of it."""
     import bench
-    _, g, model, _ = bench.build(mgg, workload)
+    g, model, x, lg, zr, z32 = _full_size_oracle(mgg, oracle_mod, workload)
     ps, dist, wpb = bench.WORKLOADS[workload][3][:3]
-    x = mgg.random_features(g.num_nodes, model.in_dim, seed=1)
-    eng = mgg.Engine(g, 1, [0], model, ps=ps, dist=dist, wpb=wpb)
+    eng = mgg.Engine(g, parts, [0] * parts, model, ps=ps, dist=dist, wpb=wpb)
     try:
+        eng.set_remote_fetch(fetch)
         eng.set_input(x)
         for _ in range(2):  # eager pass, then the captured graph
             eng.forward()
         z = eng.get_output()
-        a_last = eng.get_hidden(model.layers - 1).astype(np.float64)
+        logits = eng.get_logits()
     finally:
         eng.close()
-    if model.kind == 0:
-        d, h, c = model.in_dim, model.hidden, model.out_dim
-        w2 = model.w1[d * h: d * h + h * c].reshape(h, c).astype(np.float64)
-        logits = a_last @ w2
-        _, lg, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
-        _, _, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
-    else:
-        dims, h, c = model.gin_dims(), model.hidden, model.out_dim
-        b1 = model.b1[-h:].astype(np.float64)
-        w2 = model.w2[-h * c:].reshape(h, c).astype(np.float64)
-        b2 = model.b2[-c:].astype(np.float64)
-        logits = np.maximum(a_last + b1, 0) @ w2 + b2
-        lg, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
-        _, z32 = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
-    lerr = assert_rows_close(logits, lg.astype(np.float64), tol=TOL, what=f"{workload} logits")
+    lerr = assert_rows_close(logits, lg.astype(np.float64), tol=TOL,
+                             what=f"{workload} x{parts} {fetch} logits")
     floor = float(np.abs(z32 - zr).max())
     err = float(np.abs(z - zr).max())
-    print(f"\n{workload}: logits row-relative {lerr:.2e}, softmax {err:.2e} "
+    print(f"\n{workload} x{parts} {fetch}: logits row-relative {lerr:.2e}, softmax {err:.2e} "
           f"(fp32 oracle floor {floor:.2e}, max |logit| {np.abs(lg).max():.1f})")
     assert err <= max(TOL, 2 * floor), f"{workload}: softmax {err:.3e}, fp32 oracle floor {floor:.3e}"
+
+
+_CFG5 = {}
+
+
+@pytest.mark.parametrize("dim", [16, 64, 256])
+@pytest.mark.parametrize("fetch", ["fine", "halo"])
+def test_cfg5_aggregation_8_parts(mgg, oracle_mod, dim, fetch):
+    """BASELINE configs[4]: ogbn-proteins-shaped graph (132,534 nodes, 79M
+    edges target, reference powerlaw generator) aggregated at 8 logical parts
+    at D = 16 / 64 / 256 with the tuner's pick, against the fp64 oracle."""
+    if "g" not in _CFG5:
+        _CFG5["g"] = mgg.gen_synthetic(mgg.POWERLAW, 132_534, 79_000_000 / 132_534, 0)
+    g = _CFG5["g"]
+    x = mgg.random_features(g.num_nodes, dim, seed=dim)
+    ps, dist, wpb = {16: (32, 4, 1), 64: (32, 4, 4), 256: (32, 2, 16)}[dim]
+    eng = mgg.Engine(g, 8, [0] * 8, mgg.make_gcn(dim, 16, 8), ps=ps, dist=dist, wpb=wpb)
+    try:
+        eng.set_remote_fetch(fetch)
+        out = eng.aggregate(x, 1.0)
+    finally:
+        eng.close()
+    if ("ref", dim) not in _CFG5:
+        _CFG5[("ref", dim)] = oracle_mod.aggregate(g.row_ptr, g.col_idx, x)
+    assert_rows_close(out, _CFG5[("ref", dim)], what=f"cfg5 dim={dim} {fetch}")
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("MGG_FUZZ_N", "12"))))

@@ -212,3 +212,32 @@ def test_plan_json_roundtrip_shape(mgg):
     j = json.loads(fp.to_json())
     assert set(j) == {"cfg", "dim", "smemBytesPerBlock", "localParts", "remoteParts", "warps"}
     assert j["cfg"] == {"dist": 1, "ps": 2, "wpb": 2}
+
+
+@pytest.mark.parametrize("workload", ["reddit-gcn", "products-gcn", "orkut-gcn"])
+def test_plan_at_baseline_scale_8_parts(mgg, workload):
+    """BASELINE configs[1..3] graphs at full size, 8 parts, the bench's tuned
+    (ps, dist, wpb): every part's device plan expands to the reference's
+    KernelLaunchPlan — partitions, warp task lists, block tiling, smem
+    (R:proj/tests/acceptance.cpp:54-116 criteria, at scale)."""
+    import bench
+    _, g, model, _ = bench.build(mgg, workload)
+    ps, dist, wpb = bench.WORKLOADS[workload][3][:3]
+    dim = model.in_dim
+    r = RefGraph.from_csr(g.row_ptr, g.col_idx)
+    assert np.array_equal(mgg.split_by_edges(g, 8), r.split(8))
+    ranges = mgg.plan_ne_placement(g, 8, 1, dim).astype(np.uint64)
+    for gpu in range(8):
+        fp = mgg.build_flat_plan(g, 8, gpu, ps, dist, wpb, dim)
+        rp = r.plan(8, 1, gpu, ps, dist, wpb, dim)
+        a, b = _expand_flat(fp, ranges), _expand_ref(rp)
+        for kind in (0, 1):
+            for x, y in zip(a[kind], b[kind]):
+                assert np.array_equal(x, y), (workload, gpu, kind)
+        assert fp.num_warps == rp.n_warps and fp.num_blocks == rp.n_blocks
+        assert fp.smem_bytes_per_block == rp.smem
+        off, kind, idx = fp.tasks()
+        roff, _, rkind, ridx, bf, bc = rp.warps()
+        assert np.array_equal(off, roff)
+        assert np.array_equal(kind, rkind) and np.array_equal(idx, ridx)
+        del fp, rp, a, b
