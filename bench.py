@@ -593,6 +593,23 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
                    "overlap_of_shorter_phase": round(hidden / max(min(t_rem, t_loc), 1), 4),
                    "remote_fetch": "halo" if st.get("halo_rows", 0) else "fine"}
 
+    # peer (NVLink) bytes this rank's aggregations pull per step: fine = one
+    # row per remote edge, halo = each distinct remote row once per layer
+    link = None
+    if st["remote_parts"] > 0:
+        halo = st.get("halo_rows", 0) > 0
+        rows_pulled = st["halo_rows"] if halo else st["remote_edges"]
+        by = sum(rows_pulled * ((w + 3) // 4 * 4) * 4 for w in widths)
+        agg_ms = sum(t for k, _, t in ops if k == "aggregate") / max(nfw, 1)
+        link = {"remote_bytes_per_step": int(by), "mode": "halo" if halo else "fine",
+                "rows_per_layer": int(rows_pulled),
+                "achieved_gbs_over_k1_time": round(by / max(agg_ms, 1e-9) / 1e6, 1),
+                "peak_gbs": 900.0, "peak_source": "NVLink 5 per direction (north_star)",
+                "note": "logical parts on one GPU: the 'peer' is the same HBM"
+                        if world == 1 else "per rank; max over ranks of the time"}
+        if world > 1:
+            link["remote_bytes_per_step_all_ranks"] = int(mdist.sum_over_ranks(float(by)))
+
     e2e = None
     if full and not args.no_e2e:
         # two pinned input/output buffer pairs, alternated: every step copies
@@ -647,6 +664,7 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
         "roofline": roof,
         "ops": [{"kind": k, "width": w, "ms": round(t / nfw, 4)} for k, w, t in ops],
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "overlap": overlap,
+        "link": link,
         "clocks": clk.summary(),
         "setup": {"graph_gen_s": round(gen_s, 2), "engine_setup_s": round(setup_s, 2),
                   "plan_build_ms": round(st["plan_build_ns"] / 1e6, 1),
@@ -704,7 +722,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": m["config"], "roofline": m["roofline"], "ops": m["ops"],
             "cpu_baseline": m["cpu_baseline"], "e2e": m["e2e"],
-            "gpu_launches": m["gpu_launches"], "overlap": m["overlap"], "clocks": m["clocks"],
+            "gpu_launches": m["gpu_launches"], "overlap": m["overlap"], "link": m["link"],
+            "clocks": m["clocks"],
             "setup": m["setup"], "secondary": secondary,
         }
         print(json.dumps(line), flush=True)

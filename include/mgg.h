@@ -50,6 +50,8 @@ const char* mgg_last_error(void);
 const char* mgg_version(void);
 /* 1 if a CUDA device is visible, 0 otherwise (never fails). */
 int mgg_cuda_available(void);
+/* Number of visible CUDA devices (0 when none; never fails). */
+int mgg_device_count(void);
 /* Frees memory the library returned (JSON strings, CSV). */
 void mgg_free(void* p);
 

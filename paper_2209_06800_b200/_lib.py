@@ -171,6 +171,7 @@ _sig("mgg_engine_time_aggregate_each", I, vp, U32, U32, I, u64p)
 _sig("mgg_engine_measure_multi_gpu", I, vp, U32, U32, u64p, u64p, C.POINTER(C.c_double))
 _sig("mgg_engine_set_shard_memory", I, vp, U32, I)
 _sig("mgg_engine_get_logits", I, vp, C.POINTER(C.c_float))
+_sig("mgg_device_count", I)
 _sig("mgg_ctx_set_shard_memory", I, vp, U32, I)
 _sig("mgg_store_rehome", I, vp)
 _sig("mgg_dplan_k1_launch_info", I, vp, C.POINTER(C.c_uint32))

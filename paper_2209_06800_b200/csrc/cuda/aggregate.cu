@@ -89,6 +89,9 @@ struct AggArgs {
   uint32_t num_lblocks;       // logical CTAs = ceil(num_warps / wpb)
   uint32_t num_owners;
   int phase;                  // 0 all, 1 local only, 2 remote only
+  // pair kernels: logical CTAs dealt round-robin over the resident CTAs (1)
+  // instead of contiguous chunks (0)
+  uint32_t strided;
   const float* halo;          // deduplicated remote rows (halo mode) or null
   // device event trace (traced launches only): 16-B records
   // {globaltimer lo, hi, (smid << 8) | (stage << 1) | begin, logical warp}
@@ -199,6 +202,20 @@ __device__ __forceinline__ void cta_chunk(uint32_t total, uint32_t& b0, uint32_t
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
   b0 = min(blockIdx.x * per, total);
   b1 = min(b0 + per, total);
+}
+// Logical CTAs of this resident CTA as (first, end, step). Round-robin
+// (a.strided) is the reference's in-order block dispatch over the SMs
+// (R:proj/src/sim.cpp block dispatch): the interleaved mapping packs the
+// shorter kind's partitions into the FIRST logical warps (w·dist, ...), and
+// contiguous chunks would hand all of them to a few resident CTAs.
+struct LbRange {
+  uint32_t first, end, step;
+};
+__device__ __forceinline__ LbRange lb_range(const AggArgs& a) {
+  if (a.strided) return {blockIdx.x, a.num_lblocks, gridDim.x};
+  uint32_t b0, b1;
+  cta_chunk(a.num_lblocks, b0, b1);
+  return {b0, b1, 1u};
 }
 
 template <int VEC, bool RELU>
@@ -728,10 +745,9 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
                      __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
     return b + voff + static_cast<size_t>(c & kMask) * pb;
   };
-  uint32_t b0, b1;
-  cta_chunk(a.num_lblocks, b0, b1);
+  const LbRange rg = lb_range(a);
   const uint32_t wib = threadIdx.x >> 5;
-  for (uint32_t lb = b0; lb < b1; ++lb) {
+  for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
     const uint32_t w = lb * a.wpb + wib;
     if (w >= a.num_warps) break;
     uint32_t l0, l1, r0, r1;
@@ -849,17 +865,16 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
                      __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
     return b + voff + static_cast<size_t>(c & kMask) * pb;
   };
-  uint32_t b0, b1;
-  cta_chunk(a.num_lblocks, b0, b1);
+  const LbRange rg = lb_range(a);
   const uint32_t wib = threadIdx.x >> 5;
 
   // producer cursor over the group's remote rows in consumption order, kept
   // one row (column id in flight) and one partition (bounds in flight) ahead
   // so that issuing a copy never waits on a dependent metadata load
-  uint32_t plb = b0, pw = b0 * a.wpb + wib, pr0 = 0, pr1 = 0, pi = grp;
+  uint32_t plb = rg.first, pw = rg.first * a.wpb + wib, pr0 = 0, pr1 = 0, pi = grp;
   int pk = 0, pend = 0, qk = 0, qend = 0;
   uint32_t ncol = 0;
-  bool qvalid = false, pdone = b0 >= b1 || pw >= a.num_warps;
+  bool qvalid = false, pdone = rg.first >= rg.end || pw >= a.num_warps;
   if (!pdone) {
     uint32_t l0, l1;
     warp_groups(a, pw, l0, l1, pr0, pr1);
@@ -875,7 +890,9 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
         qvalid = true;
         return;
       }
-      if (++plb >= b1 || (pw += a.wpb) >= a.num_warps) {
+      plb += rg.step;
+      pw = plb * a.wpb + wib;
+      if (plb >= rg.end || pw >= a.num_warps) {
         pdone = true;
       } else {
         uint32_t l0, l1;
@@ -916,7 +933,7 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
 #pragma unroll 1
   for (int s = 0; s < R; ++s) produce();
 
-  for (uint32_t lb = b0; lb < b1; ++lb) {
+  for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
     const uint32_t w = lb * a.wpb + wib;
     if (w >= a.num_warps) break;
     uint32_t l0, l1, r0, r1;
@@ -1181,6 +1198,16 @@ int pair_mode() {
 // MGG_AGG_PAIR=0 keeps the warp-window pair loop (ablations, A/B).
 // Whole-list plans (granularity 1, the no_np ablation) keep the warp per
 // list of the paper's baseline.
+// Logical-CTA schedule of the pair kernels: 1 round-robin (default), 0
+// contiguous chunks (MGG_AGG_SCHED=0, A/B).
+int sched_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_SCHED");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+
 int pipe_depth() {
   static const int m = [] {
     const char* e = std::getenv("MGG_AGG_PIPE_DEPTH");  // ring slots per lane
@@ -1383,6 +1410,7 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const bool remote_lean = halo && phase == 2;
   const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
+  a.strided = remote && p->granularity == 0 && pair_mode() != 0 && sched_mode() != 0;
   KernelFn k = remote ? (relu_in ? pick_pair<true>(a.vec, p->granularity)
                                  : pick_pair<false>(a.vec, p->granularity))
                       : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity, p->k1_form)

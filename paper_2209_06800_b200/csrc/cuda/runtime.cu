@@ -178,6 +178,15 @@ int mgg_cuda_available(void) {
   return n > 0 ? 1 : 0;
 }
 
+int mgg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 int mgg_ctx_create(uint32_t num_parts, const int32_t* part_device, mgg_ctx** out) {
   return guard([&] {
     if (!out || !part_device) throw Status{MGG_E_INPUT, "ctx_create: null argument"};

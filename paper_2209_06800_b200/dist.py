@@ -45,6 +45,14 @@ def max_over_ranks(x: float, group=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(x: float, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())
+
+
 def rank_plan_summary(g, world: int, rank: int, ps: int, dist_: int, wpb: int, dim: int):
     """Host-side view of rank `rank`'s share (what its engine will upload)."""
     fp = api.build_flat_plan(g, world, rank, ps, dist_, wpb, dim)

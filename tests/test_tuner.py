@@ -178,3 +178,19 @@ def test_shipped_profiles_match_builtins(mgg):
         shipped = mgg.resolve_profile(os.path.join(d, name + ".json"))
         built = mgg.resolve_profile(name)
         assert shipped == built, name
+
+
+def test_refit_latencies_arithmetic():
+    # K5 numbers -> the reference LatencyModel schema (costmodel.hpp:32-49)
+    from paper_2209_06800_b200 import probes
+    m = {"local_chase_ns": 417.6, "local_gather_gbps": 6500.0}
+    f = probes.refit_latencies(m, 1.965, 148)
+    assert f["latencies"]["localLoadBase"] == 821
+    assert f["latencies"]["perElemLocal"] == 1
+    assert "remoteGetBase" not in f["latencies"]  # one GPU: keep the previous value
+    m.update(peer_chase_ns=1000.0, peer_gather_gbps=700.0)
+    f = probes.refit_latencies(m, 1.965, 148)
+    assert f["latencies"]["remoteGetBase"] == 1965
+    # 700 GB/s over 148 SMs = 2.41 B/cycle/SM -> 4 B take 1.66 cycles -> 2
+    assert f["latencies"]["perElemRemote"] == 2
+    assert "NVLink" in f["source"]["remoteGetBase"]
