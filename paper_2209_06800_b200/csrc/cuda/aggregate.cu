@@ -640,7 +640,10 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
 }
 // agg_group with L2 eviction hints: gathered rows evict-last (they are the
 // only reuse K1 has), column ids and accumulator reductions evict-first.
-template <int VEC, bool RELU, int UNR>
+// FETCH: L2 fetch size of the gathered-row misses — 0 the default (the line:
+// 64-B rows also bring their neighbour row in, ~1.3-1.5x DRAM bytes on
+// random tables that do not fit L2), 64 = `L2::64B` (only the row's sectors).
+template <int VEC, bool RELU, int UNR, int FETCH = 0>
 __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -654,9 +657,14 @@ __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
   auto load = [&](uint32_t c) {
     float4 x;
-    asm("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
-        : "l"(lbase + static_cast<size_t>(c) * pb), "l"(pol_last));
+    if (FETCH == 64)
+      asm("ld.global.cg.L2::64B.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+          : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+          : "l"(lbase + static_cast<size_t>(c) * pb), "l"(pol_last));
+    else
+      asm("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+          : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+          : "l"(lbase + static_cast<size_t>(c) * pb), "l"(pol_last));
     if (RELU) x = f4relu(x);
     return x;
   };
@@ -1056,13 +1064,30 @@ KernelFn pick_group(uint32_t v) {
   if (v <= 32) return agg_group<32, RELU, UNR>;
   return agg_wide<RELU>;
 }
-template <int VEC, bool RELU, int UNR>
+template <int VEC, bool RELU, int UNR, int FETCH>
 __global__ void __launch_bounds__(512, 2) agg_group_hint(AggArgs a) {
-  agg_group_hint_body<VEC, RELU, UNR>(a);
+  agg_group_hint_body<VEC, RELU, UNR, FETCH>(a);
+}
+int l2_fetch() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_L2FETCH");  // 0 default line fetch, 64 = L2::64B
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+int hint_unroll() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_HINT_UNR");  // rows in flight per group: 8 or 16
+    return e ? std::atoi(e) : 8;
+  }();
+  return m;
 }
 template <bool RELU>
 KernelFn pick_group_hint(uint32_t v) {
-  return v <= 4 ? agg_group_hint<4, RELU, 8> : agg_group_hint<16, RELU, 8>;
+  if (v > 4) return agg_group_hint<16, RELU, 8, 0>;
+  if (l2_fetch() == 64)
+    return hint_unroll() == 16 ? agg_group_hint<4, RELU, 16, 64> : agg_group_hint<4, RELU, 8, 64>;
+  return hint_unroll() == 16 ? agg_group_hint<4, RELU, 16, 0> : agg_group_hint<4, RELU, 8, 0>;
 }
 
 // The register budget is the occupancy knob of this latency-bound gather:

@@ -6,8 +6,14 @@ judged against (acceptance criterion 7's shape). Writes JSON to stdout.
 
     python tools/tune_b200.py --workload reddit-gcn [--parts N] [--exhaustive]
 
-After the tuner, a post-pass times the four local-only K1 forms at the pick
-(`Engine.set_k1_form`) and reports the fastest (`k1_form`).
+SimulateFn = what the run executes: with one part, the K1 of that part;
+with several, the measured MultiGpuReport's total (every part's K1
+concurrently + the barrier, Engine.measure_multi_gpu — the reference's
+multi_gpu_run aggregate, R:proj/src/sim.cpp:597-624, is the tuner's seam,
+R:proj/include/pipeshard/tuner.hpp:28-30). With --fold-forms the local-only
+K1 form is folded into every evaluation (SimulateFn(cfg) = the fastest of the
+four forms at cfg, so the search sees the form each (ps, dist, wpb) wants);
+otherwise a post-pass times the four forms at the pick (`k1_form`).
 """
 import argparse
 import json
@@ -28,31 +34,53 @@ def main():
     ap.add_argument("--parts", type=int, default=1)
     ap.add_argument("--exhaustive", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--fold-forms", action="store_true")
     args = ap.parse_args()
     label, g, model, _ = bench.build(mgg, args.workload)
     dim = bench.agg_widths(model)[0]
     eng = mgg.Engine(g, args.parts, [0] * args.parts, model, ps=1, dist=1, wpb=1)
     hw = mgg.resolve_profile("b200")
 
+    forms_at = {}
+
+    def one():
+        if args.parts > 1:
+            return eng.measure_multi_gpu(dim, args.reps)["total_ns"]
+        return eng.time_aggregate(dim, reps=args.reps)
+
     def measure(c):
         eng.set_config(*c)
-        return eng.time_aggregate(dim, reps=args.reps)
+        if not args.fold_forms or args.parts > 1:
+            return one()
+        per = {}
+        for f in (0, 1, 2, 3):
+            eng.set_k1_form(f)
+            per[f] = one()
+        eng.set_k1_form(0)
+        forms_at[tuple(c)] = per
+        return min(per.values())
 
     t0 = time.perf_counter()
     trace, best = mgg.optimize(measure, hw, dim)
     out = {"workload": args.workload, "label": label, "nodes": g.num_nodes,
            "edges": g.num_edges, "parts": args.parts, "dim": dim,
+           "simulate_fn": "measure_multi_gpu total_ns (concurrent parts + barrier)"
+                          if args.parts > 1 else "time_aggregate (K1 ns, median)",
+           "fold_forms": bool(args.fold_forms),
            "tuner": {"trace": trace, "best": best, "evaluations": len(trace),
                      "seconds": round(time.perf_counter() - t0, 2),
                      "speedup_vs_origin": round(trace[0][3] / best[3], 2)}}
     # post-pass (beyond the reference's tuner): the local-only K1 form at the
     # pick — by shape (0), warp-window (1), group x8 (2), group x4 (3)
     eng.set_config(*best[:3])
-    forms = {}
-    for f in (0, 1, 2, 3):
-        eng.set_k1_form(f)
-        forms[f] = eng.time_aggregate(dim, reps=args.reps)
-    eng.set_k1_form(0)
+    if args.fold_forms and tuple(best[:3]) in forms_at:
+        forms = forms_at[tuple(best[:3])]
+    else:
+        forms = {}
+        for f in (0, 1, 2, 3):
+            eng.set_k1_form(f)
+            forms[f] = one()
+        eng.set_k1_form(0)
     out["k1_form"] = {"ns": forms, "best": min(forms, key=forms.get)}
     if args.exhaustive:
         t0 = time.perf_counter()
