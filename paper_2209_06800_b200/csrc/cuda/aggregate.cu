@@ -999,13 +999,221 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
+// TMA form of agg_pipe (agg_pipe_bulk): the remote rows are fetched by the
+// bulk-copy engine — one `cp.async.bulk` of the whole row (pitch x 4 B) per
+// remote neighbour, issued by the group's first lane straight from the
+// owner's shard into a per-group ring of R row slots, completion counted in
+// bytes on the slot's mbarrier (north_star: "TMA from the mapped peer
+// address"). Remote requests then occupy the TMA unit's queue instead of the
+// SM's load/store request slots, which the local gathers keep to themselves.
+// Same cursor, order and one-row-per-consumed-row refill as agg_pipe; a
+// group syncs (__syncwarp on its lanes) before its leader refills a slot.
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+template <int VEC, bool RELU, int UNR, int R>
+__device__ __forceinline__ void agg_pipe_bulk_body(const AggArgs& a) {
+  constexpr int G = 32 / VEC;
+  extern __shared__ __align__(16) unsigned char pipe_raw[];
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / VEC, v = lane % VEC;
+  const bool vlane = v < static_cast<int>(a.vec);
+  const uint32_t voff = vlane ? 16u * v : 0u;
+  const uint32_t pb = a.pitch * 4u;
+  const bool leader = v == 0;
+  const unsigned gmask = (VEC == 32 ? 0xffffffffu : ((1u << VEC) - 1u)) << (grp * VEC);
+  const char* lbase = reinterpret_cast<const char*>(a.own) + voff;
+  asm("mov.b64 %0, %0;" : "+l"(lbase));
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t gid = wib * G + grp;  // group index in the CTA
+  const uint32_t ngroups = (blockDim.x >> 5) * G;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(pipe_raw));
+  const uint32_t slots = sbase + gid * R * pb;                  // R row slots
+  const uint32_t bars = sbase + ngroups * R * pb + gid * R * 8;  // R mbarriers
+  if (leader) {
+#pragma unroll 1
+    for (int r = 0; r < R; ++r)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * r) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto ld = [&](const char* p) {
+    float4 x;
+    asm(MGG_LD_INSN " {%0,%1,%2,%3}, [%4];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(p));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  auto rrow = [&](uint32_t c) {  // the whole remote row (bulk source)
+    const char* b =
+        a.halo ? reinterpret_cast<const char*>(a.halo)
+               : reinterpret_cast<const char*>(
+                     __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
+    return b + static_cast<size_t>(c & kMask) * pb;
+  };
+  const LbRange rg = lb_range(a);
+
+  // producer cursor (the leader's; the same as agg_pipe's)
+  uint32_t plb = rg.first, pw = rg.first * a.wpb + wib, pr0 = 0, pr1 = 0, pi = grp;
+  int pk = 0, pend = 0, qk = 0, qend = 0;
+  uint32_t ncol = 0;
+  bool qvalid = false, pdone = !leader || rg.first >= rg.end || pw >= a.num_warps;
+  if (!pdone) {
+    uint32_t l0, l1;
+    warp_groups(a, pw, l0, l1, pr0, pr1);
+  }
+  auto queue_next = [&]() {
+    qvalid = false;
+    while (!pdone) {
+      if (pr0 + pi < pr1) {
+        qk = __ldg(&a.rmeta[pr0 + pi].y);
+        qend = __ldg(&a.rmeta[pr0 + pi + 1].y);
+        pi += G;
+        qvalid = true;
+        return;
+      }
+      plb += rg.step;
+      pw = plb * a.wpb + wib;
+      if (plb >= rg.end || pw >= a.num_warps) {
+        pdone = true;
+      } else {
+        uint32_t l0, l1;
+        warp_groups(a, pw, l0, l1, pr0, pr1);
+        pi = grp;
+      }
+    }
+  };
+  auto advance = [&]() {
+    while (qvalid) {
+      pk = qk;
+      pend = qend;
+      queue_next();
+      if (pk < pend) {
+        ncol = __ldg(a.rcols + pk);
+        return;
+      }
+    }
+  };
+  if (leader) {
+    queue_next();
+    advance();
+  }
+  uint32_t issued = 0, consumed = 0;
+  auto produce = [&]() {  // leader only
+    if (pk < pend) {
+      const uint32_t c = ncol;
+      if (++pk < pend)
+        ncol = __ldg(a.rcols + pk);
+      else
+        advance();
+      const uint32_t slot = issued & (R - 1);
+      const uint32_t bar = bars + 8 * slot;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(slots + slot * pb),
+          "l"(rrow(c)), "r"(pb), "r"(bar)
+          : "memory");
+    }
+    ++issued;
+  };
+  if (leader) {
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) produce();
+  }
+
+  for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    uint32_t l0, l1, r0, r1;
+    warp_groups(a, w, l0, l1, r0, r1);
+    const uint32_t nl = l1 - l0, nr = r1 - r0, n = max(nl, nr);
+    for (uint32_t i = grp; i < n; i += G) {
+      if (i < nl) {  // reduce L_i from registers while R_i is in flight
+        const int2 m = __ldg(a.lmeta + l0 + i);
+        const int end = __ldg(&a.lmeta[l0 + i + 1].y);
+        float4 acc = f4zero();
+        int k = m.y;
+        for (; k + UNR <= end; k += UNR) {
+          uint32_t c[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) t[u] = ld(lbase + static_cast<size_t>(c[u]) * pb);
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (k < end) {
+          float4 t[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+            t[u] = k + u < end ? ld(lbase + static_cast<size_t>(__ldg(a.lcols + k + u)) * pb)
+                               : f4zero();
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
+        }
+        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+      }
+      if (i < nr) {  // consume R_i from the ring
+        const int2 m = __ldg(a.rmeta + r0 + i);
+        const int end = __ldg(&a.rmeta[r0 + i + 1].y);
+        float4 acc = f4zero();
+        for (int k = m.y; k < end; ++k) {
+          const uint32_t slot = consumed & (R - 1);
+          const uint32_t parity = (consumed / R) & 1u;
+          if (!mbar_try(bars + 8 * slot, parity)) {
+            uint64_t t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (!mbar_try(bars + 8 * slot, parity)) {
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+              if (t - t0 > 4000000000ull) __trap();  // a copy that never lands
+            }
+          }
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                       : "r"(slots + slot * pb + voff)
+                       : "memory");
+          ++consumed;
+          if (RELU) x = f4relu(x);
+          acc = f4add(acc, x);
+          __syncwarp(gmask);  // every lane of the group has read the slot
+          if (leader) produce();
+        }
+        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+      }
+    }
+  }
+  // drain: wait for copies issued past the last consumed row (none are
+  // issued beyond the stream, so every issued copy was consumed)
+}
+template <int VEC, bool RELU, int UNR, int R>
+__global__ void __launch_bounds__(512, 2) agg_pipe_bulk(AggArgs a) {
+  agg_pipe_bulk_body<VEC, RELU, UNR, R>(a);
+}
+
 template <int VEC, bool RELU, int UNR, int R>
 __global__ void __launch_bounds__(512, 2) agg_pipe(AggArgs a) {
   agg_pipe_body<VEC, RELU, UNR, R>(a);
 }
-// dynamic shared memory of the pipe kernels: R 16-B slots per thread
-std::map<const void*, uint32_t>& pipe_slots() {
-  static std::map<const void*, uint32_t> m;
+// dynamic shared memory of the pipe kernels: agg_pipe R 16-B slots per
+// thread; agg_pipe_bulk R row slots + R mbarriers per lane group
+struct PipeSmem {
+  uint32_t r, vec, bulk;
+};
+std::map<const void*, PipeSmem>& pipe_slots() {
+  static std::map<const void*, PipeSmem> m;
   return m;
 }
 template <bool RELU, int R>
@@ -1020,15 +1228,36 @@ KernelFn pick_pipe(uint32_t v) {
   if (v <= 32) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
-    pipe_slots()[reinterpret_cast<const void*>(k)] = R;
+    pipe_slots()[reinterpret_cast<const void*>(k)] = {R, 0, 0};
   }
   return k;
 }
-uint32_t dyn_smem(KernelFn k, int threads) {
+template <bool RELU, int R>
+KernelFn pick_pipe_bulk(uint32_t v) {
+  KernelFn k = v <= 1    ? agg_pipe_bulk<1, RELU, 4, R>
+               : v <= 2  ? agg_pipe_bulk<2, RELU, 4, R>
+               : v <= 4  ? agg_pipe_bulk<4, RELU, 4, R>
+               : v <= 8  ? agg_pipe_bulk<8, RELU, 4, R>
+               : v <= 16 ? agg_pipe_bulk<16, RELU, 4, R>
+               : v <= 32 ? agg_pipe_bulk<32, RELU, 4, R>
+                         : agg_wide<RELU>;
+  const uint32_t vec = v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : v <= 8 ? 8 : v <= 16 ? 16 : 32;
+  if (v <= 32) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    pipe_slots()[reinterpret_cast<const void*>(k)] = {R, vec, 1};
+  }
+  return k;
+}
+uint32_t dyn_smem(KernelFn k, int threads, uint32_t pitch) {
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
   auto it = pipe_slots().find(reinterpret_cast<const void*>(k));
-  return it == pipe_slots().end() ? 0u : it->second * 16u * static_cast<uint32_t>(threads);
+  if (it == pipe_slots().end()) return 0u;
+  const PipeSmem& p = it->second;
+  if (!p.bulk) return p.r * 16u * static_cast<uint32_t>(threads);
+  const uint32_t groups = static_cast<uint32_t>(threads) / 32u * (32u / p.vec);
+  return groups * p.r * (pitch * 4u + 8u);
 }
 
 template <int VEC, int PF>
@@ -1251,6 +1480,13 @@ KernelFn pick_pair(uint32_t v, uint32_t granularity) {
       default: return pick_pipe<RELU, 8>(v);
     }
   }
+  if (pair_mode() == 3) {  // TMA bulk-copy ring
+    switch (pipe_depth()) {
+      case 4: return pick_pipe_bulk<RELU, 4>(v);
+      case 16: return pick_pipe_bulk<RELU, 16>(v);
+      default: return pick_pipe_bulk<RELU, 8>(v);
+    }
+  }
   return pick_gpair<RELU, 4, 4>(v);
 }
 
@@ -1280,17 +1516,18 @@ const std::string& kernel_name(const void* fn) {
 }
 
 // Resident CTAs per SM for (kernel, CTA size), cached per device.
-unsigned resident_grid(KernelFn k, int threads) {
+unsigned resident_grid(KernelFn k, int threads, uint32_t pitch) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, unsigned> cache;
   int dev = 0;
   MGG_CUDA(cudaGetDevice(&dev));
-  const auto key = std::make_pair(reinterpret_cast<const void*>(k), threads * 64 + dev);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(k),
+                                  (static_cast<int>(pitch) * 1024 + threads) * 64 + dev);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int per_sm = 0, sms = 0;
-  const uint32_t smem = dyn_smem(k, threads);
+  const uint32_t smem = dyn_smem(k, threads, pitch);
   if (smem > 48 * 1024)
     MGG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
@@ -1451,9 +1688,9 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
     a.trace_warps = trace->warp_limit;
   }
   const int threads = 32 * static_cast<int>(p->wpb);
-  const unsigned full = resident_grid(k, threads);
+  const unsigned full = resident_grid(k, threads, a.pitch);
   const unsigned grid = std::min<unsigned>(full, a.num_lblocks);
-  k<<<grid, threads, dyn_smem(k, threads), st>>>(a);
+  k<<<grid, threads, dyn_smem(k, threads, a.pitch), st>>>(a);
   {
     int dev = 0, sms = 0;
     MGG_CUDA(cudaGetDevice(&dev));

@@ -626,7 +626,9 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
 
 @pytest.mark.parametrize("pair,depth,kernel", [("1", "8", "agg_gpair"), ("0", "8", "agg_kernel"),
                                                ("2", "8", "agg_pipe"), ("2", "4", "agg_pipe"),
-                                               ("2", "16", "agg_pipe")])
+                                               ("2", "16", "agg_pipe"),
+                                               ("3", "8", "agg_pipe_bulk"),
+                                               ("3", "4", "agg_pipe_bulk")])
 def test_pair_kernel_forms(pair, depth, kernel):
     # the fine-fetch pair loop: agg_gpair (default) and the warp-window loop
     # (MGG_AGG_PAIR=0, read once per process) on single-process multi-part

@@ -69,7 +69,8 @@ def run_one(args):
         fp = mgg.build_flat_plan(g, 2, 0, args.ps, args.dist, args.wpb, args.dim)
         out.append({
             "pair_form": os.environ.get("MGG_AGG_PAIR", "default"),
-            "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"), "kernels": kern,
+            "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"),
+            "sched": os.environ.get("MGG_AGG_SCHED", "1"), "kernels": kern,
             "far": far, "nodes": args.nodes, "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
@@ -98,7 +99,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--device-peer", dest="host", action="store_false",
                     help="keep part 1's shard in device memory (same-GPU peer)")
-    ap.add_argument("--forms", default="1,0,2,2:16",
+    ap.add_argument("--forms", default="1,2,3,3:16",
                     help="MGG_AGG_PAIR[:MGG_AGG_PIPE_DEPTH] values, one process each")
     ap.add_argument("--probe", action="store_true", help="host-mapped gather/latency probes")
     ap.add_argument("--out", default=None)
@@ -118,13 +119,15 @@ def main():
         print(json.dumps(pr), flush=True)
         rows.append(pr)
     for form in args.forms.split(","):
-        pair, _, depth = form.partition(":")
+        pair, _, rest = form.partition(":")
+        depth, _, sched = rest.partition(":")
         cmd = [sys.executable, os.path.abspath(__file__), "--child"] + [
             a for a in sys.argv[1:] if not a.startswith("--out") and a != args.out
             and a != "--probe"]
         r = subprocess.run(cmd, capture_output=True, text=True,
                            env={**os.environ, "MGG_AGG_PAIR": pair,
-                                "MGG_AGG_PIPE_DEPTH": depth or "8"})
+                                "MGG_AGG_PIPE_DEPTH": depth or "8",
+                                "MGG_AGG_SCHED": sched or "1"})
         sys.stderr.write(r.stderr[-3000:])
         rows += [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
         for l in r.stdout.splitlines():
