@@ -527,8 +527,10 @@ int mgg_engine_time_aggregate_each(mgg_engine* e, uint32_t dim, uint32_t reps, i
                                    uint64_t* ns);
 /* Measured MultiGpuReport (R:proj/include/pipeshard/sim.hpp:115-123,
  * multi_gpu_run R:proj/src/sim.cpp:597-624): every local part's K1 at width
- * `dim` run concurrently, median of `reps`. summary[4] = {max_gpu_ns,
- * barrier_ns, total_ns (max + barrier), remote_bytes}; per_part[num_parts x 9]
+ * `dim` run concurrently, median of `reps`. summary[6] = {max_gpu_ns,
+ * barrier_ns, total_ns (max + barrier), remote_bytes, max_alone_ns (max over
+ * parts of each part's K1 with the device to itself: the per-GPU time when
+ * logical parts share a device), devices}; per_part[num_parts x 9]
  * = {local (1/0), total_ns (concurrent), alone_ns, remote_bytes, local_bytes,
  * num_warps, num_blocks, active_sms, part}; per_part_f[num_parts x 2] =
  * {achieved_occupancy (occupancy calculator x grid), sm_utilization (SMs

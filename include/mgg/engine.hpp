@@ -131,6 +131,11 @@ class Engine {
     std::vector<PartReport> per_gpu;
     std::uint64_t max_gpu_ns = 0, barrier_ns = 0, total_ns = 0, remote_bytes = 0;
     double mean_occupancy = 0, mean_utilization = 0;
+    /// max over parts of alone_ns: the per-GPU time when logical parts share
+    /// one device (their concurrent run measures contention a multi-GPU
+    /// system does not have); equals ~max_gpu_ns with one part per device
+    std::uint64_t max_alone_ns = 0;
+    std::uint32_t devices = 0;  // distinct devices of the local parts
   };
   MultiGpuReport measure_multi_gpu(std::uint32_t dim, std::uint32_t reps);
 

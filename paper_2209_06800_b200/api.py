@@ -516,7 +516,7 @@ class Engine:
         """Measured MultiGpuReport (R:proj/include/pipeshard/sim.hpp:115-123):
         every local part's K1 concurrently; see mgg_engine_measure_multi_gpu."""
         n = self.num_parts
-        summ = np.zeros(4, np.uint64)
+        summ = np.zeros(6, np.uint64)
         pp = np.zeros(9 * n, np.uint64)
         pf = np.zeros(2 * n, np.float64)
         check(lib.mgg_engine_measure_multi_gpu(self._h, dim, reps, _p(summ, C.c_uint64),
@@ -534,6 +534,11 @@ class Engine:
             per.append(row)
         return {"per_gpu": per, "max_gpu_ns": int(summ[0]), "barrier_ns": int(summ[1]),
                 "total_ns": int(summ[2]), "remote_bytes": int(summ[3]),
+                "max_alone_ns": int(summ[4]), "devices": int(summ[5]),
+                # the per-GPU time: logical parts sharing one device are timed
+                # alone (their concurrent run is contention no 8-GPU box has)
+                "per_gpu_ns": int(summ[4]) if int(summ[5]) == 1 and len(per) > 1
+                else int(summ[2]),
                 "mean_occupancy": float(np.mean([r["achieved_occupancy"] for r in per])),
                 "mean_utilization": float(np.mean([r["sm_utilization"] for r in per]))}
 

@@ -531,6 +531,8 @@ int mgg_engine_measure_multi_gpu(mgg_engine* e, uint32_t dim, uint32_t reps,
     summary[1] = r.barrier_ns;
     summary[2] = r.total_ns;
     summary[3] = r.remote_bytes;
+    summary[4] = r.max_alone_ns;
+    summary[5] = r.devices;
     const uint32_t n = e->e->num_parts();
     std::memset(per_part, 0, sizeof(uint64_t) * 9 * n);
     std::memset(per_part_f, 0, sizeof(double) * 2 * n);

@@ -839,6 +839,7 @@ Engine::MultiGpuReport Engine::measure_multi_gpu(std::uint32_t dim, std::uint32_
     pr.num_warps = static_cast<std::uint32_t>(fp.num_warps());
     pr.num_blocks = static_cast<std::uint32_t>(fp.num_blocks());
     rep.max_gpu_ns = std::max(rep.max_gpu_ns, pr.total_ns);
+    rep.max_alone_ns = std::max(rep.max_alone_ns, pr.alone_ns);
     until = std::max(until, median(upto[p]));
     rep.remote_bytes += pr.remote_bytes;
     rep.mean_occupancy += pr.achieved_occupancy / local.size();
@@ -847,6 +848,10 @@ Engine::MultiGpuReport Engine::measure_multi_gpu(std::uint32_t dim, std::uint32_
   }
   rep.total_ns = std::max(until, rep.max_gpu_ns);
   rep.barrier_ns = rep.total_ns - rep.max_gpu_ns;
+  std::vector<std::int32_t> devs;
+  for (auto p : local)
+    if (std::find(devs.begin(), devs.end(), dev_[p]) == devs.end()) devs.push_back(dev_[p]);
+  rep.devices = static_cast<std::uint32_t>(devs.size());
   return rep;
 }
 

@@ -744,6 +744,9 @@ def test_measure_multi_gpu_report(mgg, parts, fetch):
         assert p["alone_ns"] > 0 and p["total_ns"] > 0
         assert 0 < p["achieved_occupancy"] <= 1 and 0 < p["sm_utilization"] <= 1
         assert p["num_blocks"] == fp.num_blocks and p["num_warps"] == fp.num_warps
+    assert r["devices"] == 1
+    assert r["max_alone_ns"] == max(p["alone_ns"] for p in r["per_gpu"])
+    assert r["per_gpu_ns"] == (r["max_alone_ns"] if parts > 1 else r["total_ns"])
     if parts == 1:
         assert r["remote_bytes"] == 0
     eng.close()

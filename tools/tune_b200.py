@@ -7,8 +7,11 @@ judged against (acceptance criterion 7's shape). Writes JSON to stdout.
     python tools/tune_b200.py --workload reddit-gcn [--parts N] [--exhaustive]
 
 SimulateFn = what the run executes: with one part, the K1 of that part;
-with several, the measured MultiGpuReport's total (every part's K1
-concurrently + the barrier, Engine.measure_multi_gpu — the reference's
+with several, the measured MultiGpuReport (Engine.measure_multi_gpu):
+`per_gpu_ns` = the concurrent max + barrier when the parts own their devices,
+the max over parts of each part's K1 alone when logical parts share one
+device (their concurrent run is contention a multi-GPU box does not have) —
+the reference's
 multi_gpu_run aggregate, R:proj/src/sim.cpp:597-624, is the tuner's seam,
 R:proj/include/pipeshard/tuner.hpp:28-30). With --fold-forms the local-only
 K1 form is folded into every evaluation (SimulateFn(cfg) = the fastest of the
@@ -45,7 +48,7 @@ def main():
 
     def one():
         if args.parts > 1:
-            return eng.measure_multi_gpu(dim, args.reps)["total_ns"]
+            return eng.measure_multi_gpu(dim, args.reps)["per_gpu_ns"]
         return eng.time_aggregate(dim, reps=args.reps)
 
     def measure(c):
@@ -64,7 +67,8 @@ def main():
     trace, best = mgg.optimize(measure, hw, dim)
     out = {"workload": args.workload, "label": label, "nodes": g.num_nodes,
            "edges": g.num_edges, "parts": args.parts, "dim": dim,
-           "simulate_fn": "measure_multi_gpu total_ns (concurrent parts + barrier)"
+           "simulate_fn": "measure_multi_gpu per_gpu_ns (one device: max over parts "
+                          "alone; several: concurrent max + barrier)"
                           if args.parts > 1 else "time_aggregate (K1 ns, median)",
            "fold_forms": bool(args.fold_forms),
            "tuner": {"trace": trace, "best": best, "evaluations": len(trace),
