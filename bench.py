@@ -580,8 +580,10 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
     # (compute) and both pipelined in one launch; max over parts
     overlap = None
     if full and st["remote_parts"] > 0:
+        fine = not st.get("halo_rows", 0)
         t_pipe = eng.time_aggregate(w0, 5, 0)
-        t_loc = eng.time_aggregate(w0, 5, 1)
+        # fine fetch: the local leg of the pipelined kernel itself (phase 3)
+        t_loc = eng.time_aggregate(w0, 5, 3 if fine else 1)
         t_rem = eng.time_aggregate(w0, 5, 2)
         if world > 1:
             t_pipe, t_loc, t_rem = (mdist.max_over_ranks(float(t)) for t in

@@ -192,7 +192,9 @@ int mgg_dplan_destroy(mgg_dplan* p);
 typedef struct {
   int relu_in;
   int phase; /* 0 all, 1 local partitions only, 2 remote only (phase-split
-                measurement, R:proj/src/sim.cpp:127-142) */
+                measurement, R:proj/src/sim.cpp:127-142); 3 = local only
+                through the fine-fetch pair kernel itself (its own local
+                leg: T_pipe vs T_local + T_remote of one kernel) */
   const float* halo; /* non-NULL: remote partitions read this part's halo
                         buffer instead of peers (local pass, then remote pass) */
   int halo_pull;     /* with halo: refill it first (mgg_halo_pull) on the

@@ -873,6 +873,27 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
                      __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
     return b + voff + static_cast<size_t>(c & kMask) * pb;
   };
+  uint64_t pol_last, pol_first;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  auto ldh = [&](const char* p) {
+    float4 x;
+    asm("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(p), "l"(pol_last));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  auto ldcol = [&](const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol_first));
+    return r;
+  };
+  auto redh = [&](float* p, float4 v4) {
+    asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p),
+                 "f"(v4.x), "f"(v4.y), "f"(v4.z), "f"(v4.w), "l"(pol_first)
+                 : "memory");
+  };
   const LbRange rg = lb_range(a);
   const uint32_t wib = threadIdx.x >> 5;
 
@@ -949,19 +970,27 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
     const uint32_t nl = l1 - l0, nr = r1 - r0, n = max(nl, nr);
     for (uint32_t i = grp; i < n; i += G) {
       // (1) R_i is already in flight (issued up to R rows ago)
-      // (2) reduce L_i from registers
+      // (2) reduce L_i from registers: the lean group kernel's gather (UNR
+      // rows in flight, the next UNR column ids prefetched, gathered rows
+      // evict-last / column ids and reductions evict-first in L2)
       if (i < nl) {
         const int2 m = __ldg(a.lmeta + l0 + i);
         const int end = __ldg(&a.lmeta[l0 + i + 1].y);
         float4 acc = f4zero();
         int k = m.y;
-        for (; k + UNR <= end; k += UNR) {
-          uint32_t c[UNR];
+        uint32_t c[UNR];
+        if (k + UNR <= end) {
 #pragma unroll
-          for (int u = 0; u < UNR; ++u) c[u] = __ldg(a.lcols + k + u);
+          for (int u = 0; u < UNR; ++u) c[u] = ldcol(a.lcols + k + u);
+        }
+        for (; k + UNR <= end; k += UNR) {
           float4 t[UNR];
 #pragma unroll
-          for (int u = 0; u < UNR; ++u) t[u] = ld(lbase + static_cast<size_t>(c[u]) * pb);
+          for (int u = 0; u < UNR; ++u) t[u] = ldh(lbase + static_cast<size_t>(c[u]) * pb);
+          if (k + 2 * UNR <= end) {
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) c[u] = ldcol(a.lcols + k + UNR + u);
+          }
 #pragma unroll
           for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
         }
@@ -969,12 +998,12 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
           float4 t[UNR];
 #pragma unroll
           for (int u = 0; u < UNR; ++u)
-            t[u] = k + u < end ? ld(lbase + static_cast<size_t>(__ldg(a.lcols + k + u)) * pb)
+            t[u] = k + u < end ? ldh(lbase + static_cast<size_t>(ldcol(a.lcols + k + u)) * pb)
                                : f4zero();
 #pragma unroll
           for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
         }
-        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+        if (vlane) redh(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
       // (3) consume R_i from the ring; every row consumed issues the next
       if (i < nr) {
@@ -1066,7 +1095,7 @@ __device__ __forceinline__ void agg_pipe_bulk_body(const AggArgs& a) {
   uint32_t plb = rg.first, pw = rg.first * a.wpb + wib, pr0 = 0, pr1 = 0, pi = grp;
   int pk = 0, pend = 0, qk = 0, qend = 0;
   uint32_t ncol = 0;
-  bool qvalid = false, pdone = !leader || rg.first >= rg.end || pw >= a.num_warps;
+  bool qvalid = false, pdone = rg.first >= rg.end || pw >= a.num_warps;
   if (!pdone) {
     uint32_t l0, l1;
     warp_groups(a, pw, l0, l1, pr0, pr1);
@@ -1103,34 +1132,34 @@ __device__ __forceinline__ void agg_pipe_bulk_body(const AggArgs& a) {
       }
     }
   };
-  if (leader) {
-    queue_next();
-    advance();
-  }
+  queue_next();  // every lane walks the cursor (no divergent scans) ...
+  advance();
   uint32_t issued = 0, consumed = 0;
-  auto produce = [&]() {  // leader only
+  auto produce = [&]() {  // ... and the group's leader issues the copy
     if (pk < pend) {
       const uint32_t c = ncol;
       if (++pk < pend)
         ncol = __ldg(a.rcols + pk);
       else
         advance();
-      const uint32_t slot = issued & (R - 1);
-      const uint32_t bar = bars + 8 * slot;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-              "r"(slots + slot * pb),
-          "l"(rrow(c)), "r"(pb), "r"(bar)
-          : "memory");
+      if (leader) {
+        const uint32_t slot = issued & (R - 1);
+        const uint32_t bar = bars + 8 * slot;
+        // the group's generic reads of this slot before the async-proxy write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(slots + slot * pb),
+            "l"(rrow(c)), "r"(pb), "r"(bar)
+            : "memory");
+      }
     }
     ++issued;
   };
-  if (leader) {
 #pragma unroll 1
-    for (int r = 0; r < R; ++r) produce();
-  }
+  for (int r = 0; r < R; ++r) produce();
 
   for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
     const uint32_t w = lb * a.wpb + wib;
@@ -1189,7 +1218,7 @@ __device__ __forceinline__ void agg_pipe_bulk_body(const AggArgs& a) {
           if (RELU) x = f4relu(x);
           acc = f4add(acc, x);
           __syncwarp(gmask);  // every lane of the group has read the slot
-          if (leader) produce();
+          produce();
         }
         if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
@@ -1218,12 +1247,12 @@ std::map<const void*, PipeSmem>& pipe_slots() {
 }
 template <bool RELU, int R>
 KernelFn pick_pipe(uint32_t v) {
-  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 4, R>
-               : v <= 2  ? agg_pipe<2, RELU, 4, R>
-               : v <= 4  ? agg_pipe<4, RELU, 4, R>
-               : v <= 8  ? agg_pipe<8, RELU, 4, R>
-               : v <= 16 ? agg_pipe<16, RELU, 4, R>
-               : v <= 32 ? agg_pipe<32, RELU, 4, R>
+  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 8, R>
+               : v <= 2  ? agg_pipe<2, RELU, 8, R>
+               : v <= 4  ? agg_pipe<4, RELU, 8, R>
+               : v <= 8  ? agg_pipe<8, RELU, 8, R>
+               : v <= 16 ? agg_pipe<16, RELU, 8, R>
+               : v <= 32 ? agg_pipe<32, RELU, 8, R>
                          : agg_wide<RELU>;
   if (v <= 32) {
     static std::mutex mu;
@@ -1668,7 +1697,11 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   if (warps > 0xffffffffull) throw Status{MGG_E_CONFIG, "aggregate: too many warps"};
   a.num_warps = static_cast<uint32_t>(warps);
   a.num_lblocks = (a.num_warps + a.wpb - 1) / a.wpb;
-  const bool remote = a.nR > 0 && a.phase != 1;
+  // phase 3 (fine fetch, timing decomposition): the local partitions only,
+  // through the pipelined pair kernel itself — its own local leg, so that
+  // T_pipe vs T_local + T_remote compares one kernel with itself
+  if (phase == 3) a.phase = 1;
+  const bool remote = a.nR > 0 && (a.phase != 1 || (phase == 3 && !halo));
   const bool remote_lean = halo && phase == 2;
   const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;

@@ -146,7 +146,7 @@ void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg
   }
   if (!plan->rcols_halo) throw Status{MGG_E_INPUT, "aggregate: plan has no halo"};
   const uint32_t p = plan->part;
-  const bool pull = o->halo_pull && phase != 1;
+  const bool pull = o->halo_pull && phase != 1 && phase != 3;
   if (pull) {
     MGG_CUDA(cudaEventRecord(ctx->fork[p], st));
     MGG_CUDA(cudaStreamWaitEvent(ctx->aux[p], ctx->fork[p], 0));
@@ -155,7 +155,7 @@ void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg
     count_launch(ctx);
   }
   if (phase != 2) launch_aggregate(ctx, plan, in, out, relu, 1, halo, st);
-  if (phase != 1) {
+  if (phase != 1 && phase != 3) {
     if (pull) MGG_CUDA(cudaStreamWaitEvent(st, ctx->join[p], 0));
     launch_aggregate(ctx, plan, in, out, relu, 2, halo, st);
   }

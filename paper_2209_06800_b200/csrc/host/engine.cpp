@@ -725,7 +725,7 @@ mgg_store* Engine::scratch(std::uint32_t dim, int slot) {
 
 void Engine::aggregate_host(const float* x, std::uint32_t dim, float self_scale,
                             bool relu_in, float* out, int phase) {
-  if (phase < 0 || phase > 2) throw InputError("engine: aggregate phase must be 0, 1 or 2");
+  if (phase < 0 || phase > 3) throw InputError("engine: aggregate phase must be 0..3");
   for (auto d : dev_)
     if (d < 0) throw InputError("engine: aggregate_host needs every part in this process");
   mgg_store* in = scratch(dim, 0);

@@ -5,7 +5,8 @@
 Two logical parts on device 0; part 1's shards live in pinned host memory
 mapped into the device (MGG_MEM_HOST_MAPPED), so every remote row part 0
 gathers crosses PCIe with microsecond latency — a slow "peer". Part 0's K1
-is timed local-only (phase 1), remote-only (phase 2) and pipelined (phase 0);
+is timed local-only (phase 3: the local partitions through the same pair
+kernel), remote-only (phase 2) and pipelined (phase 0);
 hidden = (T_rem + T_loc - T_pipe) / T_rem, and
 overlap_of_shorter = the same numerator over min(T_rem, T_loc) (how much of
 the shorter leg disappears; 1.0 = T_pipe == max(T_loc, T_rem)).
@@ -60,11 +61,13 @@ def run_one(args):
         eng.set_remote_fetch("fine")
         if args.host:
             eng.set_shard_memory(1, mgg.MEM_HOST_MAPPED)
-        t = {ph: eng.time_aggregate_each(args.dim, args.reps, ph)[0] for ph in (0, 1, 2)}
+        # phase 3 = the local partitions through the pipelined kernel itself;
+        # phase 1 = the lean local-only kernel (reported beside it)
+        t = {ph: eng.time_aggregate_each(args.dim, args.reps, ph)[0] for ph in (0, 3, 2, 1)}
         kern = eng.k1_kernels(0)
         st = eng.stats()
         eng.close()
-        pipe, loc, rem = t[0], t[1], t[2]
+        pipe, loc, rem = t[0], t[3], t[2]
         hid = max(0.0, rem + loc - pipe)
         fp = mgg.build_flat_plan(g, 2, 0, args.ps, args.dist, args.wpb, args.dim)
         out.append({
@@ -78,6 +81,7 @@ def run_one(args):
             "remote_edge_fraction": round(fp.remote_cols_len / max(
                 fp.local_cols_len + fp.remote_cols_len, 1), 4),
             "t_pipelined_ns": pipe, "t_local_only_ns": loc, "t_remote_only_ns": rem,
+            "t_local_only_lean_kernel_ns": t[1],
             "hidden_remote_fraction": round(hid / max(rem, 1), 4),
             "overlap_of_shorter": round(hid / max(min(rem, loc), 1), 4),
             "pipe_vs_max": round(pipe / max(loc, rem, 1), 4),
