@@ -203,19 +203,28 @@ __device__ __forceinline__ void cta_chunk(uint32_t total, uint32_t& b0, uint32_t
   b0 = min(blockIdx.x * per, total);
   b1 = min(b0 + per, total);
 }
-// Logical CTAs of this resident CTA as (first, end, step). Round-robin
-// (a.strided) is the reference's in-order block dispatch over the SMs
-// (R:proj/src/sim.cpp block dispatch): the interleaved mapping packs the
+// Logical CTAs of this resident CTA: chunks of `chunk` consecutive logical
+// CTAs dealt round-robin over the resident CTAs (a.strided = chunk size;
+// 0 = one contiguous chunk per resident CTA). Round-robin is the reference's
+// in-order block dispatch over the SMs: the interleaved mapping packs the
 // shorter kind's partitions into the FIRST logical warps (w·dist, ...), and
-// contiguous chunks would hand all of them to a few resident CTAs.
+// contiguous chunks would hand all of them to a few resident CTAs; chunks of
+// a few logical CTAs keep the metadata streams sequential.
 struct LbRange {
-  uint32_t first, end, step;
+  uint32_t first, end, chunk, jump;
+  __device__ __forceinline__ uint32_t next(uint32_t lb) const {
+    ++lb;
+    return lb % chunk ? lb : lb + jump;
+  }
 };
 __device__ __forceinline__ LbRange lb_range(const AggArgs& a) {
-  if (a.strided) return {blockIdx.x, a.num_lblocks, gridDim.x};
-  uint32_t b0, b1;
-  cta_chunk(a.num_lblocks, b0, b1);
-  return {b0, b1, 1u};
+  if (a.strided) {
+    const uint32_t c = a.strided;
+    return {blockIdx.x * c, a.num_lblocks, c, (gridDim.x - 1) * c};
+  }
+  const uint32_t per = max((a.num_lblocks + gridDim.x - 1) / gridDim.x, 1u);
+  const uint32_t b0 = min(blockIdx.x * per, a.num_lblocks);
+  return {b0, min(b0 + per, a.num_lblocks), per, a.num_lblocks};  // one chunk, then past the end
 }
 
 template <int VEC, bool RELU>
@@ -755,7 +764,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
   };
   const LbRange rg = lb_range(a);
   const uint32_t wib = threadIdx.x >> 5;
-  for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
+  for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
     const uint32_t w = lb * a.wpb + wib;
     if (w >= a.num_warps) break;
     uint32_t l0, l1, r0, r1;
@@ -919,7 +928,7 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
         qvalid = true;
         return;
       }
-      plb += rg.step;
+      plb = rg.next(plb);
       pw = plb * a.wpb + wib;
       if (plb >= rg.end || pw >= a.num_warps) {
         pdone = true;
@@ -962,7 +971,7 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
 #pragma unroll 1
   for (int s = 0; s < R; ++s) produce();
 
-  for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
+  for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
     const uint32_t w = lb * a.wpb + wib;
     if (w >= a.num_warps) break;
     uint32_t l0, l1, r0, r1;
@@ -1110,7 +1119,7 @@ __device__ __forceinline__ void agg_pipe_bulk_body(const AggArgs& a) {
         qvalid = true;
         return;
       }
-      plb += rg.step;
+      plb = rg.next(plb);
       pw = plb * a.wpb + wib;
       if (plb >= rg.end || pw >= a.num_warps) {
         pdone = true;
@@ -1161,7 +1170,7 @@ __device__ __forceinline__ void agg_pipe_bulk_body(const AggArgs& a) {
 #pragma unroll 1
   for (int r = 0; r < R; ++r) produce();
 
-  for (uint32_t lb = rg.first; lb < rg.end; lb += rg.step) {
+  for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
     const uint32_t w = lb * a.wpb + wib;
     if (w >= a.num_warps) break;
     uint32_t l0, l1, r0, r1;
@@ -1481,12 +1490,13 @@ int pair_mode() {
 // MGG_AGG_PAIR=0 keeps the warp-window pair loop (ablations, A/B).
 // Whole-list plans (granularity 1, the no_np ablation) keep the warp per
 // list of the paper's baseline.
-// Logical-CTA schedule of the pair kernels: 1 round-robin (default), 0
-// contiguous chunks (MGG_AGG_SCHED=0, A/B).
-int sched_mode() {
-  static const int m = [] {
+// Logical-CTA schedule of the pair kernels: chunks of MGG_AGG_SCHED logical
+// CTAs dealt round-robin (1 = plain round-robin, the default), 0 = one
+// contiguous chunk per resident CTA (A/B).
+uint32_t sched_mode() {
+  static const uint32_t m = [] {
     const char* e = std::getenv("MGG_AGG_SCHED");
-    return e ? std::atoi(e) : 1;
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
   }();
   return m;
 }
@@ -1705,7 +1715,7 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const bool remote_lean = halo && phase == 2;
   const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
-  a.strided = remote && p->granularity == 0 && pair_mode() != 0 && sched_mode() != 0;
+  a.strided = remote && p->granularity == 0 && pair_mode() != 0 ? sched_mode() : 0;
   KernelFn k = remote ? (relu_in ? pick_pair<true>(a.vec, p->granularity)
                                  : pick_pair<false>(a.vec, p->granularity))
                       : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity, p->k1_form)

@@ -318,8 +318,11 @@ def test_phase_halves_sum_to_aggregate(mgg, oracle_mod, fetch, mapping):
         ref = oracle_mod.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
         assert_rows_close(loc + rem, ref, what=f"phases {fetch} map={mapping} dim={dim}")
         assert np.abs(rem).max() > 0 and np.abs(loc - np.maximum(x, 0)).max() > 0
+        # phase 3: the local partitions through the pair kernel (fine) — the same sums
+        loc3 = eng.aggregate(x, 1.0, relu_in=True, phase=3)
+        assert_rows_close(loc3, loc, what=f"phase 3 vs 1 {fetch} map={mapping} dim={dim}")
         with pytest.raises(mgg.MggError):
-            eng.aggregate(x, 1.0, phase=3)
+            eng.aggregate(x, 1.0, phase=4)
         eng.close()
 
 

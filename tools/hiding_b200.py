@@ -59,11 +59,14 @@ def run_one(args):
         model = mgg.make_gcn(args.dim, 16, 8)
         eng = mgg.Engine(g, 2, [0, 0], model, ps=args.ps, dist=args.dist, wpb=args.wpb)
         eng.set_remote_fetch("fine")
+        eng.set_mapping(args.mapping, 0)
         if args.host:
             eng.set_shard_memory(1, mgg.MEM_HOST_MAPPED)
         # phase 3 = the local partitions through the pipelined kernel itself;
         # phase 1 = the lean local-only kernel (reported beside it)
-        t = {ph: eng.time_aggregate_each(args.dim, args.reps, ph)[0] for ph in (0, 3, 2, 1)}
+        t = {}
+        for ph in (1, 3, 2, 0):  # the pipelined launch last: k1_kernels names it
+            t[ph] = eng.time_aggregate_each(args.dim, args.reps, ph)[0]
         kern = eng.k1_kernels(0)
         st = eng.stats()
         eng.close()
@@ -74,7 +77,7 @@ def run_one(args):
             "pair_form": os.environ.get("MGG_AGG_PAIR", "default"),
             "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"),
             "sched": os.environ.get("MGG_AGG_SCHED", "1"), "kernels": kern,
-            "far": far, "nodes": args.nodes, "edges": int(g.num_edges), "dim": args.dim,
+            "far": far, "mapping": args.mapping, "nodes": args.nodes, "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
             "part0_local_edges": fp.local_cols_len, "part0_remote_edges": fp.remote_cols_len,
@@ -101,6 +104,7 @@ def main():
     ap.add_argument("--dist", type=int, default=8)
     ap.add_argument("--wpb", type=int, default=8)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--mapping", type=int, default=0, help="0 interleaved, 1 segregated")
     ap.add_argument("--device-peer", dest="host", action="store_false",
                     help="keep part 1's shard in device memory (same-GPU peer)")
     ap.add_argument("--forms", default="1,2,3,3:16",
