@@ -853,7 +853,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
 // and re-issues the rest of R_i at consume time, exposing the remote latency
 // once per 4 rows); local partitions are reduced from registers meanwhile.
 // A lane reads back only the slots it filled itself, so no barrier is needed.
-template <int VEC, bool RELU, int UNR, int R>
+template <int VEC, bool RELU, int UNR, int R, int DEF>
 __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
   static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
   constexpr int G = 32 / VEC;
@@ -968,6 +968,27 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
     asm volatile("cp.async.commit_group;" ::: "memory");  // empty past the end
     ++issued;
   };
+  // rows of one remote partition from the ring into target t
+  auto consume = [&](int t, int b, int e) {
+    float4 acc = f4zero();
+    for (int k = b; k < e; ++k) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(R - 1) : "memory");
+      float4 x;
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                   : "r"(ring0 + (consumed & (R - 1)) * rstride)
+                   : "memory");
+      ++consumed;
+      if (RELU) x = f4relu(x);
+      acc = f4add(acc, x);
+      produce();  // refills the slot just read (after its value is used)
+    }
+    if (b < e && vlane) red_add4(a.out + static_cast<size_t>(t) * a.pitch + 4 * v, acc);
+  };
+  // deferred remote partitions, oldest first (empty = b == e)
+  int qt[DEF > 0 ? DEF : 1], qb[DEF > 0 ? DEF : 1], qe[DEF > 0 ? DEF : 1];
+#pragma unroll
+  for (int d = 0; d < (DEF > 0 ? DEF : 1); ++d) qt[d] = qb[d] = qe[d] = 0;
 #pragma unroll 1
   for (int s = 0; s < R; ++s) produce();
 
@@ -1014,27 +1035,31 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
         }
         if (vlane) redh(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
-      // (3) consume R_i from the ring; every row consumed issues the next
+      // (3) consume R_i from the ring — or, with DEF > 0, queue it and
+      // consume the remote partition DEF remote pairs older: the group's
+      // next local partitions run while slow remote rows are still landing
       if (i < nr) {
         const int2 m = __ldg(a.rmeta + r0 + i);
         const int end = __ldg(&a.rmeta[r0 + i + 1].y);
-        float4 acc = f4zero();
-        for (int k = m.y; k < end; ++k) {
-          asm volatile("cp.async.wait_group %0;" ::"n"(R - 1) : "memory");
-          float4 x;
-          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
-                       : "r"(ring0 + (consumed & (R - 1)) * rstride)
-                       : "memory");
-          ++consumed;
-          if (RELU) x = f4relu(x);
-          acc = f4add(acc, x);
-          produce();  // refills the slot just read (after its value is used)
+        if (DEF == 0) {
+          consume(m.x, m.y, end);
+        } else {
+          consume(qt[0], qb[0], qe[0]);
+#pragma unroll
+          for (int d = 0; d + 1 < DEF; ++d) {
+            qt[d] = qt[d + 1];
+            qb[d] = qb[d + 1];
+            qe[d] = qe[d + 1];
+          }
+          qt[DEF - 1] = m.x;
+          qb[DEF - 1] = m.y;
+          qe[DEF - 1] = end;
         }
-        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
     }
   }
+#pragma unroll
+  for (int d = 0; d < DEF; ++d) consume(qt[d], qb[d], qe[d]);  // drain
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 // TMA form of agg_pipe (agg_pipe_bulk): the remote rows are fetched by the
@@ -1241,9 +1266,9 @@ __global__ void __launch_bounds__(512, 2) agg_pipe_bulk(AggArgs a) {
   agg_pipe_bulk_body<VEC, RELU, UNR, R>(a);
 }
 
-template <int VEC, bool RELU, int UNR, int R>
+template <int VEC, bool RELU, int UNR, int R, int DEF>
 __global__ void __launch_bounds__(512, 2) agg_pipe(AggArgs a) {
-  agg_pipe_body<VEC, RELU, UNR, R>(a);
+  agg_pipe_body<VEC, RELU, UNR, R, DEF>(a);
 }
 // dynamic shared memory of the pipe kernels: agg_pipe R 16-B slots per
 // thread; agg_pipe_bulk R row slots + R mbarriers per lane group
@@ -1254,14 +1279,14 @@ std::map<const void*, PipeSmem>& pipe_slots() {
   static std::map<const void*, PipeSmem> m;
   return m;
 }
-template <bool RELU, int R>
+template <bool RELU, int R, int DEF = 0>
 KernelFn pick_pipe(uint32_t v) {
-  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 8, R>
-               : v <= 2  ? agg_pipe<2, RELU, 8, R>
-               : v <= 4  ? agg_pipe<4, RELU, 8, R>
-               : v <= 8  ? agg_pipe<8, RELU, 8, R>
-               : v <= 16 ? agg_pipe<16, RELU, 8, R>
-               : v <= 32 ? agg_pipe<32, RELU, 8, R>
+  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 8, R, DEF>
+               : v <= 2  ? agg_pipe<2, RELU, 8, R, DEF>
+               : v <= 4  ? agg_pipe<4, RELU, 8, R, DEF>
+               : v <= 8  ? agg_pipe<8, RELU, 8, R, DEF>
+               : v <= 16 ? agg_pipe<16, RELU, 8, R, DEF>
+               : v <= 32 ? agg_pipe<32, RELU, 8, R, DEF>
                          : agg_wide<RELU>;
   if (v <= 32) {
     static std::mutex mu;
@@ -1501,6 +1526,15 @@ uint32_t sched_mode() {
   return m;
 }
 
+// Remote partitions a pipe group defers before consuming (0, 2 or 4).
+int pipe_defer() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_AGG_PIPE_DEFER");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 int pipe_depth() {
   static const int m = [] {
     const char* e = std::getenv("MGG_AGG_PIPE_DEPTH");  // ring slots per lane
@@ -1513,6 +1547,9 @@ template <bool RELU>
 KernelFn pick_pair(uint32_t v, uint32_t granularity) {
   if (pair_mode() == 0 || granularity == 1) return pick<RELU, true>(v);
   if (pair_mode() == 2) {
+    if (pipe_defer() == 4) return pipe_depth() == 16 ? pick_pipe<RELU, 16, 4>(v)
+                                                     : pick_pipe<RELU, 8, 4>(v);
+    if (pipe_defer() == 2) return pick_pipe<RELU, 8, 2>(v);
     switch (pipe_depth()) {
       case 4: return pick_pipe<RELU, 4>(v);
       case 16: return pick_pipe<RELU, 16>(v);

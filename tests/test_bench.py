@@ -159,3 +159,17 @@ def test_k1_form_rule():
     assert bench.k1_form(long_rows, 32, 2).startswith("agg_gpair")
     assert bench.k1_form(long_rows, 16, 1, form=1).startswith("agg_local")
     assert "4 rows" in bench.k1_form(long_rows, 32, 1, form=3)
+
+
+def test_gpus_n_without_torchrun_needs_n_devices():
+    # `--gpus N` outside torchrun re-executes under torch.distributed.run with N
+    # ranks; with fewer devices visible it says so instead of faking N logical parts
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+         "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+        env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK")})
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("two GPUs visible: the re-exec would run")
+    assert out.returncode != 0
+    assert "CUDA device(s) visible" in (out.stderr + out.stdout)

@@ -53,6 +53,8 @@ def _worker(rank, world, port, q):
         assert sorted(eng.imported) == [p for p in range(world) if p != rank]
         assert all(b == bytes([p]) * 192 for p, b in eng.imported.items())
         m = mdist.max_over_ranks(float(rank) * 1.5)
+        tot = mdist.sum_over_ranks(float(rank + 1))  # bench's link bytes over ranks
+        assert tot == world * (world + 1) / 2
         q.put((rank, allsum, m, None))
         dist.destroy_process_group()
     except Exception as e:  # noqa: BLE001

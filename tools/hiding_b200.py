@@ -76,7 +76,8 @@ def run_one(args):
         out.append({
             "pair_form": os.environ.get("MGG_AGG_PAIR", "default"),
             "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"),
-            "sched": os.environ.get("MGG_AGG_SCHED", "1"), "kernels": kern,
+            "sched": os.environ.get("MGG_AGG_SCHED", "1"),
+            "defer": os.environ.get("MGG_AGG_PIPE_DEFER", "0"), "kernels": kern,
             "far": far, "mapping": args.mapping, "nodes": args.nodes, "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
@@ -128,14 +129,16 @@ def main():
         rows.append(pr)
     for form in args.forms.split(","):
         pair, _, rest = form.partition(":")
-        depth, _, sched = rest.partition(":")
+        depth, _, rest = rest.partition(":")
+        sched, _, defer = rest.partition(":")
         cmd = [sys.executable, os.path.abspath(__file__), "--child"] + [
             a for a in sys.argv[1:] if not a.startswith("--out") and a != args.out
             and a != "--probe"]
         r = subprocess.run(cmd, capture_output=True, text=True,
                            env={**os.environ, "MGG_AGG_PAIR": pair,
                                 "MGG_AGG_PIPE_DEPTH": depth or "8",
-                                "MGG_AGG_SCHED": sched or "1"})
+                                "MGG_AGG_SCHED": sched or "1",
+                                "MGG_AGG_PIPE_DEFER": defer or "0"})
         sys.stderr.write(r.stderr[-3000:])
         rows += [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
         for l in r.stdout.splitlines():
