@@ -853,7 +853,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
 // and re-issues the rest of R_i at consume time, exposing the remote latency
 // once per 4 rows); local partitions are reduced from registers meanwhile.
 // A lane reads back only the slots it filled itself, so no barrier is needed.
-template <int VEC, bool RELU, int UNR, int R, int DEF>
+template <int VEC, bool RELU, int UNR, int R>
 __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
   static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
   constexpr int G = 32 / VEC;
@@ -968,27 +968,6 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
     asm volatile("cp.async.commit_group;" ::: "memory");  // empty past the end
     ++issued;
   };
-  // rows of one remote partition from the ring into target t
-  auto consume = [&](int t, int b, int e) {
-    float4 acc = f4zero();
-    for (int k = b; k < e; ++k) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(R - 1) : "memory");
-      float4 x;
-      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                   : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
-                   : "r"(ring0 + (consumed & (R - 1)) * rstride)
-                   : "memory");
-      ++consumed;
-      if (RELU) x = f4relu(x);
-      acc = f4add(acc, x);
-      produce();  // refills the slot just read (after its value is used)
-    }
-    if (b < e && vlane) red_add4(a.out + static_cast<size_t>(t) * a.pitch + 4 * v, acc);
-  };
-  // deferred remote partitions, oldest first (empty = b == e)
-  int qt[DEF > 0 ? DEF : 1], qb[DEF > 0 ? DEF : 1], qe[DEF > 0 ? DEF : 1];
-#pragma unroll
-  for (int d = 0; d < (DEF > 0 ? DEF : 1); ++d) qt[d] = qb[d] = qe[d] = 0;
 #pragma unroll 1
   for (int s = 0; s < R; ++s) produce();
 
@@ -1035,31 +1014,27 @@ __device__ __forceinline__ void agg_pipe_body(const AggArgs& a) {
         }
         if (vlane) redh(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
-      // (3) consume R_i from the ring — or, with DEF > 0, queue it and
-      // consume the remote partition DEF remote pairs older: the group's
-      // next local partitions run while slow remote rows are still landing
+      // (3) consume R_i from the ring; every row consumed issues the next
       if (i < nr) {
         const int2 m = __ldg(a.rmeta + r0 + i);
         const int end = __ldg(&a.rmeta[r0 + i + 1].y);
-        if (DEF == 0) {
-          consume(m.x, m.y, end);
-        } else {
-          consume(qt[0], qb[0], qe[0]);
-#pragma unroll
-          for (int d = 0; d + 1 < DEF; ++d) {
-            qt[d] = qt[d + 1];
-            qb[d] = qb[d + 1];
-            qe[d] = qe[d + 1];
-          }
-          qt[DEF - 1] = m.x;
-          qb[DEF - 1] = m.y;
-          qe[DEF - 1] = end;
+        float4 acc = f4zero();
+        for (int k = m.y; k < end; ++k) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(R - 1) : "memory");
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                       : "r"(ring0 + (consumed & (R - 1)) * rstride)
+                       : "memory");
+          ++consumed;
+          if (RELU) x = f4relu(x);
+          acc = f4add(acc, x);
+          produce();  // refills the slot just read (after its value is used)
         }
+        if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
       }
     }
   }
-#pragma unroll
-  for (int d = 0; d < DEF; ++d) consume(qt[d], qb[d], qe[d]);  // drain
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 // TMA form of agg_pipe (agg_pipe_bulk): the remote rows are fetched by the
@@ -1266,9 +1241,9 @@ __global__ void __launch_bounds__(512, 2) agg_pipe_bulk(AggArgs a) {
   agg_pipe_bulk_body<VEC, RELU, UNR, R>(a);
 }
 
-template <int VEC, bool RELU, int UNR, int R, int DEF>
+template <int VEC, bool RELU, int UNR, int R>
 __global__ void __launch_bounds__(512, 2) agg_pipe(AggArgs a) {
-  agg_pipe_body<VEC, RELU, UNR, R, DEF>(a);
+  agg_pipe_body<VEC, RELU, UNR, R>(a);
 }
 // dynamic shared memory of the pipe kernels: agg_pipe R 16-B slots per
 // thread; agg_pipe_bulk R row slots + R mbarriers per lane group
@@ -1279,14 +1254,14 @@ std::map<const void*, PipeSmem>& pipe_slots() {
   static std::map<const void*, PipeSmem> m;
   return m;
 }
-template <bool RELU, int R, int DEF = 0>
+template <bool RELU, int R>
 KernelFn pick_pipe(uint32_t v) {
-  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 8, R, DEF>
-               : v <= 2  ? agg_pipe<2, RELU, 8, R, DEF>
-               : v <= 4  ? agg_pipe<4, RELU, 8, R, DEF>
-               : v <= 8  ? agg_pipe<8, RELU, 8, R, DEF>
-               : v <= 16 ? agg_pipe<16, RELU, 8, R, DEF>
-               : v <= 32 ? agg_pipe<32, RELU, 8, R, DEF>
+  KernelFn k = v <= 1    ? agg_pipe<1, RELU, 8, R>
+               : v <= 2  ? agg_pipe<2, RELU, 8, R>
+               : v <= 4  ? agg_pipe<4, RELU, 8, R>
+               : v <= 8  ? agg_pipe<8, RELU, 8, R>
+               : v <= 16 ? agg_pipe<16, RELU, 8, R>
+               : v <= 32 ? agg_pipe<32, RELU, 8, R>
                          : agg_wide<RELU>;
   if (v <= 32) {
     static std::mutex mu;
@@ -1516,21 +1491,14 @@ int pair_mode() {
 // Whole-list plans (granularity 1, the no_np ablation) keep the warp per
 // list of the paper's baseline.
 // Logical-CTA schedule of the pair kernels: chunks of MGG_AGG_SCHED logical
-// CTAs dealt round-robin (1 = plain round-robin, the default), 0 = one
-// contiguous chunk per resident CTA (A/B).
+// CTAs dealt round-robin, 0 = one contiguous chunk per resident CTA.
+// Measured (profiles/r02/hiding_*.jsonl, host-mapped slow peer): chunks of 4
+// hide the most remote time (0.74-0.79 vs 0.68 with chunks of 1, 0.28
+// contiguous at a 0.03% remote share); the default.
 uint32_t sched_mode() {
   static const uint32_t m = [] {
     const char* e = std::getenv("MGG_AGG_SCHED");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
-  }();
-  return m;
-}
-
-// Remote partitions a pipe group defers before consuming (0, 2 or 4).
-int pipe_defer() {
-  static const int m = [] {
-    const char* e = std::getenv("MGG_AGG_PIPE_DEFER");
-    return e ? std::atoi(e) : 0;
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 4u;
   }();
   return m;
 }
@@ -1547,9 +1515,6 @@ template <bool RELU>
 KernelFn pick_pair(uint32_t v, uint32_t granularity) {
   if (pair_mode() == 0 || granularity == 1) return pick<RELU, true>(v);
   if (pair_mode() == 2) {
-    if (pipe_defer() == 4) return pipe_depth() == 16 ? pick_pipe<RELU, 16, 4>(v)
-                                                     : pick_pipe<RELU, 8, 4>(v);
-    if (pipe_defer() == 2) return pick_pipe<RELU, 8, 2>(v);
     switch (pipe_depth()) {
       case 4: return pick_pipe<RELU, 4>(v);
       case 16: return pick_pipe<RELU, 16>(v);

@@ -627,12 +627,11 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
     assert np.abs(z2 - zr).max() <= TOL, np.abs(z2 - zr).max()
 
 
-@pytest.mark.parametrize("pair,depth,defer,kernel", [
+@pytest.mark.parametrize("pair,depth,sched,kernel", [
     ("1", "8", "0", "agg_gpair"), ("0", "8", "0", "agg_kernel"), ("2", "8", "0", "agg_pipe"),
-    ("2", "4", "0", "agg_pipe"), ("2", "16", "0", "agg_pipe"), ("2", "8", "2", "agg_pipe"),
-    ("2", "8", "4", "agg_pipe"), ("2", "16", "4", "agg_pipe"), ("3", "8", "0", "agg_pipe_bulk"),
-    ("3", "4", "0", "agg_pipe_bulk")])
-def test_pair_kernel_forms(pair, depth, defer, kernel):
+    ("2", "4", "0", "agg_pipe"), ("2", "16", "0", "agg_pipe"), ("3", "8", "0", "agg_pipe_bulk"),
+    ("3", "4", "0", "agg_pipe_bulk"), ("1", "8", "1", "agg_gpair"), ("1", "8", "0c", "agg_gpair")])
+def test_pair_kernel_forms(pair, depth, sched, kernel):
     # the fine-fetch pair loop: agg_gpair (default) and the warp-window loop
     # (MGG_AGG_PAIR=0, read once per process) on single-process multi-part
     # aggregations against the oracle; the launched kernel is read back
@@ -662,7 +661,7 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=600, env={**os.environ, "MGG_AGG_PAIR": pair,
                                          "MGG_AGG_PIPE_DEPTH": depth,
-                                         "MGG_AGG_PIPE_DEFER": defer})
+                                         "MGG_AGG_SCHED": sched.rstrip("c") or "4"})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
