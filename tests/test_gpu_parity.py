@@ -628,9 +628,10 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
 
 
 @pytest.mark.parametrize("pair,depth,sched,kernel", [
-    ("1", "8", "0", "agg_gpair"), ("0", "8", "0", "agg_kernel"), ("2", "8", "0", "agg_pipe"),
-    ("2", "4", "0", "agg_pipe"), ("2", "16", "0", "agg_pipe"), ("3", "8", "0", "agg_pipe_bulk"),
-    ("3", "4", "0", "agg_pipe_bulk"), ("1", "8", "1", "agg_gpair"), ("1", "8", "0c", "agg_gpair")])
+    ("1", "8", "4", "agg_gpair"), ("0", "8", "4", "agg_kernel"), ("2", "8", "4", "agg_pipe"),
+    ("2", "4", "4", "agg_pipe"), ("2", "16", "4", "agg_pipe"), ("3", "8", "4", "agg_pipe_bulk"),
+    ("3", "4", "4", "agg_pipe_bulk"), ("1", "8", "1", "agg_gpair"), ("1", "8", "0", "agg_gpair"),
+    ("2", "8", "0", "agg_pipe"), ("1", "8", "16", "agg_gpair")])
 def test_pair_kernel_forms(pair, depth, sched, kernel):
     # the fine-fetch pair loop: agg_gpair (default) and the warp-window loop
     # (MGG_AGG_PAIR=0, read once per process) on single-process multi-part
@@ -661,7 +662,7 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=600, env={**os.environ, "MGG_AGG_PAIR": pair,
                                          "MGG_AGG_PIPE_DEPTH": depth,
-                                         "MGG_AGG_SCHED": sched.rstrip("c") or "4"})
+                                         "MGG_AGG_SCHED": sched})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
