@@ -50,12 +50,23 @@ def locality_graph(n, avg, window, far, seed=0):
     return rp, (key % n).astype(np.uint64)
 
 
+def graphs(args):
+    """(far, graph) pairs: the locality sweep, or one bench workload's graph."""
+    import paper_2209_06800_b200 as mgg
+    if args.graph:
+        import bench
+        _, g, _, _ = bench.build(mgg, args.graph)
+        yield None, g
+        return
+    for far in [float(x) for x in args.far.split(",")]:
+        rp, cl = locality_graph(args.nodes, args.avg, args.window, far)
+        yield far, mgg.CsrGraph.from_csr(rp, cl)
+
+
 def run_one(args):
     import paper_2209_06800_b200 as mgg
     out = []
-    for far in [float(x) for x in args.far.split(",")]:
-        rp, cl = locality_graph(args.nodes, args.avg, args.window, far)
-        g = mgg.CsrGraph.from_csr(rp, cl)
+    for far, g in graphs(args):
         model = mgg.make_gcn(args.dim, 16, 8)
         eng = mgg.Engine(g, 2, [0, 0], model, ps=args.ps, dist=args.dist, wpb=args.wpb)
         eng.set_remote_fetch("fine")
@@ -78,7 +89,8 @@ def run_one(args):
             "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"),
             "sched": os.environ.get("MGG_AGG_SCHED", "1"),
             "defer": os.environ.get("MGG_AGG_PIPE_DEFER", "0"), "kernels": kern,
-            "far": far, "mapping": args.mapping, "nodes": args.nodes, "edges": int(g.num_edges), "dim": args.dim,
+            "graph": args.graph or "locality", "far": far, "mapping": args.mapping,
+            "nodes": int(g.num_nodes), "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
             "part0_local_edges": fp.local_cols_len, "part0_remote_edges": fp.remote_cols_len,
@@ -106,6 +118,7 @@ def main():
     ap.add_argument("--wpb", type=int, default=8)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--mapping", type=int, default=0, help="0 interleaved, 1 segregated")
+    ap.add_argument("--graph", default=None, help="a bench workload's graph instead of the sweep")
     ap.add_argument("--device-peer", dest="host", action="store_false",
                     help="keep part 1's shard in device memory (same-GPU peer)")
     ap.add_argument("--forms", default="1,2,3,3:16",

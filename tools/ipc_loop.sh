@@ -4,7 +4,7 @@
 # usage: tools/ipc_loop.sh N [out]
 N=${1:-10}; OUT=${2:-gpurun_out/ipc_loop.txt}
 mkdir -p "$(dirname "$OUT")"; : > "$OUT"
-for pair in 0 1; do
+for pair in ${PAIRS:-1}; do
   fails=0
   for i in $(seq 1 "$N"); do
     if MGG_AGG_PAIR=$pair timeout 600 python -m pytest tests/test_gpu_multiprocess.py -x -q -m gpu \
