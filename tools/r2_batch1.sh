@@ -1,0 +1,12 @@
+set -x
+cd $GRAFT_REPO_ROOT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x 2>&1 | tail -15 > gpurun_out/r2_gputest.txt
+cat gpurun_out/r2_gputest.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.txt 2>&1; cat gpurun_out/r2_smoke.txt
+timeout 600 python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err
+cat gpurun_out/r2_bench.json; tail -5 gpurun_out/r2_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/r2_bench_ref.json 2> gpurun_out/r2_bench_ref.err
+cat gpurun_out/r2_bench_ref.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --secondary none > gpurun_out/r2_ncu_bench.log 2>&1
+tail -3 gpurun_out/r2_ncu_bench.log
