@@ -36,6 +36,7 @@
 
 #include <cxxabi.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -92,6 +93,10 @@ struct AggArgs {
   // pair kernels: logical CTAs dealt round-robin over the resident CTAs (1)
   // instead of contiguous chunks (0)
   uint32_t strided;
+  // pair kernels, dynamic schedule: resident warps take tickets of `wchunk`
+  // consecutive logical warps from sched[0] (null = the static schedule)
+  uint32_t* sched;
+  uint32_t wchunk;
   const float* halo;          // deduplicated remote rows (halo mode) or null
   // device event trace (traced launches only): 16-B records
   // {globaltimer lo, hi, (smid << 8) | (stage << 1) | begin, logical warp}
@@ -225,6 +230,85 @@ __device__ __forceinline__ LbRange lb_range(const AggArgs& a) {
   const uint32_t per = max((a.num_lblocks + gridDim.x - 1) / gridDim.x, 1u);
   const uint32_t b0 = min(blockIdx.x * per, a.num_lblocks);
   return {b0, min(b0 + per, a.num_lblocks), per, a.num_lblocks};  // one chunk, then past the end
+}
+
+// Logical warps of this resident warp under the dynamic schedule. The
+// static schedule deals every resident CTA a fixed share of logical CTAs up
+// front, so a CTA whose warps stall on remote rows finishes its local share
+// late; here warps take tickets as they go.
+// * A ticket g is a chunk of a.wchunk consecutive logical warps, dealt in a
+//   block-strided order: chunk = (g % kBlocks) * L + g / kBlocks with
+//   L = ceil(chunks / kBlocks). Consecutive tickets sweep kBlocks evenly
+//   spaced positions of the warp range, so any contiguous region — the
+//   interleaved mapping puts every (local, remote) pair in the first
+//   logical warps when one kind is scarce — is spread over the whole launch:
+//   a bounded share of the resident warps works pairs at any time (enough to
+//   keep the remote link busy) while the rest reduce local partitions.
+// * One counter would serialise (~3 ns per same-address atomic at L2), so
+//   tickets are dealt over kShards counters 128 B apart (ticket t of shard s
+//   is g = t * kShards + s); a warp starts on shard (global warp id %
+//   kShards) and moves on when it runs dry — shards only ever run dry, so one
+//   pass over them finds all remaining work.
+// * The next ticket is requested before the current chunk is worked (its
+//   atomic round trip overlaps the chunk).
+// Each resident warp retires once; the last one resets the counters for the
+// next launch on the plan (stream order makes that visible).
+constexpr uint32_t kShards = 16;
+constexpr uint32_t kShardStride = 32;  // u32 words between counters (128 B)
+constexpr uint32_t kBlocks = 32;
+
+template <class F>
+__device__ __forceinline__ void for_each_ticket(const AggArgs& a, F&& run_warp) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t wc = a.wchunk;
+  const uint32_t chunks = (a.num_warps + wc - 1) / wc;
+  const uint32_t L = (chunks + kBlocks - 1) / kBlocks;
+  const uint32_t tickets = L * kBlocks;
+  auto shard_len = [&](uint32_t s) { return tickets > s ? (tickets - s + kShards - 1) / kShards : 0u; };
+  auto ctr = [&](uint32_t s) { return a.sched + s * kShardStride; };
+  uint32_t s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % kShards;
+  auto grab = [&]() -> uint32_t {  // lane 0: a ticket from shard s onwards
+    for (uint32_t k = 0; k < kShards; ++k) {
+      const uint32_t lim = shard_len(s);
+      if (*reinterpret_cast<volatile uint32_t*>(ctr(s)) < lim) {
+        const uint32_t t = atomicAdd(ctr(s), 1u);
+        if (t < lim) return t * kShards + s;
+      }
+      s = s + 1 == kShards ? 0 : s + 1;
+    }
+    return 0xffffffffu;
+  };
+  uint32_t g = 0;
+  if (lane == 0) g = grab();
+  g = __shfl_sync(kFull, g, 0);
+  while (g != 0xffffffffu) {
+    uint32_t tn = 0;
+    if (lane == 0) tn = atomicAdd(ctr(s), 1u);  // speculative: checked after the chunk
+    const uint32_t c = (g % kBlocks) * L + g / kBlocks;  // >= chunks: an empty ticket
+    if (c < chunks) {
+      const uint32_t w0 = c * wc;
+      const uint32_t w1 = min(w0 + wc, a.num_warps);
+      for (uint32_t w = w0; w < w1; ++w) run_warp(w);
+    }
+    if (lane == 0) {
+      if (tn < shard_len(s)) {
+        g = tn * kShards + s;
+      } else {
+        s = s + 1 == kShards ? 0 : s + 1;
+        g = grab();
+      }
+    }
+    g = __shfl_sync(kFull, g, 0);
+  }
+  if (lane == 0) {
+    __threadfence();  // this warp's last ticket is ordered before it retires
+    uint32_t* retired = a.sched + kShards * kShardStride;
+    const uint32_t total = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(retired, 1u) == total - 1) {
+      for (uint32_t k = 0; k < kShards; ++k) atomicExch(ctr(k), 0u);
+      atomicExch(retired, 0u);
+    }
+  }
 }
 
 template <int VEC, bool RELU>
@@ -762,11 +846,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
                      __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
     return b + voff + static_cast<size_t>(c & kMask) * pb;
   };
-  const LbRange rg = lb_range(a);
-  const uint32_t wib = threadIdx.x >> 5;
-  for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
-    const uint32_t w = lb * a.wpb + wib;
-    if (w >= a.num_warps) break;
+  auto run_warp = [&](uint32_t w) {
     uint32_t l0, l1, r0, r1;
     warp_groups(a, w, l0, l1, r0, r1);
     const uint32_t nl = l1 - l0, nr = r1 - r0, n = max(nl, nr);
@@ -837,6 +917,17 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
         if (vlane) red_add4(a.out + static_cast<size_t>(rt) * a.pitch + 4 * v, acc);
       }
     }
+  };
+  if (a.sched) {
+    for_each_ticket(a, run_warp);
+    return;
+  }
+  const LbRange rg = lb_range(a);
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    run_warp(w);
   }
 }
 // Fine-fetch K1 with the remote rows staged in shared memory (agg_pipe):
@@ -1503,6 +1594,18 @@ uint32_t sched_mode() {
   return m;
 }
 
+// Dynamic schedule of the group-per-pair kernel (agg_gpair, for_each_ticket):
+// MGG_AGG_DYN = 1 (default) dynamic with the ticket size from the launch (1
+// or 2 logical warps), N > 1 dynamic with tickets of N logical warps, 0 the
+// static round-robin schedule above (also used when MGG_AGG_SCHED=0).
+uint32_t dyn_chunk() {
+  static const uint32_t m = [] {
+    const char* e = std::getenv("MGG_AGG_DYN");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
+  }();
+  return m;
+}
+
 int pipe_depth() {
   static const int m = [] {
     const char* e = std::getenv("MGG_AGG_PIPE_DEPTH");  // ring slots per lane
@@ -1718,6 +1821,7 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
   a.strided = remote && p->granularity == 0 && pair_mode() != 0 ? sched_mode() : 0;
+  const bool dynamic = a.strided && pair_mode() == 1 && dyn_chunk() != 0;
   KernelFn k = remote ? (relu_in ? pick_pair<true>(a.vec, p->granularity)
                                  : pick_pair<false>(a.vec, p->granularity))
                       : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity, p->k1_form)
@@ -1735,6 +1839,14 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const int threads = 32 * static_cast<int>(p->wpb);
   const unsigned full = resident_grid(k, threads, a.pitch);
   const unsigned grid = std::min<unsigned>(full, a.num_lblocks);
+  if (dynamic) {
+    a.sched = p->sched;
+    // tickets of 2 logical warps when that still leaves >= 16 per resident
+    // warp, else 1 (or the knob). Measured (profiles/r02/dyn_schedule.md):
+    // 2 and 4 hide the same, 4+ loses parallelism on small plans.
+    const uint64_t rw = uint64_t(grid) * p->wpb;
+    a.wchunk = dyn_chunk() > 1 ? dyn_chunk() : (a.num_warps >= 32 * rw ? 2u : 1u);
+  }
   k<<<grid, threads, dyn_smem(k, threads, a.pitch), st>>>(a);
   {
     int dev = 0, sms = 0;

@@ -93,6 +93,8 @@ struct mgg_trace {
   unsigned long long* count = nullptr;
 };
 
+constexpr size_t kSchedBytes = 17 * 128;
+
 struct mgg_dplan {
   mgg_ctx* ctx = nullptr;
   uint32_t part = 0;
@@ -110,6 +112,10 @@ struct mgg_dplan {
   uint32_t* halo_rows = nullptr;   // distinct packed remote rows
   uint64_t halo_len = 0;
   uint32_t* rcols_halo = nullptr;  // remote columns -> halo rows
+  // dynamic work queue of the pair kernel (aggregate.cu for_each_ticket):
+  // 16 shard counters + a retire counter, 128 B apart, kSchedBytes; zero
+  // between launches (the last warp to retire resets them)
+  uint32_t* sched = nullptr;
   // kernels launched by the plan's latest K1 (';'-separated, demangled;
   // mgg_dplan_k1_kernels) — the bench labels its roofline with them
   mutable std::string k1_names;

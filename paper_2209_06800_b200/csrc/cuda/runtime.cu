@@ -883,6 +883,8 @@ int mgg_dplan_upload(mgg_ctx* ctx, const mgg_plan_desc* d, mgg_dplan** out) {
         p->halo_len = d->halo_len;
         p->rcols_halo = upload_array(d->remote_halo_cols, d->remote_cols_len, st);
       }
+      MGG_CUDA(cudaMalloc(&p->sched, kSchedBytes));
+      MGG_CUDA(cudaMemsetAsync(p->sched, 0, kSchedBytes, st));
       MGG_CUDA(cudaStreamSynchronize(st));
       p->num_local_warps = (d->n_local + d->dist - 1) / d->dist;
       const uint64_t nr_w = (d->n_remote + d->dist - 1) / d->dist;
@@ -905,6 +907,7 @@ int mgg_dplan_destroy(mgg_dplan* p) {
   cudaFree(p->rcols);
   cudaFree(p->halo_rows);
   cudaFree(p->rcols_halo);
+  cudaFree(p->sched);
   delete p;
   return MGG_OK;
 }

@@ -627,16 +627,21 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
     assert np.abs(z2 - zr).max() <= TOL, np.abs(z2 - zr).max()
 
 
-@pytest.mark.parametrize("pair,depth,sched,kernel", [
-    ("1", "8", "4", "agg_gpair"), ("0", "8", "4", "agg_kernel"), ("2", "8", "4", "agg_pipe"),
-    ("2", "4", "4", "agg_pipe"), ("2", "16", "4", "agg_pipe"), ("3", "8", "4", "agg_pipe_bulk"),
-    ("3", "4", "4", "agg_pipe_bulk"), ("1", "8", "1", "agg_gpair"), ("1", "8", "0", "agg_gpair"),
-    ("2", "8", "0", "agg_pipe"), ("1", "8", "16", "agg_gpair")])
-def test_pair_kernel_forms(pair, depth, sched, kernel):
-    # the fine-fetch pair loop: agg_gpair (default) and the warp-window loop
-    # (MGG_AGG_PAIR=0, read once per process) on single-process multi-part
-    # aggregations against the oracle; the launched kernel is read back
-    # through mgg_engine_k1_kernels
+@pytest.mark.parametrize("pair,depth,sched,dyn,kernel", [
+    ("1", "8", "4", "1", "agg_gpair"), ("0", "8", "4", "1", "agg_kernel"),
+    ("2", "8", "4", "1", "agg_pipe"), ("2", "4", "4", "1", "agg_pipe"),
+    ("2", "16", "4", "1", "agg_pipe"), ("3", "8", "4", "1", "agg_pipe_bulk"),
+    ("3", "4", "4", "1", "agg_pipe_bulk"), ("1", "8", "1", "0", "agg_gpair"),
+    ("1", "8", "0", "0", "agg_gpair"), ("2", "8", "0", "1", "agg_pipe"),
+    ("1", "8", "16", "0", "agg_gpair"), ("1", "8", "4", "0", "agg_gpair"),
+    ("1", "8", "4", "2", "agg_gpair"), ("1", "8", "4", "7", "agg_gpair")])
+def test_pair_kernel_forms(pair, depth, sched, dyn, kernel):
+    # the fine-fetch pair loop: agg_gpair (default; dynamic ticket schedule
+    # MGG_AGG_DYN=1, static with 0, fixed ticket sizes 2/7) and the other pair
+    # forms (MGG_AGG_PAIR, read once per process) on single-process multi-part
+    # aggregations against the oracle, each aggregation run three times on the
+    # same plan (the ticket counters must come back to zero between launches);
+    # the launched kernel is read back through mgg_engine_k1_kernels
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -650,9 +655,10 @@ for dim, parts, cfg in ((16, 2, (16, 4, 4)), (64, 3, (16, 4, 4)), (200, 4, (16, 
     eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 8), *cfg)
     eng.set_remote_fetch("fine")
     ref = oracle.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
-    out = eng.aggregate(x, 1.0, relu_in=True)
-    err = (np.abs(out - ref) / np.maximum(np.abs(ref).max(1, keepdims=True), 1e-6)).max()
-    assert err <= 1e-4, (dim, parts, err)
+    for rep in range(3):
+        out = eng.aggregate(x, 1.0, relu_in=True)
+        err = (np.abs(out - ref) / np.maximum(np.abs(ref).max(1, keepdims=True), 1e-6)).max()
+        assert err <= 1e-4, (dim, parts, rep, err)
     names = eng.k1_kernels(0)
     want = {kernel!r} if dim <= 128 else "agg_wide"  # rows > 128 floats: one form
     assert any(n.startswith(want) for n in names), names
@@ -662,7 +668,7 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=600, env={**os.environ, "MGG_AGG_PAIR": pair,
                                          "MGG_AGG_PIPE_DEPTH": depth,
-                                         "MGG_AGG_SCHED": sched})
+                                         "MGG_AGG_SCHED": sched, "MGG_AGG_DYN": dyn})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 

@@ -91,14 +91,56 @@ def run(g, parts, dim, cfg, reps=5):
     return rows, csv, kern
 
 
+def run_slow_peer(g, parts, dim, cfg, reps=5):
+    """The same modes timed on part 0 with every other part's shards in pinned
+    host memory mapped into the device (MGG_MEM_HOST_MAPPED): remote rows cross
+    PCIe with microsecond latency, so interleaving / phase separation measure
+    latency hiding (same-device peers have local latency). Part 0 alone."""
+    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 8, 4), *cfg)
+    eng.set_remote_fetch("fine")
+    for q in range(1, parts):
+        eng.set_shard_memory(q, mgg.MEM_HOST_MAPPED)
+    t = {}
+    eng.set_mapping(0, 0)
+    t["mgg"] = eng.time_aggregate_each(dim, reps, 0)[0]
+    t["local_only"] = eng.time_aggregate_each(dim, reps, 3)[0]
+    t["remote_only"] = eng.time_aggregate_each(dim, reps, 2)[0]
+    t["phase_separated"] = t["remote_only"] + eng.time_aggregate_each(dim, reps, 1)[0]
+    eng.set_mapping(1, 0)
+    t["no_interleave"] = eng.time_aggregate_each(dim, reps, 0)[0]
+    eng.set_mapping(0, 1)
+    t["no_np"] = eng.time_aggregate_each(dim, max(2, reps // 2), 0)[0]
+    eng.set_mapping(0, 0)
+    eng.set_remote_fetch("halo")
+    t["mgg_halo"] = eng.time_aggregate_each(dim, reps, 0)[0]
+    kern = eng.k1_kernels(0)
+    eng.close()
+    base = t["mgg"]
+    hid = max(0, t["remote_only"] + t["local_only"] - base)
+    return {"times_ns": t, "ratio_vs_mgg": {k: round(v / max(base, 1), 4) for k, v in t.items()},
+            "hidden_remote_fraction": round(hid / max(t["remote_only"], 1), 4),
+            "pair_kernel": kern}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--slow-peer", action="store_true",
+                    help="part 0 timed with host-mapped peers (run_slow_peer)")
     args = ap.parse_args()
     graphs = [("powerlaw-10K-avg16 (acceptance crit. 6 graph)",
                lambda: mgg.gen_synthetic(mgg.POWERLAW, 10_000, 16, 0), 16)]
-    if not args.quick:
+    if args.slow_peer:  # PCIe-bandwidth-bound at the big graphs' remote shares
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from hiding_b200 import locality_graph
+
+        def loc(far):
+            rp, cl = locality_graph(2_000_000, 25.0, 64, far)
+            return mgg.CsrGraph.from_csr(rp, cl)
+        graphs += [(f"locality 2M/50M far={far}", (lambda f=far: loc(f)), 16)
+                   for far in (0.002, 0.01)]
+    elif not args.quick:
         graphs += [("reddit-shaped", lambda: mgg.gen_synthetic(mgg.POWERLAW, 232_965, 492, 0), 16),
                    ("products-shaped",
                     lambda: mgg.gen_synthetic(mgg.POWERLAW, 2_449_029, 25.259, 0), 16)]
@@ -107,6 +149,12 @@ def main():
         g = mk()
         for parts in (2, 4):
             for cfg in [(16, 8, 8), (32, 16, 2)]:
+                if args.slow_peer:
+                    res.append({"graph": name, "edges": g.num_edges, "parts": parts,
+                                "dim": dim, "cfg": cfg, "remote_shards": "host-mapped (PCIe)",
+                                **run_slow_peer(g, parts, dim, cfg)})
+                    print(json.dumps(res[-1]), flush=True)
+                    continue
                 rows, csv, kern = run(g, parts, dim, cfg)
                 res.append({"graph": name, "edges": g.num_edges, "parts": parts, "dim": dim,
                             "cfg": cfg, "pair_kernel": kern, "rows": rows, "csv": csv})

@@ -87,8 +87,8 @@ def run_one(args):
         out.append({
             "pair_form": os.environ.get("MGG_AGG_PAIR", "default"),
             "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"),
-            "sched": os.environ.get("MGG_AGG_SCHED", "1"),
-            "defer": os.environ.get("MGG_AGG_PIPE_DEFER", "0"), "kernels": kern,
+            "sched": os.environ.get("MGG_AGG_SCHED", "4 (default)"),
+            "dyn": os.environ.get("MGG_AGG_DYN", "default"), "kernels": kern,
             "graph": args.graph or "locality", "far": far, "mapping": args.mapping,
             "nodes": int(g.num_nodes), "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
@@ -143,15 +143,14 @@ def main():
     for form in args.forms.split(","):
         pair, _, rest = form.partition(":")
         depth, _, rest = rest.partition(":")
-        sched, _, defer = rest.partition(":")
+        sched = rest
         cmd = [sys.executable, os.path.abspath(__file__), "--child"] + [
             a for a in sys.argv[1:] if not a.startswith("--out") and a != args.out
             and a != "--probe"]
-        r = subprocess.run(cmd, capture_output=True, text=True,
-                           env={**os.environ, "MGG_AGG_PAIR": pair,
-                                "MGG_AGG_PIPE_DEPTH": depth or "8",
-                                "MGG_AGG_SCHED": sched or "1",
-                                "MGG_AGG_PIPE_DEFER": defer or "0"})
+        env = {**os.environ, "MGG_AGG_PAIR": pair, "MGG_AGG_PIPE_DEPTH": depth or "8"}
+        if sched:  # else the library default (chunks of 4)
+            env["MGG_AGG_SCHED"] = sched
+        r = subprocess.run(cmd, capture_output=True, text=True, env=env)
         sys.stderr.write(r.stderr[-3000:])
         rows += [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
         for l in r.stdout.splitlines():
