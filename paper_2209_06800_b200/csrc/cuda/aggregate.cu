@@ -40,6 +40,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -257,11 +258,13 @@ constexpr uint32_t kShards = 16;
 constexpr uint32_t kShardStride = 32;  // u32 words between counters (128 B)
 constexpr uint32_t kBlocks = 32;
 
-template <class F>
+// KINDS = 2 (agg_gsplit): every chunk is two items, its local and its remote
+// partitions, adjacent in the dealing order; run_warp(w, kind).
+template <int KINDS, class F>
 __device__ __forceinline__ void for_each_ticket(const AggArgs& a, F&& run_warp) {
   const int lane = threadIdx.x & 31;
   const uint32_t wc = a.wchunk;
-  const uint32_t chunks = (a.num_warps + wc - 1) / wc;
+  const uint32_t chunks = (a.num_warps + wc - 1) / wc * KINDS;  // items
   const uint32_t L = (chunks + kBlocks - 1) / kBlocks;
   const uint32_t tickets = L * kBlocks;
   auto shard_len = [&](uint32_t s) { return tickets > s ? (tickets - s + kShards - 1) / kShards : 0u; };
@@ -286,9 +289,9 @@ __device__ __forceinline__ void for_each_ticket(const AggArgs& a, F&& run_warp) 
     if (lane == 0) tn = atomicAdd(ctr(s), 1u);  // speculative: checked after the chunk
     const uint32_t c = (g % kBlocks) * L + g / kBlocks;  // >= chunks: an empty ticket
     if (c < chunks) {
-      const uint32_t w0 = c * wc;
+      const uint32_t w0 = c / KINDS * wc;
       const uint32_t w1 = min(w0 + wc, a.num_warps);
-      for (uint32_t w = w0; w < w1; ++w) run_warp(w);
+      for (uint32_t w = w0; w < w1; ++w) run_warp(w, c % KINDS);
     }
     if (lane == 0) {
       if (tn < shard_len(s)) {
@@ -846,7 +849,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
                      __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
     return b + voff + static_cast<size_t>(c & kMask) * pb;
   };
-  auto run_warp = [&](uint32_t w) {
+  auto run_warp = [&](uint32_t w, uint32_t) {
     uint32_t l0, l1, r0, r1;
     warp_groups(a, w, l0, l1, r0, r1);
     const uint32_t nl = l1 - l0, nr = r1 - r0, n = max(nl, nr);
@@ -919,7 +922,7 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
     }
   };
   if (a.sched) {
-    for_each_ticket(a, run_warp);
+    for_each_ticket<1>(a, run_warp);
     return;
   }
   const LbRange rg = lb_range(a);
@@ -927,7 +930,107 @@ __device__ __forceinline__ void agg_gpair_body(const AggArgs& a) {
   for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
     const uint32_t w = lb * a.wpb + wib;
     if (w >= a.num_warps) break;
-    run_warp(w);
+    run_warp(w, 0);
+  }
+}
+
+// Kind-split form of the fine-fetch K1 (agg_gsplit): the same plan and the
+// same dynamic ticket queue, but a ticket is ONE kind of a chunk of logical
+// warps — its local partitions or its remote ones, adjacent in the dealing
+// order — and each is reduced by the lean group-per-partition loop (UNR rows
+// in flight per group, next column ids prefetched). The overlap the
+// reference builds inside a warp (issue R_i, reduce L_i, consume R_i;
+// R:proj/src/sim.cpp:102-125) happens between warps of the same SM instead:
+// at any time some resident warps hold remote tickets and wait on the link
+// while the others reduce local partitions, and neither loop carries the
+// other's registers (agg_gpair stages PF remote rows per lane across L_i).
+template <int VEC, bool RELU, int UNR>
+__device__ __forceinline__ void agg_gsplit_body(const AggArgs& a) {
+  constexpr int G = 32 / VEC;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / VEC, v = lane % VEC;
+  const bool vlane = v < static_cast<int>(a.vec);
+  const uint32_t voff = vlane ? 16u * v : 0u;
+  const uint32_t pb = a.pitch * 4u;
+  const char* lbase = reinterpret_cast<const char*>(a.own) + voff;
+  asm("mov.b64 %0, %0;" : "+l"(lbase));
+  auto ld = [&](const char* p) {
+    float4 x;
+    asm(MGG_LD_INSN " {%0,%1,%2,%3}, [%4];"
+        : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+        : "l"(p));
+    if (RELU) x = f4relu(x);
+    return x;
+  };
+  // one loop per kind (compile-time), so the local loop carries no
+  // owner-table addressing
+  auto loop = [&](auto remc, uint32_t i0, uint32_t p1) {
+    constexpr bool REM = decltype(remc)::value;
+    constexpr int U = REM ? UNR / 2 : UNR;  // remote rows carry a 64-bit base each
+    const int2* meta = REM ? a.rmeta : a.lmeta;
+    const uint32_t* cols = REM ? a.rcols : a.lcols;
+    auto addr = [&](uint32_t c) {
+      if constexpr (!REM) {
+        return lbase + static_cast<size_t>(c) * pb;
+      } else {
+        const char* b = a.halo ? reinterpret_cast<const char*>(a.halo)
+                               : reinterpret_cast<const char*>(__ldg(
+                                     reinterpret_cast<const unsigned long long*>(a.table) +
+                                     (c >> kShift)));
+        return b + voff + static_cast<size_t>(c & kMask) * pb;
+      }
+    };
+    for (uint32_t i = i0; i < p1; i += G) {
+      const int2 m = __ldg(meta + i);
+      const int end = __ldg(&meta[i + 1].y);
+      float4 acc = f4zero();
+      int k = m.y;
+      uint32_t c[U];
+      if (k + U <= end) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = __ldg(cols + k + u);
+      }
+      for (; k + U <= end; k += U) {
+        float4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] = ld(addr(c[u]));
+        if (k + 2 * U <= end) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) c[u] = __ldg(cols + k + U + u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = f4add(acc, t[u]);
+      }
+      if (k < end) {
+        float4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          t[u] = k + u < end ? ld(addr(__ldg(cols + k + u))) : f4zero();
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = f4add(acc, t[u]);
+      }
+      if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+    }
+  };
+  auto run = [&](uint32_t w, uint32_t kind) {
+    uint32_t l0, l1, r0, r1;
+    warp_groups(a, w, l0, l1, r0, r1);
+    if (kind)
+      loop(std::true_type{}, r0 + grp, r1);
+    else
+      loop(std::false_type{}, l0 + grp, l1);
+  };
+  if (a.sched) {
+    for_each_ticket<2>(a, run);
+    return;
+  }
+  const LbRange rg = lb_range(a);  // static: both kinds of each logical warp
+  const uint32_t wib = threadIdx.x >> 5;
+  for (uint32_t lb = rg.first; lb < rg.end; lb = rg.next(lb)) {
+    const uint32_t w = lb * a.wpb + wib;
+    if (w >= a.num_warps) break;
+    run(w, 1);
+    run(w, 0);
   }
 }
 // Fine-fetch K1 with the remote rows staged in shared memory (agg_pipe):
@@ -1397,6 +1500,20 @@ template <int VEC, bool RELU, int UNR, int PF>
 __global__ void __launch_bounds__(512, 2) agg_gpair(AggArgs a) {
   agg_gpair_body<VEC, RELU, UNR, PF>(a);
 }
+template <int VEC, bool RELU, int UNR>
+__global__ void __launch_bounds__(512, 2) agg_gsplit(AggArgs a) {
+  agg_gsplit_body<VEC, RELU, UNR>(a);
+}
+template <bool RELU, int UNR>
+KernelFn pick_gsplit(uint32_t v) {
+  if (v <= 1) return agg_gsplit<1, RELU, UNR>;
+  if (v <= 2) return agg_gsplit<2, RELU, UNR>;
+  if (v <= 4) return agg_gsplit<4, RELU, UNR>;
+  if (v <= 8) return agg_gsplit<8, RELU, UNR>;
+  if (v <= 16) return agg_gsplit<16, RELU, UNR>;
+  if (v <= 32) return agg_gsplit<32, RELU, UNR>;
+  return agg_wide<RELU>;
+}
 template <bool RELU, int UNR, int PF>
 KernelFn pick_gpair(uint32_t v) {
   if (v <= 1) return agg_gpair<1, RELU, UNR, PF>;
@@ -1631,6 +1748,7 @@ KernelFn pick_pair(uint32_t v, uint32_t granularity) {
       default: return pick_pipe_bulk<RELU, 8>(v);
     }
   }
+  if (pair_mode() == 4) return pick_gsplit<RELU, 8>(v);  // kind-split tickets
   return pick_gpair<RELU, 4, 4>(v);
 }
 
@@ -1821,7 +1939,8 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
   const uint64_t lparts = remote_lean ? p->n_remote : p->n_local;
   const uint64_t ledges = remote_lean ? p->remote_edges : p->local_edges;
   a.strided = remote && p->granularity == 0 && pair_mode() != 0 ? sched_mode() : 0;
-  const bool dynamic = a.strided && pair_mode() == 1 && dyn_chunk() != 0;
+  const bool dynamic =
+      a.strided && (pair_mode() == 1 || pair_mode() == 4) && dyn_chunk() != 0;
   KernelFn k = remote ? (relu_in ? pick_pair<true>(a.vec, p->granularity)
                                  : pick_pair<false>(a.vec, p->granularity))
                       : (relu_in ? pick_lean<true>(a.vec, p->ps, lparts, ledges, p->granularity, p->k1_form)

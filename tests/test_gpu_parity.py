@@ -634,7 +634,9 @@ def test_gcn_normalized_forward(mgg, oracle_mod, parts, dims):
     ("3", "4", "4", "1", "agg_pipe_bulk"), ("1", "8", "1", "0", "agg_gpair"),
     ("1", "8", "0", "0", "agg_gpair"), ("2", "8", "0", "1", "agg_pipe"),
     ("1", "8", "16", "0", "agg_gpair"), ("1", "8", "4", "0", "agg_gpair"),
-    ("1", "8", "4", "2", "agg_gpair"), ("1", "8", "4", "7", "agg_gpair")])
+    ("1", "8", "4", "2", "agg_gpair"), ("1", "8", "4", "7", "agg_gpair"),
+    ("4", "8", "4", "1", "agg_gsplit"), ("4", "8", "4", "0", "agg_gsplit"),
+    ("4", "8", "4", "3", "agg_gsplit")])
 def test_pair_kernel_forms(pair, depth, sched, dyn, kernel):
     # the fine-fetch pair loop: agg_gpair (default; dynamic ticket schedule
     # MGG_AGG_DYN=1, static with 0, fixed ticket sizes 2/7) and the other pair
