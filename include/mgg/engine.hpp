@@ -183,7 +183,10 @@ class Engine {
   int add_store(std::uint32_t dim);
   int add_weight(const float* src, std::size_t n);
   void build_program();
-  int activated(int h, std::uint32_t width, int relu, int a, float scale, int rs);
+  int activated(int h, std::uint32_t width, int relu, int a, float scale, int rs,
+                int& relu_load);
+  // gather tables above this size are HBM-resident for K1 (half the 126 MB L2)
+  static constexpr std::uint64_t kL2GatherBytes = 63ull << 20;
   void build_plans();
   void free_plans();
   void run(const Op& op);

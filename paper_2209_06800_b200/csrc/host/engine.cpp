@@ -102,12 +102,19 @@ int Engine::add_weight(const float* src, std::size_t n) {
   return static_cast<int>(weights_.size()) - 1;
 }
 
-// Self term A = scale * f(H). With a pending ReLU f, the init also writes
-// G = ReLU(H) once per row and the aggregation gathers G (no per-edge ReLU,
-// H itself stays readable through get_hidden); returns the store to gather.
-int Engine::activated(int h, std::uint32_t width, int relu, int a, float scale, int rs) {
+// Self term A = scale * f(H). With a pending ReLU f and a gather table that
+// fits the L2 (L1TEX-bound K1), the init also writes G = ReLU(H) once per row
+// and the aggregation gathers G (no per-edge ReLU, H itself stays readable
+// through get_hidden). An HBM-resident table is instead gathered from H with
+// the ReLU applied on load (`relu_load`): K1 is DRAM-bound there, the ReLU
+// is free, and the G copy (one write of the table) is not. Returns the store
+// to gather.
+int Engine::activated(int h, std::uint32_t width, int relu, int a, float scale, int rs,
+                      int& relu_load) {
+  const std::uint64_t table = g_.num_nodes * ((std::uint64_t(width) + 3) / 4 * 4) * 4;
+  relu_load = relu && !rs && table > kL2GatherBytes ? 1 : 0;
   // a row-scaled (normalised GCN) gather table is always a separate copy
-  const int g = (relu || rs) ? add_store(width) : h;
+  const int g = ((relu && !relu_load) || rs) ? add_store(width) : h;
   Op op{OpKind::init, h, a, g != h ? g : -1, -1, -1, -1, 0, 0, scale, relu};
   op.rs = rs;
   program_.push_back(op);
@@ -159,9 +166,12 @@ void Engine::build_program() {
         pend = norm ? 1 : 0;
       } else {  // aggregate first: A = f(H) + Σ f(H_u), then A·W
         const int A = add_store(a), Y = add_store(b);
-        const int G = activated(cur, a, fin, A, 1.f, norm ? pend + 1 : 0);
+        int rl = 0;
+        const int G = activated(cur, a, fin, A, 1.f, norm ? pend + 1 : 0, rl);
         program_.push_back({OpKind::barrier});
-        program_.push_back({OpKind::aggregate, G, A});
+        Op ag{OpKind::aggregate, G, A};
+        ag.relu = rl;
+        program_.push_back(ag);
         hidden_.push_back(A);
         Op d{OpKind::dense, A, Y, -1, W, -1, -1, 0, last ? 2u : 0u, 1.f, 0};
         d.rs = norm ? 1 : 0;
@@ -203,9 +213,12 @@ void Engine::build_program() {
         program_.push_back({OpKind::dense, A, O, -1, W2, B2, B1, 2, last ? 2u : 0u, 1.f, 0});
       } else {  // A = (1+eps) f(H) + Σ f(H_u); M = ReLU(A·W1+b1); O = M·W2+b2
         const int A = add_store(a), M = add_store(h);
-        const int G = activated(cur, a, fin, A, self, 0);
+        int rl = 0;
+        const int G = activated(cur, a, fin, A, self, 0, rl);
         program_.push_back({OpKind::barrier});
-        program_.push_back({OpKind::aggregate, G, A});
+        Op ag{OpKind::aggregate, G, A};
+        ag.relu = rl;
+        program_.push_back(ag);
         hidden_.push_back(A);
         program_.push_back({OpKind::dense, A, M, -1, W1, B1, -1, 0, 1, 1.f, 0});
         program_.push_back({OpKind::dense, M, O, -1, W2, B2, -1, 0, last ? 2u : 0u, 1.f, 0});

@@ -7,3 +7,8 @@ timeout 600 python tools/hiding_b200.py --forms 1,4 --far 0.002,0.01 --dim 64 --
 for gw in config1 products-gcn reddit-gcn; do
   timeout 300 python tools/hiding_b200.py --graph $gw --device-peer --forms 1,4 --reps 3 --out $O/dev_${gw}.jsonl > /dev/null 2>&1
 done
+# sanitizer over the dynamic-schedule pair kernels
+for pair in 1 4; do for tool in memcheck racecheck synccheck; do
+  MGG_AGG_PAIR=$pair timeout 900 compute-sanitizer --tool $tool python tools/sanitize_pipe.py > $O/san_${pair}_$tool.txt 2>&1
+  echo "pair=$pair $tool: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|max row-relative' $O/san_${pair}_$tool.txt | tr '\n' ' ')"
+done; done
