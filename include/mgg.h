@@ -321,10 +321,13 @@ int mgg_probe_gather(mgg_ctx* ctx, uint32_t part, const float* table, uint32_t p
 int mgg_probe_chase(mgg_ctx* ctx, uint32_t part, const uint32_t* next, uint32_t steps,
                     double* ns_per_load);
 
-/* CUDA graphs (single-device contexts whose parts are all local): capture
- * the calls made between begin and end on the context's stream(s) — the aux
- * streams join back through events — into an executable graph, then replay
- * it with one launch. Replays count their kernels in mgg_ctx_launch_count. */
+/* CUDA graphs: capture the calls made between begin and end on the streams
+ * of the context's local parts (one or several devices) — the aux streams
+ * join back through events — into an executable graph, then replay it with
+ * one launch. Parts driven by other processes are not captured; K3 barriers
+ * towards them are captured flag kernels whose epoch lives on the device, so
+ * every process replays its own graph and the barriers still pair up.
+ * Replays count their kernels in mgg_ctx_launch_count. */
 typedef struct mgg_exec mgg_exec;
 int mgg_capture_begin(mgg_ctx* ctx);
 int mgg_capture_end(mgg_ctx* ctx, mgg_exec** out);
@@ -486,9 +489,10 @@ uint64_t mgg_remote_partition_bytes(uint64_t part_size, uint64_t dim, int paged,
 int mgg_engine_set_config(mgg_engine* e, uint32_t ps, uint32_t dist, uint32_t wpb);
 /* x: num_nodes x in_dim host rows (only this process's rows are read). */
 int mgg_engine_set_input(mgg_engine* e, const float* x);
-/* Device-resident forward (async). On a single-device context (all parts
- * local) the layer program is captured once into a CUDA graph and replayed
- * (re-captured after re-planning); mgg_engine_set_graphs(e, 0) disables it. */
+/* Device-resident forward (async). The layer program of this process's parts
+ * is captured once into a CUDA graph and replayed (re-captured after
+ * re-planning); mgg_engine_set_graphs(e, 0) disables it. With parts in other
+ * processes every process must call it the same number of times. */
 int mgg_engine_forward(mgg_engine* e);
 int mgg_engine_set_graphs(mgg_engine* e, int on);
 /* Local-only K1 form of every plan of the engine (mgg_dplan_set_k1_form). */

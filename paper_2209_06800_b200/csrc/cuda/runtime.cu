@@ -399,8 +399,8 @@ int mgg_ctx_join(mgg_ctx* ctx) {
 int mgg_capture_begin(mgg_ctx* ctx) {
   return guard([&] {
     if (!ctx) throw Status{MGG_E_INPUT, "capture_begin: null context"};
-    if (!ctx->all_local)
-      throw Status{MGG_E_CONFIG, "capture: needs every part in this process"};
+    // parts driven by other processes are not captured: their side of every
+    // K3 barrier is their own replay (the barrier's epoch lives on the device)
     if (ctx->capturing) throw Status{MGG_E_INPUT, "capture_begin: already capturing"};
     const uint32_t p0 = first_local(ctx);
     cudaStream_t st = enter(ctx, p0);
@@ -410,7 +410,7 @@ int mgg_capture_begin(mgg_ctx* ctx) {
     // pull the other parts' streams (other devices' too) into the capture
     MGG_CUDA(cudaEventRecord(ctx->bar_ev[p0], st));
     for (uint32_t p = 0; p < ctx->num_parts; ++p)
-      if (p != p0 && ctx->stream[p] != st) {
+      if (p != p0 && ctx->device[p] >= 0 && ctx->stream[p] != st) {
         enter(ctx, p);
         MGG_CUDA(cudaStreamWaitEvent(ctx->stream[p], ctx->bar_ev[p0], 0));
       }
@@ -426,7 +426,7 @@ int mgg_capture_end(mgg_ctx* ctx, mgg_exec** out) {
     cudaStream_t st = enter(ctx, p);
     ctx->capturing = false;
     for (uint32_t q = 0; q < ctx->num_parts; ++q)  // join the other parts' streams back
-      if (q != p && ctx->stream[q] != st) {
+      if (q != p && ctx->device[q] >= 0 && ctx->stream[q] != st) {
         enter(ctx, q);
         MGG_CUDA(cudaEventRecord(ctx->bar_ev[q], ctx->stream[q]));
         enter(ctx, p);

@@ -417,10 +417,11 @@ void Engine::set_input(const float* x) {
 }
 
 void Engine::forward() {
-  // every part in this process (one device or several): the forward replays
-  // as one CUDA graph — barriers are event joins across the parts' streams
-  bool graphable = graphs_ && !profiling_;
-  for (std::uint32_t p = 0; p < num_parts_ && graphable; ++p) graphable = dev_[p] >= 0;
+  // the forward replays as one CUDA graph of this process's parts: between
+  // parts of this process the barriers are event joins across their streams,
+  // towards parts in other processes K3 flag kernels (device-held epoch, so
+  // every replay advances it; each process replays its own graph)
+  const bool graphable = graphs_ && !profiling_;
   if (!graphable) {
     forward_ops(false);
     return;
