@@ -99,6 +99,13 @@ struct AggArgs {
   uint32_t* sched;
   uint32_t wchunk;
   const float* halo;          // deduplicated remote rows (halo mode) or null
+  // halo pull fused into a local-only group pass (halo mode): copy the
+  // plan's pull_n distinct remote rows (packed owner|offset in pull_rows)
+  // from the owners' shards (`table`) into pull_dst, a proportional slice
+  // per logical warp interleaved with its partitions (HaloPull below)
+  const uint32_t* pull_rows;
+  uint64_t pull_n;
+  float* pull_dst;
   // device event trace (traced launches only): 16-B records
   // {globaltimer lo, hi, (smid << 8) | (stage << 1) | begin, logical warp}
   uint4* trace;
@@ -670,12 +677,72 @@ __device__ __forceinline__ void agg_local_body(const AggArgs& a) {
   if (cur >= 0) ln.flush(a, acc, cur);
 }
 
+// Halo pull riding along a local pass (halo mode, fused): logical warp w of
+// the pass copies halo rows [w·H/W, (w+1)·H/W) (H distinct remote rows, W
+// logical warps) from their owners' shards into the halo. A group issues
+// one row's load before each of its partitions and stores it after, so the
+// remote read's latency is covered by the partition's local gathers, and the
+// remote traffic is spread evenly over the whole pass instead of running as
+// a separate kernel that (persistent, full occupancy) cannot co-run with it.
+// Rows left when a group runs out of partitions are copied two at a time.
+struct HaloPull {
+  uint64_t r = 0, end = 0;
+  uint64_t pol = 0;  // L2 evict-first: the copy must not push the local table out
+  uint32_t step = 0, vec = 0, pitch = 0;
+  int v = 0;
+  bool vlane = false;
+  __device__ __forceinline__ void begin(const AggArgs& a, uint32_t w, int grp, int G, int lane_v,
+                                        bool vl) {
+    end = 0;
+    r = 0;
+    if (!a.pull_n) return;
+    const uint64_t H = a.pull_n, W = a.num_warps;
+    r = w * H / W + grp;
+    end = (w + 1ull) * H / W;
+    step = static_cast<uint32_t>(G);
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    vec = a.vec;
+    pitch = a.pitch;
+    v = lane_v;
+    vlane = vl;
+  }
+  __device__ __forceinline__ bool more() const { return r < end; }
+  __device__ __forceinline__ float4 load(const AggArgs& a, uint64_t row) const {
+    const uint32_t c = __ldg(a.pull_rows + row);
+    const float* b = reinterpret_cast<const float*>(
+        __ldg(reinterpret_cast<const unsigned long long*>(a.table) + (c >> kShift)));
+    float4 x = f4zero();
+    if (vlane)
+      asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                   : "l"(b + static_cast<size_t>(c & kMask) * pitch + 4 * v), "l"(pol));
+    return x;
+  }
+  __device__ __forceinline__ void store(const AggArgs& a, uint64_t row, float4 x) const {
+    if (vlane)
+      asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(
+                       a.pull_dst + row * pitch + 4 * v),
+                   "f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w), "l"(pol)
+                   : "memory");
+  }
+  // the rows this group has left, two per round
+  __device__ __forceinline__ void drain(const AggArgs& a) {
+    for (; r < end; r += 2ull * step) {
+      const bool two = r + step < end;
+      const float4 x0 = load(a, r);
+      const float4 x1 = two ? load(a, r + step) : f4zero();
+      store(a, r, x0);
+      if (two) store(a, r + step, x1);
+    }
+  }
+};
+
 // Group-per-partition local K1 for short partitions (HBM-resident tables):
 // each VEC-lane group walks its own partition, UNR rows in flight per group
 // (the next UNR column ids prefetched),
 // so a warp keeps 32/VEC partitions' gathers outstanding at once instead of
 // one partition's predicated window.
-template <int VEC, bool RELU, int UNR>
+template <int VEC, bool RELU, int UNR, bool PULL = false>
 __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -700,7 +767,12 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
     if (w >= a.num_warps) break;
     const uint32_t l0 = w * a.dist;
     const uint32_t l1 = min(l0 + a.dist, a.nL);
+    HaloPull hp;
+    if (PULL) hp.begin(a, w, grp, G, v, vlane);
     for (uint32_t i = l0 + grp; i < l1; i += G) {
+      const bool pull = PULL && hp.more();
+      const uint64_t pr = hp.r;
+      const float4 px = pull ? hp.load(a, pr) : f4zero();
       const int2 m = __ldg(a.lmeta + i);
       const int end = __ldg(&a.lmeta[i + 1].y);
       float4 acc = f4zero();
@@ -731,7 +803,12 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
         for (int u = 0; u < UNR; ++u) acc = f4add(acc, t[u]);
       }
       if (vlane) red_add4(a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v, acc);
+      if (pull) {
+        hp.store(a, pr, px);
+        hp.r += G;
+      }
     }
+    if (PULL) hp.drain(a);
   }
 }
 // agg_group with L2 eviction hints: gathered rows evict-last (they are the
@@ -739,7 +816,7 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
 // FETCH: L2 fetch size of the gathered-row misses — 0 the default (the line:
 // 64-B rows also bring their neighbour row in, ~1.3-1.5x DRAM bytes on
 // random tables that do not fit L2), 64 = `L2::64B` (only the row's sectors).
-template <int VEC, bool RELU, int UNR, int FETCH = 0>
+template <int VEC, bool RELU, int UNR, int FETCH = 0, bool PULL = false>
 __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -781,7 +858,12 @@ __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
     if (w >= a.num_warps) break;
     const uint32_t l0 = w * a.dist;
     const uint32_t l1 = min(l0 + a.dist, a.nL);
+    HaloPull hp;
+    if (PULL) hp.begin(a, w, grp, G, v, vlane);
     for (uint32_t i = l0 + grp; i < l1; i += G) {
+      const bool pull = PULL && hp.more();
+      const uint64_t pr = hp.r;
+      const float4 px = pull ? hp.load(a, pr) : f4zero();
       const int2 m = __ldg(a.lmeta + i);
       const int end = __ldg(&a.lmeta[i + 1].y);
       float4 acc = f4zero();
@@ -816,7 +898,12 @@ __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
                          a.out + static_cast<size_t>(m.x) * a.pitch + 4 * v),
                      "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w), "l"(pol_first)
                      : "memory");
+      if (pull) {
+        hp.store(a, pr, px);
+        hp.r += G;
+      }
     }
+    if (PULL) hp.drain(a);
   }
 }
 // Group-per-partition form of the paired (fine-fetch) K1: group g of a
@@ -1525,9 +1612,9 @@ KernelFn pick_gpair(uint32_t v) {
   return agg_wide<RELU>;
 }
 
-template <int VEC, bool RELU, int UNR>
+template <int VEC, bool RELU, int UNR, bool PULL = false>
 __global__ void __launch_bounds__(512, 2) agg_group(AggArgs a) {
-  agg_group_body<VEC, RELU, UNR>(a);
+  agg_group_body<VEC, RELU, UNR, PULL>(a);
 }
 template <bool RELU, int UNR>
 KernelFn pick_group(uint32_t v) {
@@ -1539,9 +1626,9 @@ KernelFn pick_group(uint32_t v) {
   if (v <= 32) return agg_group<32, RELU, UNR>;
   return agg_wide<RELU>;
 }
-template <int VEC, bool RELU, int UNR, int FETCH>
+template <int VEC, bool RELU, int UNR, int FETCH, bool PULL = false>
 __global__ void __launch_bounds__(512, 2) agg_group_hint(AggArgs a) {
-  agg_group_hint_body<VEC, RELU, UNR, FETCH>(a);
+  agg_group_hint_body<VEC, RELU, UNR, FETCH, PULL>(a);
 }
 int l2_fetch() {
   static const int m = [] {
@@ -1887,9 +1974,53 @@ KernelFn pick_traced(uint32_t v) {
   throw Status{MGG_E_CONFIG, "trace: rows wider than 128 floats are not traced"};
 }
 
+// The group-form kernel with the halo pull compiled in (PULL = true) that
+// matches a local-pass kernel, or null when the form has none (warp window,
+// wide rows, A/B variants): then the pull kernel runs first.
+template <int VEC, bool RELU>
+void add_pull_pairs(std::map<const void*, KernelFn>& m) {
+  m[reinterpret_cast<const void*>(agg_group<VEC, RELU, 8>)] = agg_group<VEC, RELU, 8, true>;
+  m[reinterpret_cast<const void*>(agg_group<VEC, RELU, 4>)] = agg_group<VEC, RELU, 4, true>;
+}
+KernelFn pull_variant(KernelFn k) {
+  static const std::map<const void*, KernelFn> pairs = [] {
+    std::map<const void*, KernelFn> m;
+    add_pull_pairs<1, false>(m), add_pull_pairs<2, false>(m), add_pull_pairs<4, false>(m);
+    add_pull_pairs<8, false>(m), add_pull_pairs<16, false>(m), add_pull_pairs<32, false>(m);
+    add_pull_pairs<1, true>(m), add_pull_pairs<2, true>(m), add_pull_pairs<4, true>(m);
+    add_pull_pairs<8, true>(m), add_pull_pairs<16, true>(m), add_pull_pairs<32, true>(m);
+    m[reinterpret_cast<const void*>(agg_group_hint<4, false, 8, 0>)] =
+        agg_group_hint<4, false, 8, 0, true>;
+    m[reinterpret_cast<const void*>(agg_group_hint<4, true, 8, 0>)] =
+        agg_group_hint<4, true, 8, 0, true>;
+    m[reinterpret_cast<const void*>(agg_group_hint<16, false, 8, 0>)] =
+        agg_group_hint<16, false, 8, 0, true>;
+    m[reinterpret_cast<const void*>(agg_group_hint<16, true, 8, 0>)] =
+        agg_group_hint<16, true, 8, 0, true>;
+    return m;
+  }();
+  const auto it = pairs.find(reinterpret_cast<const void*>(k));
+  return it == pairs.end() ? nullptr : it->second;
+}
+
+// Halo pull fused into the local pass (HaloPull) or the pull kernel on the
+// aux stream (which, next to a persistent full-occupancy local pass, cannot
+// co-run with it): MGG_HALO_FUSE = 1 always fused, 0 never, unset = fused
+// when the halo comes over a slower link than the part's own HBM (run_aggregate).
+// Measured (profiles/r02/halo_fuse.md): against a slow peer the fused pass
+// hides 0.50-0.54 of the remote time where the separate pull hides 0.02-0.05;
+// with same-device "peers" (both legs on one HBM) it costs 10-18%.
+int halo_fuse_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_HALO_FUSE");
+    return e ? std::atoi(e) : -1;
+  }();
+  return m;
+}
+
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                       mgg_store* out, int relu_in, int phase, const float* halo,
-                      cudaStream_t st, const TraceSink* trace) {
+                      cudaStream_t st, const TraceSink* trace, float* pull_dst) {
   AggArgs a{};
   a.lmeta = p->lmeta;
   a.lcols = p->lcols;
@@ -1926,6 +2057,11 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
     a.halo = nullptr;
     warps = (a.nL + a.dist - 1) / a.dist;
   }
+  if (pull_dst && (warps == 0 || !halo || phase != 1)) {  // nothing to ride along
+    launch_halo_pull(p, in, pull_dst, st);
+    count_launch(ctx);
+    pull_dst = nullptr;
+  }
   if (warps == 0) return;
   if (warps > 0xffffffffull) throw Status{MGG_E_CONFIG, "aggregate: too many warps"};
   a.num_warps = static_cast<uint32_t>(warps);
@@ -1954,6 +2090,17 @@ void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
     a.trace_n = reinterpret_cast<unsigned long long*>(trace->count);
     a.trace_cap = trace->capacity;
     a.trace_warps = trace->warp_limit;
+  }
+  if (pull_dst) {
+    if (KernelFn kp = pull_variant(k)) {
+      k = kp;
+      a.pull_rows = p->halo_rows;
+      a.pull_n = p->halo_len;
+      a.pull_dst = pull_dst;
+    } else {  // warp-window / wide forms carry no pull: copy first
+      launch_halo_pull(p, in, pull_dst, st);
+      count_launch(ctx);
+    }
   }
   const int threads = 32 * static_cast<int>(p->wpb);
   const unsigned full = resident_grid(k, threads, a.pitch);

@@ -136,9 +136,14 @@ struct TraceSink {
   void* count;
   uint32_t capacity, warp_limit;
 };
+// pull_dst (halo mode, the local pass): also copy the plan's distinct remote
+// rows into pull_dst — fused into the local pass when its kernel is a group
+// form, else by the pull kernel on `st` first.
 void launch_aggregate(mgg_ctx* ctx, const mgg_dplan* p, const mgg_store* in,
                       mgg_store* out, int relu_in, int phase, const float* halo,
-                      cudaStream_t st, const TraceSink* trace = nullptr);
+                      cudaStream_t st, const TraceSink* trace = nullptr,
+                      float* pull_dst = nullptr);
+int halo_fuse_mode();
 void launch_strip_owner(uint32_t* cols, uint64_t n, cudaStream_t st);
 void launch_halo_pull(const mgg_dplan* p, const mgg_store* in, float* halo, cudaStream_t st);
 void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg_store* out,

@@ -147,6 +147,18 @@ void run_aggregate(mgg_ctx* ctx, const mgg_dplan* plan, const mgg_store* in, mgg
   if (!plan->rcols_halo) throw Status{MGG_E_INPUT, "aggregate: plan has no halo"};
   const uint32_t p = plan->part;
   const bool pull = o->halo_pull && phase != 1 && phase != 3;
+  bool fuse = halo_fuse_mode() == 1;
+  if (halo_fuse_mode() < 0)  // auto: the halo comes over a link slower than own HBM
+    for (uint32_t q = 0; q < ctx->num_parts; ++q)
+      if (q != p)
+        fuse |= in->imported[q] || in->mem[q] != MGG_MEM_DEVICE ||
+                (ctx->device[q] >= 0 && ctx->device[q] != ctx->device[p]);
+  if (pull && phase == 0 && fuse) {
+    // the pull rides along the local pass (HaloPull), then the remote pass
+    launch_aggregate(ctx, plan, in, out, relu, 1, halo, st, nullptr, const_cast<float*>(halo));
+    launch_aggregate(ctx, plan, in, out, relu, 2, halo, st);
+    return;
+  }
   if (pull) {
     MGG_CUDA(cudaEventRecord(ctx->fork[p], st));
     MGG_CUDA(cudaStreamWaitEvent(ctx->aux[p], ctx->fork[p], 0));

@@ -818,3 +818,35 @@ def test_peer_probes_refit_on_multi_gpu(mgg):
                                                                           4_000_000),
                                   "peer_chase_ns": ns, "peer_gather_gbps": gbps}, 1.965, 148)
     assert fit["latencies"]["remoteGetBase"] > fit["latencies"]["localLoadBase"] // 4
+
+
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_halo_pull_fused_and_separate(fuse):
+    # halo mode: the distinct remote rows copied by the local pass itself
+    # (HaloPull, group forms; MGG_HALO_FUSE=1, the default for peers behind a
+    # slower link) or by the pull kernel (MGG_HALO_FUSE=0, the default for
+    # same-device parts, and the warp-window / wide forms), against the
+    # oracle; three launches per plan, several layer widths and configs
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np, oracle, paper_2209_06800_b200 as mgg
+g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 18, 12)
+for dim, parts, cfg in ((16, 2, (16, 4, 4)), (64, 3, (16, 2, 8)), (200, 4, (16, 4, 4)),
+                        (3, 2, (32, 16, 2)), (16, 4, (8, 1, 1)), (32, 8, (16, 16, 16))):
+    x = mgg.random_features(g.num_nodes, dim, seed=dim)
+    eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 8), *cfg)
+    eng.set_remote_fetch("halo")
+    ref = oracle.aggregate(g.row_ptr, g.col_idx, x, relu_in=True)
+    for rep in range(3):
+        out = eng.aggregate(x, 1.0, relu_in=True)
+        err = (np.abs(out - ref) / np.maximum(np.abs(ref).max(1, keepdims=True), 1e-6)).max()
+        assert err <= 1e-4, (dim, parts, cfg, rep, err)
+    eng.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=600, env={**os.environ, "MGG_HALO_FUSE": fuse})
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

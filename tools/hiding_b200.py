@@ -69,7 +69,7 @@ def run_one(args):
     for far, g in graphs(args):
         model = mgg.make_gcn(args.dim, 16, 8)
         eng = mgg.Engine(g, 2, [0, 0], model, ps=args.ps, dist=args.dist, wpb=args.wpb)
-        eng.set_remote_fetch("fine")
+        eng.set_remote_fetch(args.fetch)
         eng.set_mapping(args.mapping, 0)
         if args.host:
             eng.set_shard_memory(1, mgg.MEM_HOST_MAPPED)
@@ -90,6 +90,7 @@ def run_one(args):
             "sched": os.environ.get("MGG_AGG_SCHED", "4 (default)"),
             "dyn": os.environ.get("MGG_AGG_DYN", "default"), "kernels": kern,
             "graph": args.graph or "locality", "far": far, "mapping": args.mapping,
+            "fetch": args.fetch,
             "nodes": int(g.num_nodes), "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
@@ -119,6 +120,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--mapping", type=int, default=0, help="0 interleaved, 1 segregated")
     ap.add_argument("--graph", default=None, help="a bench workload's graph instead of the sweep")
+    ap.add_argument("--fetch", default="fine", choices=["fine", "halo"],
+                    help="halo: deduplicated pull on the aux stream || local pass, then the "
+                         "remote pass (phase 2 = pull + remote pass)")
     ap.add_argument("--device-peer", dest="host", action="store_false",
                     help="keep part 1's shard in device memory (same-GPU peer)")
     ap.add_argument("--forms", default="1,2,3,3:16",
