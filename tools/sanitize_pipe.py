@@ -2,7 +2,8 @@
 pair kernels (MGG_AGG_PAIR=2 agg_pipe / 3 agg_pipe_bulk):
 `MGG_AGG_PAIR=3 compute-sanitizer --tool {memcheck,racecheck,synccheck} python
 tools/sanitize_pipe.py` — widths 3-64, 2-3 parts, device and host-mapped
-peers, checked against the oracle."""
+peers, checked against the oracle. MGG_SAN_FETCH=halo: the halo path (the
+host-mapped case takes the pull fused into the local pass)."""
 import os
 import sys
 
@@ -19,7 +20,7 @@ for dim in (3, 16, 64):
     ref = oracle.aggregate(g.row_ptr, g.col_idx, x)
     for parts, cfg, host in ((2, (16, 4, 4), False), (3, (8, 2, 2), True), (2, (32, 16, 8), False)):
         eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 8, 4), *cfg)
-        eng.set_remote_fetch("fine")
+        eng.set_remote_fetch(os.environ.get("MGG_SAN_FETCH", "fine"))
         if host:
             eng.set_shard_memory(parts - 1, mgg.MEM_HOST_MAPPED)
         out = eng.aggregate(x, 1.0)
