@@ -89,6 +89,14 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim,
                      mgg_store** out);
 int mgg_store_destroy(mgg_store* s);
 int mgg_store_info(const mgg_store* s, uint32_t* dim, uint32_t* pitch);
+/* Layout of a store's shards: *symmetric = 1 when every part's shard lives
+ * in ONE virtual range reserved with the CUDA VMM API (cuMemAddressReserve +
+ * one cuMemCreate per part on its device, mapped for every local device):
+ * part p at base + p * stride, so kernels address a peer's rows
+ * arithmetically. Used for single-process contexts whose shards are device
+ * memory (MGG_VMM=0 disables it); stores of multi-process contexts are one
+ * allocation per shard plus CUDA IPC imports (*symmetric = 0). */
+int mgg_store_layout(const mgg_store* s, int* symmetric, uint64_t* stride);
 /* Where a local part's shards live (stores created after the call):
  *  MGG_MEM_DEVICE (0)       cudaMalloc on the part's device (default);
  *  MGG_MEM_HOST_MAPPED (1)  pinned host memory mapped into the device: a slow

@@ -80,6 +80,7 @@ _sig("mgg_ctx_launch_count", U64, vp)
 _sig("mgg_store_create", I, vp, u64p, U32, PP)
 _sig("mgg_store_destroy", I, vp)
 _sig("mgg_store_info", I, vp, u32p, u32p)
+_sig("mgg_store_layout", I, vp, C.POINTER(C.c_int), u64p)
 _sig("mgg_store_ipc_export", I, vp, U32, vp)
 _sig("mgg_store_ipc_import", I, vp, U32, vp)
 _sig("mgg_store_upload", I, vp, f32p, U64, U64, U32)

@@ -66,6 +66,12 @@ struct mgg_store {
   // alternate slabs so the DMA engine never waits for a re-pitch
   std::vector<float*> stage;
   std::vector<cudaEvent_t> stage_ev;
+  // symmetric VMM layout (single-process stores of device memory): one
+  // virtual range, part p's shard at vmm_base + p * vmm_stride, physically
+  // on part p's device and mapped for every local device (vmm_size per part)
+  char* vmm_base = nullptr;
+  uint64_t vmm_stride = 0;
+  std::vector<size_t> vmm_size;
   uint64_t rows(uint32_t p) const { return lb[p + 1] - lb[p]; }
 };
 

@@ -1,5 +1,6 @@
 // Device runtime: contexts, symmetric stores, device plans, K3 barrier and
 // the C-ABI of layer A (include/mgg.h).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -516,6 +517,126 @@ int mgg_event_elapsed_between(mgg_ctx* ctx, uint32_t part_a, uint32_t a, uint32_
   });
 }
 
+// ---- symmetric VMM stores -------------------------------------------------
+// Driver entry points are fetched through the runtime (no link-time libcuda
+// dependency: the library still loads where no driver exists).
+struct Vmm {
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemSetAccess) access = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemAddressFree) vfree = nullptr;
+  bool ok = false;
+};
+const Vmm& vmm() {
+  static const Vmm v = [] {
+    Vmm r;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q{};
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    r.ok = get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&r.granularity)) &&
+           get("cuMemCreate", reinterpret_cast<void**>(&r.create)) &&
+           get("cuMemAddressReserve", reinterpret_cast<void**>(&r.reserve)) &&
+           get("cuMemMap", reinterpret_cast<void**>(&r.map)) &&
+           get("cuMemSetAccess", reinterpret_cast<void**>(&r.access)) &&
+           get("cuMemRelease", reinterpret_cast<void**>(&r.release)) &&
+           get("cuMemUnmap", reinterpret_cast<void**>(&r.unmap)) &&
+           get("cuMemAddressFree", reinterpret_cast<void**>(&r.vfree));
+    cudaGetLastError();
+    return r;
+  }();
+  return v;
+}
+// MGG_VMM=0 keeps one cudaMalloc per shard (the pointer-table layout).
+bool vmm_wanted() {
+  static const bool m = [] {
+    const char* e = std::getenv("MGG_VMM");
+    return !e || std::atoi(e) != 0;
+  }();
+  return m;
+}
+void drv(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw Status{MGG_E_CUDA, std::string("VMM ") + what + " failed"};
+}
+
+// Allocates every local part's shard in one symmetric virtual range (all
+// parts local and in device memory); false when VMM is off or unavailable.
+bool vmm_store_alloc(mgg_store* s) {
+  mgg_ctx* ctx = s->ctx;
+  if (!vmm_wanted() || !ctx->all_local || !vmm().ok) return false;
+  for (uint32_t p = 0; p < ctx->num_parts; ++p)
+    if (ctx->shard_mem[p] != MGG_MEM_DEVICE) return false;
+  const Vmm& v = vmm();
+  size_t gran = 0;
+  std::vector<int> devs;
+  for (uint32_t p = 0; p < ctx->num_parts; ++p)
+    if (std::find(devs.begin(), devs.end(), ctx->device[p]) == devs.end())
+      devs.push_back(ctx->device[p]);
+  for (int d : devs) {
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = d;
+    size_t g = 0;
+    drv(v.granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "granularity");
+    gran = std::max(gran, g);
+  }
+  auto up = [&](size_t x) { return (x + gran - 1) / gran * gran; };
+  s->vmm_size.assign(ctx->num_parts, 0);
+  size_t stride = gran;
+  for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+    s->vmm_size[p] = up(std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256));
+    stride = std::max(stride, s->vmm_size[p]);
+  }
+  CUdeviceptr base = 0;
+  drv(v.reserve(&base, stride * ctx->num_parts, gran, 0, 0), "address reserve");
+  s->vmm_base = reinterpret_cast<char*>(base);
+  s->vmm_stride = stride;
+  std::vector<CUmemAccessDesc> acc(devs.size());
+  for (size_t i = 0; i < devs.size(); ++i) {
+    acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc[i].location.id = devs[i];
+    acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  }
+  for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = ctx->device[p];
+    CUmemGenericAllocationHandle h = 0;
+    drv(v.create(&h, s->vmm_size[p], &prop, 0), "create");
+    const CUdeviceptr at = base + p * stride;
+    const CUresult mr = v.map(at, s->vmm_size[p], 0, h, 0);
+    v.release(h);  // the mapping keeps the memory alive
+    drv(mr, "map");
+    drv(v.access(at, s->vmm_size[p], acc.data(), acc.size()), "set access");
+    s->shard[p] = reinterpret_cast<float*>(at);
+    s->owned[p] = 1;
+    s->mem[p] = MGG_MEM_DEVICE;
+    s->bytes[p] = std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256);
+    MGG_CUDA(cudaSetDevice(ctx->device[p]));
+    MGG_CUDA(cudaMemsetAsync(s->shard[p], 0, s->bytes[p], ctx->stream[p]));
+    MGG_CUDA(cudaStreamSynchronize(ctx->stream[p]));
+  }
+  return true;
+}
+
+void vmm_store_free(mgg_store* s) {
+  if (!s->vmm_base) return;
+  const Vmm& v = vmm();
+  const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(s->vmm_base);
+  for (uint32_t p = 0; p < s->ctx->num_parts; ++p)
+    if (p < s->vmm_size.size() && s->vmm_size[p] && s->shard[p])
+      v.unmap(base + p * s->vmm_stride, s->vmm_size[p]);
+  v.vfree(base, s->vmm_stride * s->ctx->num_parts);
+  s->vmm_base = nullptr;
+}
+
 int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_store** out) {
   return guard([&] {
     if (!ctx || !part_lb || !out) throw Status{MGG_E_INPUT, "store_create: null argument"};
@@ -536,7 +657,8 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
       s->dtable.assign(ctx->num_parts, nullptr);
       s->stage.assign(2 * ctx->num_parts, nullptr);
       s->stage_ev.assign(5 * ctx->num_parts, nullptr);
-      for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+      const bool symmetric = vmm_store_alloc(s);
+      for (uint32_t p = 0; p < ctx->num_parts && !symmetric; ++p) {
         if (ctx->device[p] < 0) continue;
         MGG_CUDA(cudaSetDevice(ctx->device[p]));
         const size_t bytes = std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256);
@@ -611,6 +733,13 @@ int mgg_store_rehome(mgg_store* s) {
 int mgg_store_destroy(mgg_store* s) {
   if (!s) return MGG_OK;
   mgg_ctx* ctx = s->ctx;
+  if (s->vmm_base) {  // symmetric range: every device done with it, then unmapped
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      if (ctx->device[p] >= 0 && cudaSetDevice(ctx->device[p]) == cudaSuccess)
+        cudaDeviceSynchronize();
+    vmm_store_free(s);
+    std::fill(s->owned.begin(), s->owned.end(), 0);
+  }
   for (uint32_t p = 0; p < ctx->num_parts; ++p) {
     if (s->owned[p] && s->shard[p]) {
       cudaSetDevice(ctx->device[p]);
@@ -636,6 +765,13 @@ int mgg_store_destroy(mgg_store* s) {
   return MGG_OK;
 }
 
+int mgg_store_layout(const mgg_store* s, int* symmetric, uint64_t* stride) {
+  if (!s) return MGG_E_INPUT;
+  if (symmetric) *symmetric = s->vmm_base ? 1 : 0;
+  if (stride) *stride = s->vmm_stride;
+  return MGG_OK;
+}
+
 int mgg_store_info(const mgg_store* s, uint32_t* dim, uint32_t* pitch) {
   if (!s) return MGG_E_INPUT;
   if (dim) *dim = s->dim;
@@ -649,6 +785,8 @@ int mgg_store_ipc_export(const mgg_store* s, uint32_t part, void* handle64) {
       throw Status{MGG_E_INPUT, "ipc_export: part is not a local shard"};
     if (s->mem[part] != MGG_MEM_DEVICE)
       throw Status{MGG_E_CONFIG, "ipc_export: shard is not device memory"};
+    if (s->vmm_base)
+      throw Status{MGG_E_CONFIG, "ipc_export: symmetric (VMM) store of a single-process context"};
     MGG_CUDA(cudaSetDevice(s->ctx->device[part]));
     cudaIpcMemHandle_t h;
     MGG_CUDA(cudaIpcGetMemHandle(&h, s->shard[part]));

@@ -850,3 +850,46 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=600, env={**os.environ, "MGG_HALO_FUSE": fuse})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("vmm", ["1", "0"])
+def test_symmetric_vmm_store(vmm):
+    # single-process stores are one VMM range (mgg_store_layout: symmetric,
+    # part p at base + p * stride) unless MGG_VMM=0; the pair kernel and the
+    # halo pull address peers arithmetically on it (MGG_FLAT) — both layouts
+    # against the oracle, fine and halo fetch, one and several devices' worth
+    # of parts on device 0
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys, ctypes as C; sys.path.insert(0, {root!r})
+import numpy as np, oracle, paper_2209_06800_b200 as mgg
+from paper_2209_06800_b200._lib import lib
+ctx = C.c_void_p(); devs = (C.c_int32 * 3)(0, 0, 0)
+assert lib.mgg_ctx_create(3, devs, C.byref(ctx)) == 0
+lb = np.array([0, 1000, 5000, 7000], np.uint64)
+st = C.c_void_p()
+assert lib.mgg_store_create(ctx, lb.ctypes.data_as(C.POINTER(C.c_uint64)), 24, C.byref(st)) == 0
+sym, stride = C.c_int(), C.c_uint64()
+assert lib.mgg_store_layout(st, C.byref(sym), C.byref(stride)) == 0
+want = {vmm!r} == "1"
+assert bool(sym.value) == want and ((stride.value >= 4000 * 24 * 4) if want else True), (sym.value, stride.value)
+lib.mgg_store_destroy(st); lib.mgg_ctx_destroy(ctx)
+g = mgg.gen_synthetic(mgg.POWERLAW, 3000, 18, 12)
+for fetch in ("fine", "halo"):
+    for dim, parts in ((16, 2), (40, 3), (16, 4)):
+        x = mgg.random_features(g.num_nodes, dim, seed=dim)
+        eng = mgg.Engine(g, parts, [0] * parts, mgg.make_gcn(dim, 16, 8), 16, 4, 4)
+        eng.set_remote_fetch(fetch)
+        ref = oracle.aggregate(g.row_ptr, g.col_idx, x)
+        for rep in range(2):
+            out = eng.aggregate(x, 1.0)
+            err = (np.abs(out - ref) / np.maximum(np.abs(ref).max(1, keepdims=True), 1e-6)).max()
+            assert err <= 1e-4, (fetch, dim, parts, err)
+        eng.close()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       timeout=600, env={**os.environ, "MGG_VMM": vmm, "MGG_HALO_FUSE": "1"})
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:] + r.stdout[-500:]
