@@ -679,12 +679,12 @@ __device__ __forceinline__ void agg_local_body(const AggArgs& a) {
 
 // Halo pull riding along a local pass (halo mode, fused): logical warp w of
 // the pass copies halo rows [w·H/W, (w+1)·H/W) (H distinct remote rows, W
-// logical warps) from their owners' shards into the halo. A group issues
-// one row's load before each of its partitions and stores it after, so the
-// remote read's latency is covered by the partition's local gathers, and the
-// remote traffic is spread evenly over the whole pass instead of running as
-// a separate kernel that (persistent, full occupancy) cannot co-run with it.
-// Rows left when a group runs out of partitions are copied two at a time.
+// logical warps) from their owners' shards into the halo, so the remote
+// traffic is spread evenly over the whole pass (and its latency covered by
+// the other warps' gathers) instead of running as a separate kernel that
+// (persistent, full occupancy) cannot co-run with the pass. PULL 2 (default):
+// after the warp's partitions, two rows at a time; PULL 1: one row issued
+// before each partition and stored after it, the rest two at a time.
 struct HaloPull {
   uint64_t r = 0, end = 0;
   uint64_t pol = 0;  // L2 evict-first: the copy must not push the local table out
@@ -742,7 +742,7 @@ struct HaloPull {
 // (the next UNR column ids prefetched),
 // so a warp keeps 32/VEC partitions' gathers outstanding at once instead of
 // one partition's predicated window.
-template <int VEC, bool RELU, int UNR, bool PULL = false>
+template <int VEC, bool RELU, int UNR, int PULL = 0>
 __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -770,7 +770,7 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
     HaloPull hp;
     if (PULL) hp.begin(a, w, grp, G, v, vlane);
     for (uint32_t i = l0 + grp; i < l1; i += G) {
-      const bool pull = PULL && hp.more();
+      const bool pull = PULL == 1 && hp.more();
       const uint64_t pr = hp.r;
       const float4 px = pull ? hp.load(a, pr) : f4zero();
       const int2 m = __ldg(a.lmeta + i);
@@ -816,7 +816,7 @@ __device__ __forceinline__ void agg_group_body(const AggArgs& a) {
 // FETCH: L2 fetch size of the gathered-row misses — 0 the default (the line:
 // 64-B rows also bring their neighbour row in, ~1.3-1.5x DRAM bytes on
 // random tables that do not fit L2), 64 = `L2::64B` (only the row's sectors).
-template <int VEC, bool RELU, int UNR, int FETCH = 0, bool PULL = false>
+template <int VEC, bool RELU, int UNR, int FETCH = 0, int PULL = 0>
 __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
   constexpr int G = 32 / VEC;
   const int lane = threadIdx.x & 31;
@@ -861,7 +861,7 @@ __device__ __forceinline__ void agg_group_hint_body(const AggArgs& a) {
     HaloPull hp;
     if (PULL) hp.begin(a, w, grp, G, v, vlane);
     for (uint32_t i = l0 + grp; i < l1; i += G) {
-      const bool pull = PULL && hp.more();
+      const bool pull = PULL == 1 && hp.more();
       const uint64_t pr = hp.r;
       const float4 px = pull ? hp.load(a, pr) : f4zero();
       const int2 m = __ldg(a.lmeta + i);
@@ -1612,7 +1612,7 @@ KernelFn pick_gpair(uint32_t v) {
   return agg_wide<RELU>;
 }
 
-template <int VEC, bool RELU, int UNR, bool PULL = false>
+template <int VEC, bool RELU, int UNR, int PULL = 0>
 __global__ void __launch_bounds__(512, 2) agg_group(AggArgs a) {
   agg_group_body<VEC, RELU, UNR, PULL>(a);
 }
@@ -1626,7 +1626,7 @@ KernelFn pick_group(uint32_t v) {
   if (v <= 32) return agg_group<32, RELU, UNR>;
   return agg_wide<RELU>;
 }
-template <int VEC, bool RELU, int UNR, int FETCH, bool PULL = false>
+template <int VEC, bool RELU, int UNR, int FETCH, int PULL = 0>
 __global__ void __launch_bounds__(512, 2) agg_group_hint(AggArgs a) {
   agg_group_hint_body<VEC, RELU, UNR, FETCH, PULL>(a);
 }
@@ -1977,28 +1977,37 @@ KernelFn pick_traced(uint32_t v) {
 // The group-form kernel with the halo pull compiled in (PULL = true) that
 // matches a local-pass kernel, or null when the form has none (warp window,
 // wide rows, A/B variants): then the pull kernel runs first.
-template <int VEC, bool RELU>
+// PULL 1: one halo row per partition, interleaved with the partition's
+// gathers; PULL 2: the partition loop untouched, the logical warp's halo rows
+// copied after its partitions (MGG_HALO_PULL_MODE, default 2).
+int pull_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("MGG_HALO_PULL_MODE");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  return m;
+}
+template <int VEC, bool RELU, int M>
 void add_pull_pairs(std::map<const void*, KernelFn>& m) {
-  m[reinterpret_cast<const void*>(agg_group<VEC, RELU, 8>)] = agg_group<VEC, RELU, 8, true>;
-  m[reinterpret_cast<const void*>(agg_group<VEC, RELU, 4>)] = agg_group<VEC, RELU, 4, true>;
+  m[reinterpret_cast<const void*>(agg_group<VEC, RELU, 8>)] = agg_group<VEC, RELU, 8, M>;
+  m[reinterpret_cast<const void*>(agg_group<VEC, RELU, 4>)] = agg_group<VEC, RELU, 4, M>;
+}
+template <int M>
+std::map<const void*, KernelFn> pull_pairs() {
+  std::map<const void*, KernelFn> m;
+  add_pull_pairs<1, false, M>(m), add_pull_pairs<2, false, M>(m), add_pull_pairs<4, false, M>(m);
+  add_pull_pairs<8, false, M>(m), add_pull_pairs<16, false, M>(m), add_pull_pairs<32, false, M>(m);
+  add_pull_pairs<1, true, M>(m), add_pull_pairs<2, true, M>(m), add_pull_pairs<4, true, M>(m);
+  add_pull_pairs<8, true, M>(m), add_pull_pairs<16, true, M>(m), add_pull_pairs<32, true, M>(m);
+  m[reinterpret_cast<const void*>(agg_group_hint<4, false, 8, 0>)] = agg_group_hint<4, false, 8, 0, M>;
+  m[reinterpret_cast<const void*>(agg_group_hint<4, true, 8, 0>)] = agg_group_hint<4, true, 8, 0, M>;
+  m[reinterpret_cast<const void*>(agg_group_hint<16, false, 8, 0>)] = agg_group_hint<16, false, 8, 0, M>;
+  m[reinterpret_cast<const void*>(agg_group_hint<16, true, 8, 0>)] = agg_group_hint<16, true, 8, 0, M>;
+  return m;
 }
 KernelFn pull_variant(KernelFn k) {
-  static const std::map<const void*, KernelFn> pairs = [] {
-    std::map<const void*, KernelFn> m;
-    add_pull_pairs<1, false>(m), add_pull_pairs<2, false>(m), add_pull_pairs<4, false>(m);
-    add_pull_pairs<8, false>(m), add_pull_pairs<16, false>(m), add_pull_pairs<32, false>(m);
-    add_pull_pairs<1, true>(m), add_pull_pairs<2, true>(m), add_pull_pairs<4, true>(m);
-    add_pull_pairs<8, true>(m), add_pull_pairs<16, true>(m), add_pull_pairs<32, true>(m);
-    m[reinterpret_cast<const void*>(agg_group_hint<4, false, 8, 0>)] =
-        agg_group_hint<4, false, 8, 0, true>;
-    m[reinterpret_cast<const void*>(agg_group_hint<4, true, 8, 0>)] =
-        agg_group_hint<4, true, 8, 0, true>;
-    m[reinterpret_cast<const void*>(agg_group_hint<16, false, 8, 0>)] =
-        agg_group_hint<16, false, 8, 0, true>;
-    m[reinterpret_cast<const void*>(agg_group_hint<16, true, 8, 0>)] =
-        agg_group_hint<16, true, 8, 0, true>;
-    return m;
-  }();
+  static const std::map<const void*, KernelFn> pairs =
+      pull_mode() == 1 ? pull_pairs<1>() : pull_pairs<2>();
   const auto it = pairs.find(reinterpret_cast<const void*>(k));
   return it == pairs.end() ? nullptr : it->second;
 }
