@@ -614,8 +614,8 @@ bool vmm_store_alloc(mgg_store* s) {
     const CUresult mr = v.map(at, s->vmm_size[p], 0, h, 0);
     v.release(h);  // the mapping keeps the memory alive
     drv(mr, "map");
+    s->shard[p] = reinterpret_cast<float*>(at);  // mapped: unmapped by vmm_store_free
     drv(v.access(at, s->vmm_size[p], acc.data(), acc.size()), "set access");
-    s->shard[p] = reinterpret_cast<float*>(at);
     s->owned[p] = 1;
     s->mem[p] = MGG_MEM_DEVICE;
     s->bytes[p] = std::max<size_t>(s->rows(p) * s->pitch * sizeof(float), 256);
@@ -657,7 +657,17 @@ int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_st
       s->dtable.assign(ctx->num_parts, nullptr);
       s->stage.assign(2 * ctx->num_parts, nullptr);
       s->stage_ev.assign(5 * ctx->num_parts, nullptr);
-      const bool symmetric = vmm_store_alloc(s);
+      bool symmetric = false;
+      try {
+        symmetric = vmm_store_alloc(s);
+      } catch (const Status&) {  // e.g. devices without peer mappings: per-shard allocations
+        vmm_store_free(s);
+        std::fill(s->shard.begin(), s->shard.end(), nullptr);
+        std::fill(s->owned.begin(), s->owned.end(), 0);
+        s->vmm_size.clear();
+        s->vmm_stride = 0;
+        cudaGetLastError();
+      }
       for (uint32_t p = 0; p < ctx->num_parts && !symmetric; ++p) {
         if (ctx->device[p] < 0) continue;
         MGG_CUDA(cudaSetDevice(ctx->device[p]));
