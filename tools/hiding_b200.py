@@ -68,11 +68,13 @@ def run_one(args):
     out = []
     for far, g in graphs(args):
         model = mgg.make_gcn(args.dim, 16, 8)
-        eng = mgg.Engine(g, 2, [0, 0], model, ps=args.ps, dist=args.dist, wpb=args.wpb)
+        n = args.parts
+        eng = mgg.Engine(g, n, [0] * n, model, ps=args.ps, dist=args.dist, wpb=args.wpb)
         eng.set_remote_fetch(args.fetch)
         eng.set_mapping(args.mapping, 0)
         if args.host:
-            eng.set_shard_memory(1, mgg.MEM_HOST_MAPPED)
+            for q in range(1, n):
+                eng.set_shard_memory(q, mgg.MEM_HOST_MAPPED)
         # phase 3 = the local partitions through the pipelined kernel itself;
         # phase 1 = the lean local-only kernel (reported beside it)
         t = {}
@@ -83,14 +85,14 @@ def run_one(args):
         eng.close()
         pipe, loc, rem = t[0], t[3], t[2]
         hid = max(0.0, rem + loc - pipe)
-        fp = mgg.build_flat_plan(g, 2, 0, args.ps, args.dist, args.wpb, args.dim)
+        fp = mgg.build_flat_plan(g, n, 0, args.ps, args.dist, args.wpb, args.dim)
         out.append({
             "pair_form": os.environ.get("MGG_AGG_PAIR", "default"),
             "pipe_depth": os.environ.get("MGG_AGG_PIPE_DEPTH", "8"),
             "sched": os.environ.get("MGG_AGG_SCHED", "4 (default)"),
             "dyn": os.environ.get("MGG_AGG_DYN", "default"), "kernels": kern,
             "graph": args.graph or "locality", "far": far, "mapping": args.mapping,
-            "fetch": args.fetch,
+            "fetch": args.fetch, "parts": args.parts,
             "nodes": int(g.num_nodes), "edges": int(g.num_edges), "dim": args.dim,
             "config": [args.ps, args.dist, args.wpb],
             "remote_shard": "host-mapped (PCIe)" if args.host else "device (same GPU)",
@@ -120,6 +122,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--mapping", type=int, default=0, help="0 interleaved, 1 segregated")
     ap.add_argument("--graph", default=None, help="a bench workload's graph instead of the sweep")
+    ap.add_argument("--parts", type=int, default=2,
+                    help="logical parts; every part but 0 is the (host-mapped) peer")
     ap.add_argument("--fetch", default="fine", choices=["fine", "halo"],
                     help="halo: deduplicated pull on the aux stream || local pass, then the "
                          "remote pass (phase 2 = pull + remote pass)")
