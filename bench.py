@@ -383,6 +383,26 @@ def roofline(nodes, edges, parts, rows, dim, launch_ms, gather_peak, traffic, ke
     return r
 
 
+def link_roofline(roof, nvl_bytes, launch_ms, hbm_peak_gbs, nvl_peak_gbs=900.0):
+    """SURVEY §8d for one GPU of an N-GPU run: T_roof = max(HBM_g / HBM peak,
+    NVL_g / NVLink peak). Adds the link term (the peer rows the rank's K1
+    pulls: halo = each distinct row once, fine = one row per remote edge) to
+    `roof` and makes it the reported bound when it is the larger one."""
+    t = launch_ms * 1e-3
+    gbs = nvl_bytes / t / 1e9
+    hbm_t = roof["algorithmic_bytes_per_launch"] / (hbm_peak_gbs * 1e9)
+    roof["nvlink"] = {"bytes_per_launch": int(nvl_bytes), "achieved": round(gbs, 1),
+                      "peak": nvl_peak_gbs, "frac": round(gbs / nvl_peak_gbs, 4),
+                      "peak_source": "NVLink 5 per direction (datasheet)"}
+    if nvl_bytes / (nvl_peak_gbs * 1e9) > hbm_t:
+        roof["hbm_bound"] = {k: roof[k] for k in ("achieved", "peak", "frac") if k in roof}
+        roof.update(bound="nvlink", achieved=round(gbs, 1), peak=nvl_peak_gbs,
+                    frac=round(gbs / nvl_peak_gbs, 4),
+                    peak_source="NVLink 5 per direction (datasheet); the HBM term is "
+                                "'hbm_bound'")
+    return roof
+
+
 def _traffic(args, parts, name=None):
     """DRAM bytes per K1 launch from the committed ncu capture of this config."""
     name = name or args.workload
@@ -573,6 +593,10 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
     roof = roofline(N, my_edges, my_parts, rows, w0, agg_ms_per_launch, gather_peak,
                     _traffic(args, n, name), kernels)
     roof["share_of_step"] = round(share, 4)
+    if world > 1 and st["remote_parts"] > 0:
+        pitch0 = (w0 + 3) // 4 * 4
+        nvl = (st["halo_rows"] if st.get("halo_rows", 0) else st["remote_edges"]) * pitch0 * 4
+        link_roofline(roof, nvl, agg_ms_per_launch, _peaks()[0])
 
     # remote-access hiding (mirrors the phase-separated
     # decomposition R:proj/src/sim.cpp:127-142, 530-569): K1 of the first

@@ -173,3 +173,18 @@ def test_gpus_n_without_torchrun_needs_n_devices():
         pytest.skip("two GPUs visible: the re-exec would run")
     assert out.returncode != 0
     assert "CUDA device(s) visible" in (out.stderr + out.stdout)
+
+
+def test_link_roofline_picks_the_binding_term():
+    # per GPU the roofline is the larger of the HBM and NVLink terms
+    import bench
+    base = {"algorithmic_bytes_per_launch": 650_000_000, "bound": "hbm", "achieved": 5000.0,
+            "peak": 6500.0, "frac": 0.77}
+    # 0.1 ms launch, 130 MB over the link: 130e6/900e9 = 0.144 ms > 650e6/6500e9 = 0.1 ms
+    r = bench.link_roofline(dict(base), 130_000_000, 0.2, 6500.0)
+    assert r["bound"] == "nvlink" and r["peak"] == 900.0
+    assert abs(r["achieved"] - 650.0) < 1e-6 and abs(r["frac"] - 650 / 900) < 1e-4
+    assert r["hbm_bound"]["frac"] == 0.77
+    # a small link term leaves the HBM bound in place
+    r = bench.link_roofline(dict(base), 10_000_000, 0.2, 6500.0)
+    assert r["bound"] == "hbm" and r["nvlink"]["bytes_per_launch"] == 10_000_000
