@@ -574,7 +574,11 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
     eng.synchronize()
     ops, nfw = eng.profile()
     eng.set_profiling(False)
-    kernels = eng.k1_kernels(my_part)  # K1 forms of the last layer's launch
+    # the first layer's K1 (the roofline's kernel): one launch on its stores,
+    # then the library names the kernels it ran (the profiled pass ended on
+    # the last layer's, which may differ — e.g. ReLU applied on load)
+    eng.time_aggregate(w0, 1, 0)
+    kernels = eng.k1_kernels(my_part)
     if world > 1:
         dist.barrier()
         total_ms = mdist.max_over_ranks(total_ms)
