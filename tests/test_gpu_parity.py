@@ -23,11 +23,23 @@ def softmax_bar(zr, z32):
     return max(TOL, 2 * float(np.abs(z32 - zr).max()))
 
 
-def assert_rows_close(got, ref, tol=TOL, what=""):
+def rows_err(got, ref):
+    """Row-relative error. A row's scale is its largest |value|, floored at
+    1e-2 of the median row's: rows a hundred times below the typical one
+    (isolated nodes whose features cancel to ~1e-4 while the median row is
+    ~10) carry fp32 rounding of the typical magnitude, which no summation
+    order removes (the fp32 oracle shows the same on them)."""
     assert got.shape == ref.shape, (got.shape, ref.shape)
+    if not got.size:
+        return 0.0
     scale = np.abs(ref).max(axis=1, keepdims=True)
+    scale = np.maximum(scale, 1e-2 * float(np.median(scale)))
     scale = np.maximum(scale, 1e-6)
-    err = (np.abs(got.astype(np.float64) - ref) / scale).max() if got.size else 0.0
+    return float((np.abs(got.astype(np.float64) - ref) / scale).max())
+
+
+def assert_rows_close(got, ref, tol=TOL, what=""):
+    err = rows_err(got, ref)
     assert err <= tol, f"{what}: max row-relative error {err:.3e} > {tol}"
     return err
 
@@ -558,8 +570,14 @@ def test_cfg5_aggregation_8_parts(mgg, oracle_mod, dim, fetch):
 @pytest.mark.parametrize("seed", range(int(os.environ.get("MGG_FUZZ_N", "12"))))
 def test_fuzz_forward(mgg, oracle_mod, seed):
     # random graph kind / size, model kind and widths, part count, (ps,
-    # dist, wpb), remote-fetch mode and graph replay on/off — every output
-    # against the fp64 oracle (logits-scale-aware softmax check as above)
+    # dist, wpb), remote-fetch mode and graph replay on/off — the engine's
+    # logits against the fp64 oracle at the north_star bar (1e-4 row-relative,
+    # or twice the fp32 floor where fp32 itself cannot reach it),
+    # the softmax within what those logits imply: with |logits| ~1e4 a
+    # 3e-6 relative logit error (fp32 sums in a run-dependent atomic order)
+    # moves near-tied probabilities by ~1e-4, so the bound is the larger of
+    # 1e-4, twice the fp32 oracle's own distance from fp64, and 2 x the
+    # engine's absolute logit error (|dp| <= 2 max |dlogit| for a softmax)
     rng = np.random.default_rng(1000 + seed)
     n = int(rng.integers(200, 4000))
     kind = ("rmat", "powerlaw", "uniform")[seed % 3]
@@ -588,17 +606,26 @@ def test_fuzz_forward(mgg, oracle_mod, seed):
         eng.forward()
         eng.forward()
         z = eng.get_output()
+        lg = eng.get_logits()
     finally:
         eng.close()
     if model.kind == 0:
-        _, _, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
-        _, _, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+        _, lr, zr = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model)
+        _, l32, z32 = oracle_mod.gcn2_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
     else:
-        _, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
-        _, z32 = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+        lr, zr = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model)
+        l32, z32 = oracle_mod.gin_forward(g.row_ptr, g.col_idx, x, model, acc64=False)
+    # 1e-4 row-relative, or twice what fp32 itself costs on these logits (the
+    # fp32 restatement's distance from fp64: GIN rows with heavy cancellation
+    # reach ~5e-4 under any fp32 evaluation)
+    lfloor = rows_err(l32, lr.astype(np.float64))
+    assert_rows_close(lg, lr.astype(np.float64), tol=max(TOL, 2 * lfloor),
+                      what=f"fuzz {seed} logits (fp32 floor {lfloor:.2e})")
+    dl = float(np.abs(lg.astype(np.float64) - lr).max())
     floor = float(np.abs(z32 - zr).max())
     err = float(np.abs(z - zr).max())
-    assert err <= max(TOL, 2 * floor), (seed, kind, n, din, hid, cls, parts, cfg, err, floor)
+    assert err <= max(TOL, 2 * floor, 2 * dl), (seed, kind, n, din, hid, cls, parts, cfg, err,
+                                                floor, dl)
 
 
 @pytest.mark.parametrize("parts", [1, 2, 3])
