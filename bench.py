@@ -39,6 +39,9 @@ It never loads the product: the graph comes from the reference library's own
 generator (oracle/_ref) or the oracle's C restatement of it, X and W from the
 numpy generators below (identical arrays, tests/test_bench.py).
 
+hiding  : (N=1) remote-latency hiding of the pipelined K1 against a slow peer
+            (host-mapped shard of a second logical part; slow_peer_hiding).
+
 Multi-GPU: torchrun, one process per GPU; part r = rank r's edge-balanced
 node range (Alg. 1); remote rows read in-kernel over NVLink from peer shards
 imported through CUDA IPC; no NCCL on the data path ("scaling": "strong").
@@ -111,6 +114,8 @@ def _args():
                          "rows in flight); default: the workload's tuned form")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-hiding", action="store_true",
+                    help="skip the slow-peer remote-latency hiding measurement (N=1)")
     a = ap.parse_args()
     tuned = WORKLOADS[a.workload][3]
     a.ps = a.ps or tuned[0]
@@ -702,6 +707,55 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
     }
 
 
+def locality_csr(n, avg, window, far, seed=0):
+    """CSR (row = target) whose neighbours lie within +-window of the target
+    except a `far` fraction drawn uniformly — tunes the remote-edge share of
+    the 1D split (tools/hiding_b200.py uses the same generator)."""
+    rng = np.random.default_rng(seed)
+    deg = np.maximum(rng.poisson(avg, n), 1).astype(np.int64)
+    rp = np.zeros(n + 1, np.uint64)
+    rp[1:] = np.cumsum(deg)
+    e = int(rp[-1])
+    tgt = np.repeat(np.arange(n, dtype=np.int64), deg)
+    near = np.clip(tgt + rng.integers(-window, window + 1, e), 0, n - 1)
+    col = np.where(rng.random(e) < far, rng.integers(0, n, e), near)
+    return rp, (np.sort(tgt * n + col) % n).astype(np.uint64)
+
+
+def slow_peer_hiding(mgg, far=0.002, n=2_000_000, dim=16, reps=5):
+    """Remote-latency hiding of the fine-grained pipelined K1 (SURVEY §8d,
+    R:PAPER.md:405-419) on one GPU: two logical parts, part 1's shards in
+    pinned host memory mapped into the device, so part 0's remote rows cross
+    PCIe with microsecond latency (a slower stand-in for an NVLink peer).
+    Part 0's K1 timed local-only (its local partitions through the same pair
+    kernel), remote-only and pipelined; hidden = (T_rem + T_loc - T_pipe) /
+    T_rem. tools/hiding_b200.py sweeps the remote share."""
+    rp, cl = locality_csr(n, 25.0, 64, far)
+    g = mgg.CsrGraph.from_csr(rp, cl)
+    eng = mgg.Engine(g, 2, [0, 0], mgg.make_gcn(dim, 16, 8), ps=16, dist=8, wpb=8)
+    try:
+        eng.set_remote_fetch("fine")
+        eng.set_shard_memory(1, mgg.MEM_HOST_MAPPED)
+        t = {ph: eng.time_aggregate_each(dim, reps, ph)[0] for ph in (3, 2, 0)}
+        kernels = eng.k1_kernels(0)
+        st = eng.stats()
+    finally:
+        eng.close()
+    loc, rem, pipe = t[3], t[2], t[0]
+    hid = max(0, rem + loc - pipe)
+    fp = mgg.build_flat_plan(g, 2, 0, 16, 8, 8, dim)
+    return {"method": "2 logical parts on this GPU, part 1 host-mapped (PCIe peer); part 0's K1 "
+                      "local-only / remote-only / pipelined, CUDA events, median of 5",
+            "graph": f"locality CSR {n} nodes, avg degree 25, far fraction {far}",
+            "remote_edge_fraction": round(fp.remote_cols_len / max(
+                fp.local_cols_len + fp.remote_cols_len, 1), 5),
+            "k1_local_only_ns": int(loc), "k1_remote_only_ns": int(rem),
+            "k1_pipelined_ns": int(pipe),
+            "hidden_remote_fraction": round(hid / max(rem, 1), 4),
+            "pipelined_vs_max_leg": round(pipe / max(loc, rem, 1), 4),
+            "kernel": ";".join(kernels), "remote_parts": int(st["remote_parts"])}
+
+
 def main():
     args = _args()
     if args.impl == "reference":
@@ -743,6 +797,12 @@ def main():
             secondary.append({k: r[k] for k in ("metric", "value", "ms_per_step", "config",
                                                  "roofline", "ops", "gpu_launches", "clocks")}
                              | {"unit": "GEdges/s", "steps": args.steps})
+    hiding = None
+    if rank == 0 and world == 1 and not args.no_hiding:
+        try:
+            hiding = slow_peer_hiding(mgg)
+        except Exception as ex:  # noqa: BLE001  (a box without mapped host memory)
+            hiding = {"error": str(ex)[:200]}
     if rank == 0:
         m = main_line
         line = {
@@ -754,7 +814,7 @@ def main():
             "cpu_baseline": m["cpu_baseline"], "e2e": m["e2e"],
             "gpu_launches": m["gpu_launches"], "overlap": m["overlap"], "link": m["link"],
             "clocks": m["clocks"],
-            "setup": m["setup"], "secondary": secondary,
+            "setup": m["setup"], "secondary": secondary, "hiding": hiding,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -188,3 +188,20 @@ def test_link_roofline_picks_the_binding_term():
     # a small link term leaves the HBM bound in place
     r = bench.link_roofline(dict(base), 10_000_000, 0.2, 6500.0)
     assert r["bound"] == "hbm" and r["nvlink"]["bytes_per_launch"] == 10_000_000
+
+
+def test_locality_csr_for_the_hiding_line():
+    # the slow-peer hiding measurement's graph: rows sorted, neighbours within
+    # the window except the `far` fraction
+    import numpy as np
+
+    import bench
+    rp, cl = bench.locality_csr(20000, 10.0, 8, 0.02, seed=3)
+    assert rp[0] == 0 and np.all(np.diff(rp.astype(np.int64)) >= 1) and int(rp[-1]) == len(cl)
+    assert cl.max() < 20000
+    tgt = np.repeat(np.arange(20000), np.diff(rp.astype(np.int64)))
+    far = np.abs(cl.astype(np.int64) - tgt) > 8
+    assert 0.01 < far.mean() < 0.03
+    for r in range(0, 20000, 997):  # rows sorted
+        row = cl[int(rp[r]):int(rp[r + 1])]
+        assert np.all(np.diff(row.astype(np.int64)) >= 0)
