@@ -246,7 +246,7 @@ __device__ __forceinline__ LbRange lb_range(const AggArgs& a) {
 // late; here warps take tickets as they go.
 // * A ticket g is a chunk of a.wchunk consecutive logical warps, dealt in a
 //   block-strided order: chunk = (g % kBlocks) * L + g / kBlocks with
-//   L = ceil(chunks / kBlocks). Consecutive tickets sweep kBlocks evenly
+//   L = ceil(chunks / kBlocks) (kBlocks = 512). Consecutive tickets sweep kBlocks evenly
 //   spaced positions of the warp range, so any contiguous region — the
 //   interleaved mapping puts every (local, remote) pair in the first
 //   logical warps when one kind is scarce — is spread over the whole launch:
@@ -263,7 +263,13 @@ __device__ __forceinline__ LbRange lb_range(const AggArgs& a) {
 // next launch on the plan (stream order makes that visible).
 constexpr uint32_t kShards = 16;
 constexpr uint32_t kShardStride = 32;  // u32 words between counters (128 B)
-constexpr uint32_t kBlocks = 32;
+// 512 positions (profiles/r02/dyn_schedule.md, kBlocks sweep): slow-peer
+// hidden remote 0.79-0.85 at 32 -> 0.92-0.95 at 512 (0.92-0.99 at 2048, with
+// a 2-3% slower local leg), same-device launch unchanged
+#ifndef MGG_KBLOCKS
+#define MGG_KBLOCKS 512
+#endif
+constexpr uint32_t kBlocks = MGG_KBLOCKS;
 
 // KINDS = 2 (agg_gsplit): every chunk is two items, its local and its remote
 // partitions, adjacent in the dealing order; run_warp(w, kind).
