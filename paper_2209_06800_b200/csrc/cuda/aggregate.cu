@@ -261,7 +261,7 @@ __device__ __forceinline__ LbRange lb_range(const AggArgs& a) {
 //   atomic round trip overlaps the chunk).
 // Each resident warp retires once; the last one resets the counters for the
 // next launch on the plan (stream order makes that visible).
-constexpr uint32_t kShards = 16;
+constexpr uint32_t kShards = MGG_KSHARDS;  // common.cuh
 constexpr uint32_t kShardStride = 32;  // u32 words between counters (128 B)
 // 512 positions (profiles/r02/dyn_schedule.md, kBlocks sweep): slow-peer
 // hidden remote 0.79-0.85 at 32 -> 0.92-0.95 at 512 (0.92-0.99 at 2048, with

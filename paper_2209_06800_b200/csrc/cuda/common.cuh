@@ -99,7 +99,10 @@ struct mgg_trace {
   unsigned long long* count = nullptr;
 };
 
-constexpr size_t kSchedBytes = 17 * 128;
+#ifndef MGG_KSHARDS
+#define MGG_KSHARDS 16  // pair-kernel ticket counters (aggregate.cu for_each_ticket)
+#endif
+constexpr size_t kSchedBytes = (MGG_KSHARDS + 1) * 128;
 
 struct mgg_dplan {
   mgg_ctx* ctx = nullptr;
