@@ -198,3 +198,72 @@ def test_restatement_vs_reference_library_fuzz():
         assert np.array_equal(oracle.split_points(rp, gpus), r.split(gpus))
         for mode in (0, 1):
             assert np.array_equal(oracle.placement(rp, gpus, mode), r.placement(gpus, mode))
+
+
+def _scipy_adj(rp, cl, n, self_loops):
+    import scipy.sparse as sp
+    rp = np.asarray(rp, np.int64)
+    cl = np.asarray(cl, np.int64)
+    a = sp.csr_matrix((np.ones(len(cl)), cl, rp), shape=(n, n))  # row = target, duplicates summed
+    return a + sp.identity(n, format="csr") if self_loops else a
+
+
+@pytest.mark.parametrize("norm", [0, 1])
+def test_gcn2_vs_independent_scipy_restatement(mgg, norm):
+    """The oracle's GCN-2L (R:PAPER.md:504-508: Z = softmax(Â·ReLU(Â·X·W1)·W2),
+    Â = A + I, optionally D^-1/2 (A+I) D^-1/2 with d = |N(v)| + 1) against an
+    independent fp64 restatement with scipy.sparse matrix products — two
+    implementations of the paper's formula agreeing to fp32 output rounding
+    (the layer arithmetic has no reference code to pin it, R:SPEC.md:121-124)."""
+    g = mgg.gen_rmat(3000, 40000, seed=11)
+    n = g.num_nodes
+    x = mgg.random_features(n, 20, seed=12)
+    model = mgg.make_gcn(20, 12, 7, seed=13)
+    w1 = model.w1[: 20 * 12].reshape(20, 12).astype(np.float64)
+    w2 = model.w1[20 * 12:].reshape(12, 7).astype(np.float64)
+    ahat = _scipy_adj(g.row_ptr, g.col_idx, n, True)
+    if norm:
+        d = np.diff(np.asarray(g.row_ptr, np.int64)).astype(np.float64) + 1.0
+        import scipy.sparse as sp
+        s = sp.diags(1.0 / np.sqrt(d))
+        ahat = s @ ahat @ s
+    h1 = np.maximum(ahat @ (x.astype(np.float64) @ w1), 0)
+    logits = ahat @ h1 @ w2
+    z = np.exp(logits - logits.max(axis=1, keepdims=True))
+    z /= z.sum(axis=1, keepdims=True)
+    _, lg, zo = oracle.gcn2_forward(g.row_ptr, g.col_idx, x, model, norm=norm)
+    scale = np.maximum(np.abs(logits).max(axis=1, keepdims=True), 1e-6)
+    assert (np.abs(lg - logits) / scale).max() < 2e-6
+    # the oracle's softmax reads its fp32 logits: |dp| <= 2 |dlogit| ~ 2 |l| 2^-24
+    assert np.abs(zo - z).max() < 2e-6 + 4 * np.abs(logits).max() * 2.0 ** -24
+
+
+def test_gin_vs_independent_scipy_restatement(mgg):
+    """The oracle's GIN (R:PAPER.md:511-517: h' = MLP((1+eps) h_v + Σ h_u),
+    MLP = Linear-ReLU-Linear, ReLU between layers, softmax head) against the
+    same independent scipy.sparse fp64 restatement."""
+    g = mgg.gen_synthetic(mgg.POWERLAW, 2500, 9.0, 5)
+    n = g.num_nodes
+    x = mgg.random_features(n, 18, seed=6)
+    model = mgg.make_gin(18, 10, 6, layers=3, seed=7, eps=0.3)
+    adj = _scipy_adj(g.row_ptr, g.col_idx, n, False)
+    dims = model.gin_dims()
+    h = x.astype(np.float64)
+    o1 = ob1 = o2 = ob2 = 0
+    for l in range(model.layers):
+        din, dout = dims[l], dims[l + 1]
+        w1 = model.w1[o1:o1 + din * 10].reshape(din, 10).astype(np.float64)
+        b1 = model.b1[ob1:ob1 + 10].astype(np.float64)
+        w2 = model.w2[o2:o2 + 10 * dout].reshape(10, dout).astype(np.float64)
+        b2 = model.b2[ob2:ob2 + dout].astype(np.float64)
+        o1, ob1, o2, ob2 = o1 + din * 10, ob1 + 10, o2 + 10 * dout, ob2 + dout
+        a = (1.0 + model.eps) * h + adj @ h
+        h = np.maximum(a @ w1 + b1, 0) @ w2 + b2
+        if l + 1 < model.layers:
+            h = np.maximum(h, 0)
+    z = np.exp(h - h.max(axis=1, keepdims=True))
+    z /= z.sum(axis=1, keepdims=True)
+    lg, zo = oracle.gin_forward(g.row_ptr, g.col_idx, x, model)
+    scale = np.maximum(np.abs(h).max(axis=1, keepdims=True), 1e-6)
+    assert (np.abs(lg - h) / scale).max() < 2e-6
+    assert np.abs(zo - z).max() < 2e-6 + 4 * np.abs(h).max() * 2.0 ** -24
