@@ -97,6 +97,14 @@ int mgg_store_info(const mgg_store* s, uint32_t* dim, uint32_t* pitch);
  * memory (MGG_VMM=0 disables it); stores of multi-process contexts are one
  * allocation per shard plus CUDA IPC imports (*symmetric = 0). */
 int mgg_store_layout(const mgg_store* s, int* symmetric, uint64_t* stride);
+/* Cross-process symmetric stores (opt-in, MGG_VMM_IPC=1; *symmetric = 2 from
+ * mgg_store_layout): every process reserves the same range layout, allocates
+ * its local shard with a POSIX-fd-exportable VMM handle, and maps each peer's
+ * shard at base + q * stride from the fd the peer exported (passed between
+ * processes by the caller, e.g. SCM_RIGHTS over a Unix socket). The fd
+ * returned by export is owned by the caller; import does not keep the fd. */
+int mgg_store_vmm_export(const mgg_store* s, uint32_t part, int* fd);
+int mgg_store_vmm_import(mgg_store* s, uint32_t part, int fd);
 /* Where a local part's shards live (stores created after the call):
  *  MGG_MEM_DEVICE (0)       cudaMalloc on the part's device (default);
  *  MGG_MEM_HOST_MAPPED (1)  pinned host memory mapped into the device: a slow
@@ -483,6 +491,13 @@ int mgg_engine_ipc_export(const mgg_engine* e, uint32_t part, void* blob,
                           size_t* len);
 int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob,
                           size_t len);
+/* Cross-process symmetric VMM stores (MGG_VMM_IPC=1, see mgg_store_vmm_export):
+ * *on = 1 when this engine's stores are fd-exportable VMM ranges; export
+ * writes one POSIX fd per store of local part `part` (caller-owned, count in
+ * *count; fds may be NULL to query), import maps a peer's from its fds. */
+int mgg_engine_vmm_ipc(const mgg_engine* e, int* on);
+int mgg_engine_vmm_export(const mgg_engine* e, uint32_t part, int* fds, size_t* count);
+int mgg_engine_vmm_import(mgg_engine* e, uint32_t part, const int* fds, size_t count);
 /* Remote fetch: 0 auto (halo when it moves >= 2x fewer bytes), 1 fine
  * (per-edge peer reads in K1, the paper's design), 2 halo (deduplicated
  * pull, then local reads). Re-plans. */

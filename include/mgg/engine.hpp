@@ -63,6 +63,12 @@ class Engine {
 
   std::vector<std::uint8_t> export_ipc(std::uint32_t part) const;
   void import_ipc(std::uint32_t part, const std::vector<std::uint8_t>& blob);
+  /// Cross-process symmetric VMM stores (MGG_VMM_IPC=1): true when this
+  /// engine's stores are fd-exportable VMM ranges; export returns one POSIX
+  /// fd per store (the K3 flags first, caller-owned), import maps a peer's.
+  bool vmm_ipc() const;
+  std::vector<int> export_vmm(std::uint32_t part) const;
+  void import_vmm(std::uint32_t part, const std::vector<int>& fds);
 
   void set_config(const KernelConfig& cfg);
   /// Ablation knobs of the reference's baselines (R:proj/src/sim.cpp:571-595):

@@ -81,6 +81,8 @@ _sig("mgg_store_create", I, vp, u64p, U32, PP)
 _sig("mgg_store_destroy", I, vp)
 _sig("mgg_store_info", I, vp, u32p, u32p)
 _sig("mgg_store_layout", I, vp, C.POINTER(C.c_int), u64p)
+_sig("mgg_store_vmm_export", I, vp, U32, C.POINTER(C.c_int))
+_sig("mgg_store_vmm_import", I, vp, U32, C.c_int)
 _sig("mgg_store_ipc_export", I, vp, U32, vp)
 _sig("mgg_store_ipc_import", I, vp, U32, vp)
 _sig("mgg_store_upload", I, vp, f32p, U64, U64, U32)
@@ -141,6 +143,9 @@ _sig("mgg_engine_create", I, vp, U32, i32p, U32, U32, U32, C.POINTER(ModelDesc),
 _sig("mgg_engine_destroy", I, vp)
 _sig("mgg_engine_ipc_export", I, vp, U32, vp, C.POINTER(SZ))
 _sig("mgg_engine_ipc_import", I, vp, U32, vp, SZ)
+_sig("mgg_engine_vmm_ipc", I, vp, C.POINTER(C.c_int))
+_sig("mgg_engine_vmm_export", I, vp, U32, C.POINTER(C.c_int), C.POINTER(SZ))
+_sig("mgg_engine_vmm_import", I, vp, U32, C.POINTER(C.c_int), SZ)
 _sig("mgg_engine_set_config", I, vp, U32, U32, U32)
 _sig("mgg_engine_set_mapping", I, vp, I, I)
 _sig("mgg_engine_set_remote_fetch", I, vp, I)

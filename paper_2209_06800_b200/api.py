@@ -420,6 +420,24 @@ class Engine:
         b = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
         check(lib.mgg_engine_ipc_import(self._h, part, b, len(blob)))
 
+    def vmm_ipc(self) -> bool:
+        """True when the stores are cross-process symmetric VMM ranges (MGG_VMM_IPC=1)."""
+        on = C.c_int(0)
+        check(lib.mgg_engine_vmm_ipc(self._h, C.byref(on)))
+        return bool(on.value)
+
+    def vmm_export(self, part: int) -> list[int]:
+        """One POSIX fd per store of local part `part` (caller closes them)."""
+        n = C.c_size_t(0)
+        check(lib.mgg_engine_vmm_export(self._h, part, None, C.byref(n)))
+        buf = (C.c_int * n.value)()
+        check(lib.mgg_engine_vmm_export(self._h, part, buf, C.byref(n)))
+        return list(buf)
+
+    def vmm_import(self, part: int, fds: list[int]) -> None:
+        buf = (C.c_int * len(fds))(*fds)
+        check(lib.mgg_engine_vmm_import(self._h, part, buf, len(fds)))
+
     def set_config(self, ps: int, dist: int, wpb: int) -> None:
         check(lib.mgg_engine_set_config(self._h, ps, dist, wpb))
 

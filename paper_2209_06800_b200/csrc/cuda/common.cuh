@@ -72,6 +72,11 @@ struct mgg_store {
   char* vmm_base = nullptr;
   uint64_t vmm_stride = 0;
   std::vector<size_t> vmm_size;
+  // cross-process symmetric stores (MGG_VMM_IPC=1): the local shard's VMM
+  // allocation handle (exported as a POSIX fd) and which slots are mapped
+  bool vmm_ipc = false;
+  std::vector<unsigned long long> vmm_handle;
+  std::vector<uint8_t> vmm_mapped;
   uint64_t rows(uint32_t p) const { return lb[p + 1] - lb[p]; }
 };
 

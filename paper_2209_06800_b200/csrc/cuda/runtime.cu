@@ -529,7 +529,9 @@ struct Vmm {
   decltype(&cuMemRelease) release = nullptr;
   decltype(&cuMemUnmap) unmap = nullptr;
   decltype(&cuMemAddressFree) vfree = nullptr;
-  bool ok = false;
+  decltype(&cuMemExportToShareableHandle) export_fd = nullptr;
+  decltype(&cuMemImportFromShareableHandle) import_fd = nullptr;
+  bool ok = false, fd_ok = false;
 };
 const Vmm& vmm() {
   static const Vmm v = [] {
@@ -547,6 +549,8 @@ const Vmm& vmm() {
            get("cuMemRelease", reinterpret_cast<void**>(&r.release)) &&
            get("cuMemUnmap", reinterpret_cast<void**>(&r.unmap)) &&
            get("cuMemAddressFree", reinterpret_cast<void**>(&r.vfree));
+    r.fd_ok = r.ok && get("cuMemExportToShareableHandle", reinterpret_cast<void**>(&r.export_fd)) &&
+              get("cuMemImportFromShareableHandle", reinterpret_cast<void**>(&r.import_fd));
     cudaGetLastError();
     return r;
   }();
@@ -560,6 +564,16 @@ bool vmm_wanted() {
   }();
   return m;
 }
+// MGG_VMM_IPC=1: one-process-per-GPU stores are symmetric VMM ranges too,
+// each rank's shard exported as a POSIX fd and mapped by its peers at the same
+// offset (mgg_store_vmm_export / _import); default: CUDA IPC handles.
+bool vmm_ipc_wanted() {
+  static const bool m = [] {
+    const char* e = std::getenv("MGG_VMM_IPC");
+    return e && std::atoi(e) != 0;
+  }();
+  return m;
+}
 void drv(CUresult r, const char* what) {
   if (r != CUDA_SUCCESS) throw Status{MGG_E_CUDA, std::string("VMM ") + what + " failed"};
 }
@@ -568,14 +582,17 @@ void drv(CUresult r, const char* what) {
 // parts local and in device memory); false when VMM is off or unavailable.
 bool vmm_store_alloc(mgg_store* s) {
   mgg_ctx* ctx = s->ctx;
-  if (!vmm_wanted() || !ctx->all_local || !vmm().ok) return false;
+  const bool cross = !ctx->all_local;  // parts in other processes: fd-exported shards
+  if (!vmm_wanted() || !vmm().ok) return false;
+  if (cross && !(vmm_ipc_wanted() && vmm().fd_ok)) return false;
   for (uint32_t p = 0; p < ctx->num_parts; ++p)
-    if (ctx->shard_mem[p] != MGG_MEM_DEVICE) return false;
+    if (ctx->device[p] >= 0 && ctx->shard_mem[p] != MGG_MEM_DEVICE) return false;
   const Vmm& v = vmm();
   size_t gran = 0;
   std::vector<int> devs;
   for (uint32_t p = 0; p < ctx->num_parts; ++p)
-    if (std::find(devs.begin(), devs.end(), ctx->device[p]) == devs.end())
+    if (ctx->device[p] >= 0 &&
+        std::find(devs.begin(), devs.end(), ctx->device[p]) == devs.end())
       devs.push_back(ctx->device[p]);
   for (int d : devs) {
     CUmemAllocationProp prop{};
@@ -603,17 +620,26 @@ bool vmm_store_alloc(mgg_store* s) {
     acc[i].location.id = devs[i];
     acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   }
+  s->vmm_ipc = cross;
+  s->vmm_handle.assign(ctx->num_parts, 0);
+  s->vmm_mapped.assign(ctx->num_parts, 0);
   for (uint32_t p = 0; p < ctx->num_parts; ++p) {
+    if (ctx->device[p] < 0) continue;  // a peer's slot: mapped by mgg_store_vmm_import
     CUmemAllocationProp prop{};
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = ctx->device[p];
+    if (cross) prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     CUmemGenericAllocationHandle h = 0;
     drv(v.create(&h, s->vmm_size[p], &prop, 0), "create");
     const CUdeviceptr at = base + p * stride;
     const CUresult mr = v.map(at, s->vmm_size[p], 0, h, 0);
-    v.release(h);  // the mapping keeps the memory alive
+    if (cross && mr == CUDA_SUCCESS)
+      s->vmm_handle[p] = h;  // kept for the fd export, released at destroy
+    else
+      v.release(h);  // the mapping keeps the memory alive
     drv(mr, "map");
+    s->vmm_mapped[p] = 1;
     s->shard[p] = reinterpret_cast<float*>(at);  // mapped: unmapped by vmm_store_free
     drv(v.access(at, s->vmm_size[p], acc.data(), acc.size()), "set access");
     s->owned[p] = 1;
@@ -630,11 +656,15 @@ void vmm_store_free(mgg_store* s) {
   if (!s->vmm_base) return;
   const Vmm& v = vmm();
   const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(s->vmm_base);
-  for (uint32_t p = 0; p < s->ctx->num_parts; ++p)
-    if (p < s->vmm_size.size() && s->vmm_size[p] && s->shard[p])
+  for (uint32_t p = 0; p < s->ctx->num_parts; ++p) {
+    if (p < s->vmm_mapped.size() && s->vmm_mapped[p])
       v.unmap(base + p * s->vmm_stride, s->vmm_size[p]);
+    if (p < s->vmm_handle.size() && s->vmm_handle[p]) v.release(s->vmm_handle[p]);
+  }
   v.vfree(base, s->vmm_stride * s->ctx->num_parts);
   s->vmm_base = nullptr;
+  s->vmm_mapped.clear();
+  s->vmm_handle.clear();
 }
 
 int mgg_store_create(mgg_ctx* ctx, const uint64_t* part_lb, uint32_t dim, mgg_store** out) {
@@ -775,9 +805,55 @@ int mgg_store_destroy(mgg_store* s) {
   return MGG_OK;
 }
 
+int mgg_store_vmm_export(const mgg_store* s, uint32_t part, int* fd) {
+  return guard([&] {
+    if (!s || !fd || part >= s->ctx->num_parts) throw Status{MGG_E_INPUT, "vmm_export: bad argument"};
+    if (!s->vmm_ipc || part >= s->vmm_handle.size() || !s->vmm_handle[part])
+      throw Status{MGG_E_CONFIG, "vmm_export: not a local shard of a cross-process VMM store"};
+    int out = -1;
+    drv(vmm().export_fd(&out, s->vmm_handle[part], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+        "export");
+    *fd = out;
+  });
+}
+
+int mgg_store_vmm_import(mgg_store* s, uint32_t part, int fd) {
+  return guard([&] {
+    if (!s || part >= s->ctx->num_parts) throw Status{MGG_E_INPUT, "vmm_import: bad argument"};
+    mgg_ctx* ctx = s->ctx;
+    if (!s->vmm_ipc) throw Status{MGG_E_CONFIG, "vmm_import: not a cross-process VMM store"};
+    if (ctx->device[part] >= 0) throw Status{MGG_E_INPUT, "vmm_import: part is local"};
+    if (s->vmm_mapped[part]) throw Status{MGG_E_INPUT, "vmm_import: slot already mapped"};
+    const Vmm& v = vmm();
+    CUmemGenericAllocationHandle h = 0;
+    drv(v.import_fd(&h, reinterpret_cast<void*>(static_cast<intptr_t>(fd)),
+                    CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+        "import");
+    const CUdeviceptr at = reinterpret_cast<CUdeviceptr>(s->vmm_base) + part * s->vmm_stride;
+    const CUresult mr = v.map(at, s->vmm_size[part], 0, h, 0);
+    v.release(h);
+    drv(mr, "map (import)");
+    s->vmm_mapped[part] = 1;
+    s->shard[part] = reinterpret_cast<float*>(at);
+    std::vector<CUmemAccessDesc> acc;
+    for (uint32_t p = 0; p < ctx->num_parts; ++p)
+      if (ctx->device[p] >= 0) {
+        CUmemAccessDesc d{};
+        d.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        d.location.id = ctx->device[p];
+        d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        bool dup = false;
+        for (auto& x : acc) dup |= x.location.id == d.location.id;
+        if (!dup) acc.push_back(d);
+      }
+    drv(v.access(at, s->vmm_size[part], acc.data(), acc.size()), "set access (import)");
+    refresh_tables(s);
+  });
+}
+
 int mgg_store_layout(const mgg_store* s, int* symmetric, uint64_t* stride) {
   if (!s) return MGG_E_INPUT;
-  if (symmetric) *symmetric = s->vmm_base ? 1 : 0;
+  if (symmetric) *symmetric = s->vmm_base ? (s->vmm_ipc ? 2 : 1) : 0;
   if (stride) *stride = s->vmm_stride;
   return MGG_OK;
 }

@@ -444,6 +444,25 @@ int mgg_engine_ipc_import(mgg_engine* e, uint32_t part, const void* blob, size_t
   });
 }
 
+int mgg_engine_vmm_ipc(const mgg_engine* e, int* on) {
+  return guard([&] { *on = e->e->vmm_ipc() ? 1 : 0; });
+}
+
+int mgg_engine_vmm_export(const mgg_engine* e, uint32_t part, int* fds, size_t* count) {
+  return guard([&] {
+    const auto v = e->e->export_vmm(part);
+    if (fds) {
+      if (*count < v.size()) throw InputError("engine_vmm_export: buffer too small");
+      std::memcpy(fds, v.data(), v.size() * sizeof(int));
+    }
+    *count = v.size();
+  });
+}
+
+int mgg_engine_vmm_import(mgg_engine* e, uint32_t part, const int* fds, size_t count) {
+  return guard([&] { e->e->import_vmm(part, std::vector<int>(fds, fds + count)); });
+}
+
 int mgg_engine_set_config(mgg_engine* e, uint32_t ps, uint32_t dist, uint32_t wpb) {
   return guard([&] { e->e->set_config(KernelConfig{ps, dist, wpb}); });
 }

@@ -354,6 +354,32 @@ void Engine::import_ipc(std::uint32_t part, const std::vector<std::uint8_t>& blo
     ok(mgg_store_ipc_import(stores_[i], part, blob.data() + 64 * (i + 1)));
 }
 
+bool Engine::vmm_ipc() const {
+  int sym = 0;
+  ok(mgg_store_layout(flags_, &sym, nullptr));
+  return sym == 2;
+}
+
+std::vector<int> Engine::export_vmm(std::uint32_t part) const {
+  std::vector<int> fds;
+  auto put = [&](const mgg_store* s) {
+    int fd = -1;
+    ok(mgg_store_vmm_export(s, part, &fd));
+    fds.push_back(fd);
+  };
+  put(flags_);
+  for (auto* s : stores_) put(s);
+  return fds;
+}
+
+void Engine::import_vmm(std::uint32_t part, const std::vector<int>& fds) {
+  if (fds.size() != stores_.size() + 1)
+    throw InputError("engine: VMM fd list does not match this engine's stores");
+  ok(mgg_store_vmm_import(flags_, part, fds[0]));
+  for (std::size_t i = 0; i < stores_.size(); ++i)
+    ok(mgg_store_vmm_import(stores_[i], part, fds[i + 1]));
+}
+
 void Engine::run(const Op& op) {
   if (op.kind == OpKind::barrier) {
     ok(mgg_barrier(ctx_, flags_));

@@ -26,8 +26,18 @@ def part_devices(world: int, rank: int, local_rank: int) -> list[int]:
 
 
 def exchange_ipc(engine, rank: int, world: int, group=None) -> None:
-    """All-gather every rank's shard handles and import the peers'."""
+    """Make every peer's shards visible to this rank: CUDA IPC handles
+    all-gathered over the process group (default), or — for cross-process
+    symmetric VMM stores (MGG_VMM_IPC=1) — POSIX fds passed over Unix sockets
+    (exchange_vmm_fds)."""
     import torch.distributed as dist
+    modes = [None] * world
+    dist.all_gather_object(modes, engine.vmm_ipc(), group=group)
+    if len(set(modes)) != 1:
+        raise api.ConfigError(f"ranks disagree on the store layout (VMM-IPC per rank: {modes})")
+    if modes[0]:
+        exchange_vmm_fds(engine, rank, world, group)
+        return
     blobs = [None] * world
     dist.all_gather_object(blobs, engine.ipc_export(rank), group=group)
     for p in range(world):
@@ -61,3 +71,57 @@ def rank_plan_summary(g, world: int, rank: int, ps: int, dist_: int, wpb: int, d
             "local_parts": fp.n_local, "remote_parts": fp.n_remote,
             "warps": fp.num_warps, "owners": sorted(set(
                 (fp.cols(1) >> np.uint32(28)).tolist())) if fp.remote_cols_len else []}
+
+
+def exchange_vmm_fds(engine, rank: int, world: int, group=None) -> None:
+    """Every rank serves the POSIX fds of its VMM shards (SCM_RIGHTS over an
+    abstract-namespace Unix socket) and maps every peer's at the peer's slot
+    of its own symmetric ranges (mgg_engine_vmm_import)."""
+    import secrets
+    import socket
+    import threading
+
+    import torch.distributed as dist
+    tok = [secrets.token_hex(8) if rank == 0 else None]
+    dist.broadcast_object_list(tok, src=0, group=group)
+    name = lambda r: f"\0mgg-vmm-{tok[0]}-{r}"  # noqa: E731
+    mine = engine.vmm_export(rank)
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(name(rank))
+    srv.listen(world)
+    err = []
+
+    def serve():
+        try:
+            for _ in range(world - 1):
+                c, _ = srv.accept()
+                with c:
+                    socket.send_fds(c, [rank.to_bytes(4, "little")], mine)
+        except Exception as ex:  # noqa: BLE001
+            err.append(ex)
+
+    th = threading.Thread(target=serve, daemon=True)
+    th.start()
+    dist.barrier(group=group)
+    try:
+        for q in range(world):
+            if q == rank:
+                continue
+            with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+                c.connect(name(q))
+                msg, fds, _, _ = socket.recv_fds(c, 4, len(mine))
+                if len(fds) != len(mine) or int.from_bytes(msg, "little") != q:
+                    raise api.IntegrityError(f"rank {rank}: bad fd message from rank {q}")
+                try:
+                    engine.vmm_import(q, fds)
+                finally:
+                    for fd in fds:
+                        os.close(fd)
+        th.join(timeout=120)
+        if err:
+            raise err[0]
+    finally:
+        srv.close()
+        for fd in mine:
+            os.close(fd)
+    dist.barrier(group=group)

@@ -20,9 +20,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, fetch="auto", kind="gcn"):
+def _worker(rank, world, port, q, fetch="auto", kind="gcn", vmm=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0")
+    if vmm:  # cross-process symmetric VMM stores, fds over Unix sockets
+        os.environ["MGG_VMM_IPC"] = "1"
     try:
         import torch.distributed as dist
 
@@ -40,6 +42,7 @@ def _worker(rank, world, port, q, fetch="auto", kind="gcn"):
                          wpb=4)
         if fetch != "auto":
             eng.set_remote_fetch(fetch)  # before the IPC exchange: halo buffers are per part
+        assert eng.vmm_ipc() == vmm, "store layout does not match MGG_VMM_IPC"
         mdist.exchange_ipc(eng, rank, world)
         dist.barrier()
         z = np.zeros((g.num_nodes, 24), np.float32)
@@ -67,12 +70,12 @@ def _worker(rank, world, port, q, fetch="auto", kind="gcn"):
         q.put((rank, None, None, traceback.format_exc()))
 
 
-def _run_pair(fetch, kind):
+def _run_pair(fetch, kind, vmm=False):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fetch, kind))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fetch, kind, vmm))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -82,11 +85,15 @@ def _run_pair(fetch, kind):
     return res
 
 
-@pytest.mark.parametrize("fetch,kind", [("auto", "gcn"), ("fine", "gcn"), ("halo", "gin")])
-def test_two_processes_ipc_forward(fetch, kind):
+@pytest.mark.parametrize("fetch,kind,vmm", [("auto", "gcn", False), ("fine", "gcn", False),
+                                            ("halo", "gin", False), ("fine", "gcn", True),
+                                            ("halo", "gin", True)])
+def test_two_processes_ipc_forward(fetch, kind, vmm):
+    # vmm: the stores are cross-process symmetric VMM ranges (MGG_VMM_IPC=1),
+    # each rank's shard mapped by its peer from a POSIX fd (SCM_RIGHTS)
     import paper_2209_06800_b200 as mgg
     assert mgg.cuda_available()
-    res = _run_pair(fetch, kind)
+    res = _run_pair(fetch, kind, vmm)
     for rank, err, remote, tb in res:
         assert tb is None, tb
         assert remote > 0, "no remote edges: the peer path was not exercised"
