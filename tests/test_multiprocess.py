@@ -19,10 +19,13 @@ def _free_port():
 
 
 class FakeEngine:
-    """Stands in for Engine's IPC surface (no GPU on this box)."""
+    """Stands in for Engine's IPC surface (no GPU on this box). With vmm=True
+    it plays a cross-process VMM store: its 'shards' are temp files whose fds
+    travel over the Unix-socket exchange (dist.exchange_vmm_fds)."""
 
-    def __init__(self, rank):
+    def __init__(self, rank, vmm=False):
         self.rank = rank
+        self.vmm = vmm
         self.imported = {}
 
     def ipc_export(self, part):
@@ -32,8 +35,26 @@ class FakeEngine:
     def ipc_import(self, part, blob):
         self.imported[part] = blob
 
+    def vmm_ipc(self):
+        return self.vmm
 
-def _worker(rank, world, port, q):
+    def vmm_export(self, part):
+        import tempfile
+        assert part == self.rank
+        fds = []
+        for i in range(3):
+            fd, path = tempfile.mkstemp()
+            os.write(fd, bytes([part]) * (i + 1) * 64)
+            os.unlink(path)
+            fds.append(fd)
+        return fds
+
+    def vmm_import(self, part, fds):
+        # the received fds are new descriptors of the peer's open files
+        self.imported[part] = b"".join(os.pread(fd, 1024, 0) for fd in fds)
+
+
+def _worker(rank, world, port, q, vmm=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     try:
@@ -48,10 +69,11 @@ def _worker(rank, world, port, q):
         summ = mdist.rank_plan_summary(g, world, rank, 16, 2, 4, 16)
         allsum = [None] * world
         dist.all_gather_object(allsum, (summ, int(g.num_edges), int(g.col_idx.sum())))
-        eng = FakeEngine(rank)
+        eng = FakeEngine(rank, vmm)
         mdist.exchange_ipc(eng, rank, world)
         assert sorted(eng.imported) == [p for p in range(world) if p != rank]
-        assert all(b == bytes([p]) * 192 for p, b in eng.imported.items())
+        want = (lambda p: bytes([p]) * 384) if vmm else (lambda p: bytes([p]) * 192)
+        assert all(b == want(p) for p, b in eng.imported.items()), eng.imported
         m = mdist.max_over_ranks(float(rank) * 1.5)
         tot = mdist.sum_over_ranks(float(rank + 1))  # bench's link bytes over ranks
         assert tot == world * (world + 1) / 2
@@ -62,12 +84,13 @@ def _worker(rank, world, port, q):
         q.put((rank, None, None, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_world_orchestration(world):
+@pytest.mark.parametrize("world,vmm", [(2, False), (3, False), (2, True), (3, True)])
+def test_world_orchestration(world, vmm):
+    # vmm: the cross-process VMM fd exchange (SCM_RIGHTS over Unix sockets)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, vmm)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
