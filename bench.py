@@ -660,7 +660,7 @@ def measure(name, args, mgg, lib, mdist, world, rank, local_rank, dist, full=Tru
         sync_s = time.perf_counter() - t0
         if world > 1:
             dist.barrier()
-        k2 = max(5, args.steps)
+        k2 = int(os.environ.get("MGG_E2E_STEPS", max(5, args.steps)))
         t0 = time.perf_counter()
         tickets = [eng.submit_host(xs[i % 2], zs[i % 2]) for i in range(k2)]
         eng.wait(tickets[-1])
