@@ -920,3 +920,21 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=600, env={**os.environ, "MGG_VMM": vmm, "MGG_HALO_FUSE": "1"})
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:] + r.stdout[-500:]
+
+
+@pytest.mark.parametrize("fetch", ["fine", "halo"])
+def test_sixteen_parts_with_empty_parts(mgg, oracle_mod, fetch):
+    # the maximum part count (16 owners in the packed column ids) on a graph
+    # so small that Alg. 1 leaves trailing parts empty: symmetric VMM store
+    # slots of 0 rows, plans without partitions, both fetch modes
+    g = mgg.gen_rmat(40, 300, seed=2)
+    x = mgg.random_features(g.num_nodes, 12, seed=3)
+    eng = mgg.Engine(g, 16, [0] * 16, mgg.make_gcn(12, 8, 4), 4, 2, 2)
+    try:
+        eng.set_remote_fetch(fetch)
+        for _ in range(2):
+            out = eng.aggregate(x, 1.0)
+            assert_rows_close(out, oracle_mod.aggregate(g.row_ptr, g.col_idx, x),
+                              what=f"16 parts {fetch}")
+    finally:
+        eng.close()
